@@ -1,0 +1,157 @@
+// Shared device helpers for libbass (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#define BASS_DEV __device__ __forceinline__
+
+namespace bass {
+
+constexpr int kWarp = 32;
+
+// element access in either storage dtype; all math is fp32 (or fp64 for sampling)
+BASS_DEV float ld(const float* p, int64_t i) { return p[i]; }
+BASS_DEV float ld(const __nv_bfloat16* p, int64_t i) { return __bfloat162float(p[i]); }
+BASS_DEV void st(float* p, int64_t i, float v) { p[i] = v; }
+BASS_DEV void st(__nv_bfloat16* p, int64_t i, float v) { p[i] = __float2bfloat16_rn(v); }
+
+template <typename T> BASS_DEV T cvt(float v);
+template <> BASS_DEV float cvt<float>(float v) { return v; }
+template <> BASS_DEV __nv_bfloat16 cvt<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+BASS_DEV float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+BASS_DEV double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+BASS_DEV float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// orderable key of a float: larger float -> larger key (NaN-free input)
+BASS_DEV uint32_t fkey(float x) {
+    uint32_t u = __float_as_uint(x);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// (value, index) argmax with first-index tie break (np.argmax semantics)
+struct ArgMax {
+    float v;
+    int i;
+};
+BASS_DEV ArgMax better(ArgMax a, ArgMax b) {
+    if (b.v > a.v || (b.v == a.v && b.i < a.i)) return b;
+    return a;
+}
+BASS_DEV ArgMax warp_argmax(ArgMax a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ArgMax b{__shfl_xor_sync(0xffffffffu, a.v, o), __shfl_xor_sync(0xffffffffu, a.i, o)};
+        a = better(a, b);
+    }
+    return a;
+}
+
+// Deterministic block reductions (fixed tree; identical result every launch).
+// `scratch` must hold blockDim.x/32 elements.
+template <typename T>
+BASS_DEV T block_sum(T v, T* scratch) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) scratch[w] = v;
+    __syncthreads();
+    T r = 0;
+    if (w == 0) {
+        r = lane < nw ? scratch[lane] : T(0);
+        r = warp_sum(r);
+        if (lane == 0) scratch[0] = r;
+    }
+    __syncthreads();
+    r = scratch[0];
+    __syncthreads();
+    return r;
+}
+
+BASS_DEV float block_max(float v, float* scratch) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_max(v);
+    __syncthreads();
+    if (lane == 0) scratch[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        float r = lane < nw ? scratch[lane] : -INFINITY;
+        r = warp_max(r);
+        if (lane == 0) scratch[0] = r;
+    }
+    __syncthreads();
+    float r = scratch[0];
+    __syncthreads();
+    return r;
+}
+
+BASS_DEV ArgMax block_argmax(ArgMax a, float* sv, int* si) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    a = warp_argmax(a);
+    __syncthreads();
+    if (lane == 0) { sv[w] = a.v; si[w] = a.i; }
+    __syncthreads();
+    if (w == 0) {
+        ArgMax r{-INFINITY, 0x7fffffff};
+        if (lane < nw) r = ArgMax{sv[lane], si[lane]};
+        r = warp_argmax(r);
+        if (lane == 0) { sv[0] = r.v; si[0] = r.i; }
+    }
+    __syncthreads();
+    ArgMax r{sv[0], si[0]};
+    __syncthreads();
+    return r;
+}
+
+// Exclusive block scan of one value per thread (fixed order).  `scratch`
+// holds 33 elements.  Returns the exclusive prefix; *total = sum.
+template <typename T>
+BASS_DEV T block_exclusive_scan(T v, T* scratch, T* total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    T incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T n = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += n;
+    }
+    T excl = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) excl = T(0);
+    __syncthreads();
+    if (lane == 31) scratch[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        T s = lane < nw ? scratch[lane] : T(0);
+        T si = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            T n = __shfl_up_sync(0xffffffffu, si, o);
+            if (lane >= o) si += n;
+        }
+        T se = __shfl_up_sync(0xffffffffu, si, 1);
+        if (lane == 0) se = T(0);
+        if (lane < nw) scratch[lane] = se;       // exclusive warp offsets
+        if (lane == nw - 1) scratch[32] = si;    // total
+    }
+    __syncthreads();
+    T off = scratch[w];
+    T tot = scratch[32];
+    __syncthreads();
+    *total = tot;
+    return off + excl;
+}
+
+}  // namespace bass

@@ -1,0 +1,515 @@
+// Device-computed decode loops: batched speculative decoding
+// (ref:engine.py:200-385) and regular decoding (ref:engine.py:120-197).
+//
+// The host keeps only bookkeeping (committed tokens, cache lengths, the
+// Algorithm-1 state); every forward, every draft pick (greedy or sampled),
+// the verify accept/resample pass, the bonus token, EOS/length finalize and
+// the logprobs run on the GPU.  One device->host read per step returns the
+// per-slot outcome (accepted count, emitted tokens, logprobs, finish flag).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "runtime.h"
+#include "sampling_kernels.cuh"
+
+using namespace bass;
+
+struct bass_engine {
+    bass_model* main = nullptr;
+    bass_model* draft = nullptr;
+    bass_kv* kv_main = nullptr;
+    bass_kv* kv_draft = nullptr;
+    int n_slots = 0, cap = 0;
+    int strategy = BASS_RAGGED;
+    static constexpr int kPstride = kMaxEmit;
+    int32_t* proposals = nullptr;     // [n_slots][kPstride]
+    DevBuf vlog, dlog, vamax, vlse, accf, corr, bonus, scratch, slotbuf, stepbuf, align_tok;
+    SlotStep* step_host = nullptr;    // pinned
+    int32_t* small_host = nullptr;    // pinned staging for tiny per-step arrays
+};
+
+namespace {
+
+using clk = std::chrono::steady_clock;
+
+double secs(clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); }
+
+template <typename F>
+int guarded_e(bass_engine* e, F&& f) {
+    bass_ctx* c = e ? e->main->ctx : nullptr;
+    try {
+        f();
+        return BASS_OK;
+    } catch (const Error& x) {
+        if (c) c->err = x.what();
+        return x.code;
+    } catch (const std::exception& x) {
+        if (c) c->err = x.what();
+        return BASS_ERR_STATE;
+    }
+}
+
+void launched(bass_ctx* c) {
+    c->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Error(BASS_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+void up(bass_ctx* c, void* dev, const void* src, size_t bytes) {
+    void* h = c->staging.take(bytes);
+    if (!h) {
+        c->sync();
+        h = c->staging.take(bytes);
+        if (!h) throw Error(BASS_ERR_MEMORY, "staging arena too small");
+    }
+    std::memcpy(h, src, bytes);
+    BASS_CUDA(cudaMemcpyAsync(dev, h, bytes, cudaMemcpyHostToDevice, c->stream));
+}
+
+// Algorithm 1 (ref:draft_control.py:49-69)
+struct Controller {
+    int fixed, l, s, incre, mod, limit;
+    int length() const { return fixed ? fixed : l; }
+    int max_length() const { return fixed ? fixed : limit; }
+    void observe(const std::vector<int>& acc) {
+        if (fixed || acc.empty()) return;
+        int mx = 0;
+        for (int a : acc) mx = std::max(mx, a);
+        if (mx == l) {
+            l = std::min(l + incre, limit);
+            s = 0;
+        } else {
+            int ln = l - (l + mod - 1) / mod - s;
+            l = std::max(std::max(1, mx), ln);
+            s = 1;
+        }
+    }
+};
+
+struct Request {
+    int b;
+    std::vector<std::vector<int32_t>> prompts;
+    std::vector<int64_t> sid;
+};
+
+Request parse(const bass_gen_request* r, int V) {
+    Request q;
+    BASS_REQUIRE(r->batch >= 1, "batch size must be >= 1");
+    BASS_REQUIRE(r->max_new_tokens >= 1, "max_new_tokens must be >= 1");
+    q.b = r->batch;
+    for (int i = 0; i < r->batch; ++i) {
+        const int a = r->prompt_offsets[i], z = r->prompt_offsets[i + 1];
+        BASS_REQUIRE(z > a, "every prompt needs at least one token");
+        q.prompts.emplace_back(r->prompt_tokens + a, r->prompt_tokens + z);
+        for (int t : q.prompts.back()) BASS_REQUIRE(t >= 0 && t < V, "token id outside vocab");
+        q.sid.push_back(r->sequence_ids ? r->sequence_ids[i] : i);
+        BASS_REQUIRE(q.sid.back() >= 0 && q.sid.back() < (int64_t(1) << 31), "sequence ids must be in [0, 2^31)");
+    }
+    BASS_REQUIRE(r->top_p > 0.0 && r->top_p <= 1.0, "top_p must be in (0, 1]");
+    BASS_REQUIRE(r->temperature >= 0.0, "temperature must be >= 0");
+    return q;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bass_engine_create(bass_model* mm, bass_kv* mkv, bass_model* dm, bass_kv* dkv, bass_engine** out) {
+    *out = nullptr;
+    bass_engine tmp;
+    tmp.main = mm;
+    return guarded_e(&tmp, [&] {
+        BASS_REQUIRE(dm == nullptr || dm->ctx == mm->ctx, "main and draft must share a context");
+        BASS_REQUIRE(mkv && mkv->m == mm, "main cache must belong to the main model");
+        BASS_REQUIRE(dm == nullptr || (dkv && dkv->m == dm), "draft cache must belong to the draft model");
+        bass_engine* e = new bass_engine();
+        e->main = mm;
+        e->draft = dm;
+        e->kv_main = mkv;
+        e->kv_draft = dkv;
+        e->n_slots = dkv ? std::min(mkv->n_slots, dkv->n_slots) : mkv->n_slots;
+        e->cap = dkv ? std::min(mkv->cap, dkv->cap) : mkv->cap;
+        const int n_slots = std::max(mkv->n_slots, dkv ? dkv->n_slots : 0);
+        BASS_CUDA(cudaMalloc((void**)&e->proposals, (size_t)n_slots * bass_engine::kPstride * 4));
+        BASS_CUDA(cudaMallocHost((void**)&e->step_host, (size_t)n_slots * sizeof(SlotStep)));
+        BASS_CUDA(cudaMallocHost((void**)&e->small_host, (size_t)n_slots * 64 * 4));
+        *out = e;
+    });
+}
+
+int bass_engine_destroy(bass_engine* e) {
+    if (!e) return BASS_OK;
+    cudaStreamSynchronize(e->main->ctx->stream);
+    cudaFree(e->proposals);
+    cudaFreeHost(e->step_host);
+    cudaFreeHost(e->small_host);
+    for (DevBuf* b : {&e->vlog, &e->dlog, &e->vamax, &e->vlse, &e->accf, &e->corr, &e->bonus, &e->scratch,
+                      &e->slotbuf, &e->stepbuf, &e->align_tok})
+        b->release();
+    delete e;
+    return BASS_OK;
+}
+
+int bass_engine_set_strategy(bass_engine* e, int strategy) {
+    return guarded_e(e, [&] {
+        BASS_REQUIRE(strategy >= BASS_PAD && strategy <= BASS_RAGGED, "unknown strategy");
+        e->strategy = strategy;
+    });
+}
+
+// ------------------------------------------------------------------ spec
+int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_result* res) {
+    return guarded_e(e, [&] {
+        BASS_REQUIRE(e->draft != nullptr, "speculative decoding needs a draft model");
+        bass_model& M = *e->main;
+        bass_model& D = *e->draft;
+        bass_ctx* c = M.ctx;
+        cudaStream_t st = c->stream;
+        const int V = M.g.vocab_size;
+        BASS_REQUIRE(D.g.vocab_size == V, "vocab mismatch: main " + std::to_string(V) + " vs draft " +
+                                              std::to_string(D.g.vocab_size));
+        Request q = parse(r, V);
+        const int b = q.b;
+        BASS_REQUIRE(b <= e->n_slots, "batch exceeds engine slots");
+        Controller ctl{r->ctl_fixed, r->l0, r->s0, r->incre, r->mod, r->limit};
+        if (!r->ctl_fixed) {
+            BASS_REQUIRE(r->l0 >= 1 && r->l0 <= r->limit, "l0 must be in [1, limit]");
+            BASS_REQUIRE(r->s0 == 0 || r->s0 == 1, "s must be 0 or 1");
+            BASS_REQUIRE(r->incre >= 0 && r->mod >= 1 && r->limit >= 1, "incre >= 0, mod >= 1, limit >= 1 required");
+        }
+        const int limit = ctl.max_length();
+        BASS_REQUIRE(limit >= 1 && limit < kMaxEmit, "draft limit must be in [1, 63]");
+        const int max_seq = std::min(M.g.max_seq_len, D.g.max_seq_len);
+        for (auto& p : q.prompts)
+            BASS_REQUIRE((int)p.size() + r->max_new_tokens + limit <= max_seq,
+                         "context overflow: prompt (" + std::to_string(p.size()) + ") + max_new_tokens (" +
+                             std::to_string(r->max_new_tokens) + ") + draft limit (" + std::to_string(limit) +
+                             ") exceeds max_seq_len " + std::to_string(max_seq));
+        for (auto& p : q.prompts)
+            BASS_REQUIRE((int)p.size() + r->max_new_tokens + limit <= e->cap, "context exceeds cache capacity");
+        const bool greedy = r->temperature == 0.0;
+        const int maxnew = r->max_new_tokens;
+
+        // per-slot device tables: sid, prompt_len (by slot); aligned override tokens
+        int32_t* slot_tab = (int32_t*)e->slotbuf.need((size_t)e->n_slots * 2 * 4, st);
+        std::vector<int32_t> tab(2 * e->n_slots, 0);
+        for (int s = 0; s < b; ++s) {
+            tab[s] = (int32_t)q.sid[s];
+            tab[e->n_slots + s] = (int32_t)q.prompts[s].size();
+        }
+        up(c, slot_tab, tab.data(), tab.size() * 4);
+        const int32_t* d_sid = slot_tab;
+        const int32_t* d_plen = slot_tab + e->n_slots;
+        const int32_t* d_align = nullptr;
+        if (r->align >= 0.0) {
+            BASS_REQUIRE(r->align_tokens != nullptr, "align_tokens required when align >= 0");
+            int32_t* at = (int32_t*)e->align_tok.need((size_t)b * maxnew * 4, st);
+            BASS_CUDA(cudaMemcpyAsync(at, r->align_tokens, (size_t)b * maxnew * 4, cudaMemcpyHostToDevice, st));
+            d_align = at;
+        }
+        // the caches continue from their current lengths (fresh providers: 0,
+        // so step 1's blocks carry the whole prompt, ref:engine.py:248, 268)
+        for (int s = 0; s < b; ++s)
+            BASS_REQUIRE(e->kv_main->len[s] < (int)q.prompts[s].size() + 0 &&
+                             e->kv_draft->len[s] < (int)q.prompts[s].size(),
+                         "cached context longer than the prompt");
+
+        std::vector<std::vector<int32_t>> com(b);
+        for (int s = 0; s < b; ++s) com[s] = q.prompts[s];
+        std::vector<int> ngen(b, 0), done(b, 0);
+        for (int s = 0; s < b; ++s) {
+            res->n_tokens[s] = 0;
+            res->finish_reason[s] = -1;
+            res->completion_step[s] = 0;
+            res->finish_wall_s[s] = 0.0;
+        }
+        int64_t main_calls = 0, draft_calls = 0;
+        int step = 0;
+        const auto t0 = clk::now();
+        const int Lmax = limit + 1;
+        // device buffers sized for the worst step
+        float* vlog = (float*)e->vlog.need((size_t)b * Lmax * V * 4, st);
+        float* dlog = (float*)e->dlog.need((size_t)Lmax * b * V * 4, st);
+        int32_t* vamax = (int32_t*)e->vamax.need((size_t)b * Lmax * 4, st);
+        double* vlse = (double*)e->vlse.need((size_t)b * Lmax * 8, st);
+        int32_t* accf = (int32_t*)e->accf.need((size_t)b * Lmax * 4, st);
+        int32_t* corr = (int32_t*)e->corr.need((size_t)b * Lmax * 4, st);
+        int32_t* btok = (int32_t*)e->bonus.need((size_t)b * 4, st);
+        double* scratch = greedy ? nullptr : (double*)e->scratch.need((size_t)b * Lmax * 2 * V * 8, st);
+        SlotStep* step_dev = (SlotStep*)e->stepbuf.need((size_t)b * sizeof(SlotStep) + (size_t)b * 4 * 4, st);
+        int32_t* per = (int32_t*)(step_dev + b);       // [4][nA]: slot, committed, generated, pos
+
+        while (true) {
+            std::vector<int> A;
+            for (int s = 0; s < b; ++s)
+                if (!done[s]) A.push_back(s);
+            if (A.empty()) break;
+            ++step;
+            const auto ts = clk::now();
+            const int l = ctl.length(), nA = (int)A.size();
+            // per-active tables: slot, committed C, generated count, (draft pos filled per j)
+            {
+                std::vector<int32_t> h(3 * nA);
+                for (int i = 0; i < nA; ++i) {
+                    h[i] = A[i];
+                    h[nA + i] = (int32_t)com[A[i]].size();
+                    h[2 * nA + i] = ngen[A[i]];
+                }
+                up(c, per, h.data(), h.size() * 4);
+            }
+            const int32_t* d_slot = per;
+            const int32_t* d_com = per + nA;
+            const int32_t* d_gen = per + 2 * nA;
+            int32_t* d_pos = per + 3 * nA;
+
+            // ---------------------------------------------- draft phase
+            for (int j = 0; j < l + (greedy ? 0 : 1); ++j) {
+                Batch bt;
+                std::vector<int32_t> pos(nA);
+                for (int i = 0; i < nA; ++i) {
+                    const int s = A[i];
+                    const int dl = e->kv_draft->len[s];
+                    if (j == 0) {
+                        const int C = (int)com[s].size();
+                        BASS_REQUIRE(dl < C, "draft cache ahead of committed prefix");
+                        bt.add_seq(s, dl, com[s].data() + dl, C - dl);
+                    } else {
+                        const int32_t ind = -j;   // proposals[s][j-1]
+                        bt.add_seq(s, dl, &ind, 1);
+                    }
+                    bt.logit_rows.push_back(bt.rows() - 1);
+                    pos[i] = (int)com[s].size() + j;
+                }
+                float* out = dlog + (size_t)j * nA * V;
+                forward(D, *e->kv_draft, bt, e->strategy, out, e->proposals, bass_engine::kPstride);
+                for (int i = 0; i < nA; ++i) e->kv_draft->len[A[i]] += bt.qn[i];
+                if (j == l) break;   // sampled bonus row: no pick here
+                draft_calls += nA;
+                up(c, d_pos, pos.data(), nA * 4);
+                DraftPick dp{d_slot, d_sid, d_pos, e->proposals, bass_engine::kPstride, j,
+                             r->align, r->align_seed, d_align, d_plen, maxnew};
+                if (greedy) draft_greedy_kernel<<<nA, SM_THREADS, 0, st>>>(out, V, dp);
+                else draft_sample_kernel<<<nA, SM_THREADS, 0, st>>>(out, V, r->temperature, r->top_p, r->seed,
+                                                                     scratch, dp);
+                launched(c);
+            }
+            // ---------------------------------------------- verify
+            {
+                Batch bt;
+                std::vector<int32_t> blk;
+                for (int i = 0; i < nA; ++i) {
+                    const int s = A[i];
+                    const int ml = e->kv_main->len[s], C = (int)com[s].size();
+                    blk.assign(com[s].begin() + ml, com[s].end());
+                    for (int j = 0; j < l; ++j) blk.push_back(-(j + 1));
+                    bt.add_seq(s, ml, blk.data(), (int)blk.size());
+                    for (int j = 0; j <= l; ++j) bt.logit_rows.push_back(bt.rows() - (l + 1) + j);
+                    (void)C;
+                }
+                forward(M, *e->kv_main, bt, e->strategy, vlog, e->proposals, bass_engine::kPstride);
+                for (int i = 0; i < nA; ++i) e->kv_main->len[A[i]] += bt.qn[i];
+                main_calls += nA;
+            }
+            const int R = nA * (l + 1);
+            row_stats_kernel<<<R, SM_THREADS, 0, st>>>(vlog, V, vamax, vlse);
+            launched(c);
+            if (!greedy) {
+                VerifyArgs va{nA, l, V, r->temperature, r->top_p, r->seed, d_slot, d_sid, d_com,
+                              e->proposals, bass_engine::kPstride, vlog, dlog, scratch, accf, corr, btok};
+                verify_sampled_kernel<<<dim3(l + 1, nA), SM_THREADS, 0, st>>>(va);
+                launched(c);
+            }
+            StepArgs sa{nA, l, V, d_slot, d_com, d_gen, e->proposals, bass_engine::kPstride, vlog, vamax, vlse,
+                        maxnew, r->eos_token, accf, corr, btok, greedy ? 1 : 0, step_dev};
+            finalize_kernel<<<(nA + 63) / 64, 64, 0, st>>>(sa);
+            launched(c);
+            BASS_CUDA(cudaMemcpyAsync(e->step_host, step_dev, (size_t)nA * sizeof(SlotStep),
+                                      cudaMemcpyDeviceToHost, st));
+            c->sync();
+            const double now = secs(t0, clk::now());
+            // ---------------------------------------------- bookkeeping
+            std::vector<int> acc(nA);
+            if (res->step_draft_len && step <= res->max_steps) {
+                res->step_draft_len[step - 1] = l;
+                res->step_wall_s[step - 1] = secs(ts, clk::now());
+            }
+            for (int i = 0; i < nA; ++i) {
+                const int s = A[i];
+                const SlotStep& o = e->step_host[i];
+                if (o.err == -2)
+                    throw Error(BASS_ERR_VALUE, "draft token has zero draft probability");
+                if (o.err == -3) throw Error(BASS_ERR_VALUE, "residual is empty: q <= p everywhere");
+                acc[i] = o.accepted;
+                // reference counts the bonus draft forward per eligible slot
+                if (!greedy && o.accepted == l && o.n_emit >= 1) {
+                    bool eos_in_core = false;
+                    for (int j = 0; j < std::min(o.n_emit, l); ++j)
+                        eos_in_core |= (r->eos_token >= 0 && o.tok[j] == r->eos_token);
+                    if (!eos_in_core && maxnew - ngen[s] > l) ++draft_calls;
+                }
+                for (int j = 0; j < o.n_emit; ++j) {
+                    res->tokens[(size_t)s * maxnew + ngen[s] + j] = o.tok[j];
+                    res->logprobs[(size_t)s * maxnew + ngen[s] + j] = o.lp[j];
+                    com[s].push_back(o.tok[j]);
+                }
+                ngen[s] += o.n_emit;
+                if (o.reason >= 0) {
+                    done[s] = 1;
+                    res->finish_reason[s] = o.reason;
+                    res->completion_step[s] = step;
+                    res->finish_wall_s[s] = now;
+                }
+                const int target = (int)com[s].size() - 1;   // ref:engine.py:358-360
+                e->kv_main->len[s] = std::min(e->kv_main->len[s], target);
+                e->kv_draft->len[s] = std::min(e->kv_draft->len[s], target);
+                if (res->step_accepted && step <= res->max_steps) {
+                    res->step_accepted[(size_t)(step - 1) * b + s] = o.accepted;
+                    res->step_emitted[(size_t)(step - 1) * b + s] = o.n_emit;
+                }
+            }
+            if (res->step_accepted && step <= res->max_steps)
+                for (int s = 0; s < b; ++s) {
+                    if (done[s] && res->completion_step[s] != step) {
+                        res->step_accepted[(size_t)(step - 1) * b + s] = -1;
+                        res->step_emitted[(size_t)(step - 1) * b + s] = -1;
+                    }
+                    res->step_kv_len[(size_t)(step - 1) * b + s] = (int32_t)com[s].size();
+                }
+            ctl.observe(acc);
+        }
+        for (int s = 0; s < b; ++s) res->n_tokens[s] = ngen[s];
+        res->n_steps = step;
+        res->main_forward_calls = main_calls;
+        res->draft_forward_calls = draft_calls;
+        res->wall_s = secs(t0, clk::now());
+        res->final_l_draft = ctl.l;
+        res->final_s = ctl.s;
+    });
+}
+
+// --------------------------------------------------------------- regular
+int bass_regular_generate(bass_engine* e, const bass_gen_request* r, bass_gen_result* res) {
+    return guarded_e(e, [&] {
+        bass_model& M = *e->main;
+        bass_ctx* c = M.ctx;
+        cudaStream_t st = c->stream;
+        const int V = M.g.vocab_size;
+        Request q = parse(r, V);
+        const int b = q.b, maxnew = r->max_new_tokens;
+        BASS_REQUIRE(b <= e->n_slots, "batch exceeds engine slots");
+        for (auto& p : q.prompts)
+            BASS_REQUIRE((int)p.size() + maxnew <= M.g.max_seq_len,
+                         "prompt (" + std::to_string(p.size()) + ") + max_new_tokens (" + std::to_string(maxnew) +
+                             ") exceeds max_seq_len " + std::to_string(M.g.max_seq_len));
+        for (auto& p : q.prompts) BASS_REQUIRE((int)p.size() + maxnew <= e->cap, "context exceeds cache capacity");
+        const bool greedy = r->temperature == 0.0;
+        int32_t* slot_tab = (int32_t*)e->slotbuf.need((size_t)e->n_slots * 2 * 4, st);
+        std::vector<int32_t> tab(2 * e->n_slots, 0);
+        for (int s = 0; s < b; ++s) tab[s] = (int32_t)q.sid[s];
+        up(c, slot_tab, tab.data(), tab.size() * 4);
+        for (int s = 0; s < b; ++s)
+            BASS_REQUIRE(e->kv_main->len[s] == 0, "sequence " + std::to_string(s) + " already has cached context");
+        float* cur = (float*)e->vlog.need((size_t)b * V * 4, st);
+        double* scratch = greedy ? nullptr : (double*)e->scratch.need((size_t)b * V * 8, st);
+        int32_t* per = (int32_t*)e->stepbuf.need((size_t)b * 4 * 4 + (size_t)b * 16, st);
+        int32_t* d_slot = per;
+        int32_t* d_pos = per + b;
+        int32_t* d_tok = per + 2 * b;
+        double* d_lp = (double*)(per + 4 * b);
+        std::vector<int> ngen(b, 0), done(b, 0);
+        for (int s = 0; s < b; ++s) {
+            res->n_tokens[s] = 0;
+            res->finish_reason[s] = -1;
+            res->completion_step[s] = 0;
+        }
+        const auto t0 = clk::now();
+        // prefill all slots in one ragged block (row-independent == per-slot prefill)
+        {
+            Batch bt;
+            for (int s = 0; s < b; ++s) {
+                bt.add_seq(s, 0, q.prompts[s].data(), (int)q.prompts[s].size());
+                bt.logit_rows.push_back(bt.rows() - 1);
+            }
+            forward(M, *e->kv_main, bt, e->strategy, cur, nullptr, 0);
+            for (int s = 0; s < b; ++s) e->kv_main->len[s] = (int)q.prompts[s].size();
+        }
+        int64_t main_calls = b;
+        std::vector<int> A;
+        for (int s = 0; s < b; ++s) A.push_back(s);
+        int step = 0;
+        std::vector<int32_t> htok(b);
+        std::vector<double> hlp(b);
+        while (!A.empty()) {
+            ++step;
+            const auto ts = clk::now();
+            const int nA = (int)A.size();
+            std::vector<int32_t> h(2 * nA);
+            for (int i = 0; i < nA; ++i) {
+                h[i] = A[i];
+                h[nA + i] = (int32_t)q.prompts[A[i]].size() + ngen[A[i]];
+            }
+            up(c, d_slot, h.data(), nA * 4);
+            up(c, d_pos, h.data() + nA, nA * 4);
+            RegularArgs ra{d_slot, slot_tab, d_pos, e->proposals, bass_engine::kPstride, V, r->temperature,
+                           r->top_p, r->seed, scratch, d_tok, d_lp};
+            regular_pick_kernel<<<nA, SM_THREADS, 0, st>>>(cur, ra);
+            launched(c);
+            BASS_CUDA(cudaMemcpyAsync(htok.data(), d_tok, nA * 4, cudaMemcpyDeviceToHost, st));
+            BASS_CUDA(cudaMemcpyAsync(hlp.data(), d_lp, nA * 8, cudaMemcpyDeviceToHost, st));
+            c->sync();
+            std::vector<int> surv;
+            for (int i = 0; i < nA; ++i) {
+                const int s = A[i];
+                res->tokens[(size_t)s * maxnew + ngen[s]] = htok[i];
+                res->logprobs[(size_t)s * maxnew + ngen[s]] = hlp[i];
+                ++ngen[s];
+                int why = -1;
+                if (r->eos_token >= 0 && htok[i] == r->eos_token) why = 0;
+                else if (ngen[s] >= maxnew) why = 1;
+                if (why >= 0) {
+                    done[s] = 1;
+                    res->finish_reason[s] = why;
+                } else {
+                    surv.push_back(s);
+                }
+            }
+            if (!surv.empty()) {
+                Batch bt;
+                const int32_t ind = -1;
+                for (int s : surv) {
+                    bt.add_seq(s, e->kv_main->len[s], &ind, 1);
+                    bt.logit_rows.push_back(bt.rows() - 1);
+                }
+                forward(M, *e->kv_main, bt, e->strategy, cur, e->proposals, bass_engine::kPstride);
+                for (int s : surv) e->kv_main->len[s] += 1;
+                main_calls += (int64_t)surv.size();
+            }
+            const double now = secs(t0, clk::now());
+            for (int s : A)
+                if (done[s] && res->completion_step[s] == 0) {
+                    res->completion_step[s] = step;
+                    res->finish_wall_s[s] = now;
+                }
+            if (res->step_draft_len && step <= res->max_steps) {
+                res->step_draft_len[step - 1] = 0;
+                res->step_wall_s[step - 1] = secs(ts, clk::now());
+                for (int s = 0; s < b; ++s) {
+                    const bool act = std::find(A.begin(), A.end(), s) != A.end();
+                    res->step_accepted[(size_t)(step - 1) * b + s] = act ? 0 : -1;
+                    res->step_emitted[(size_t)(step - 1) * b + s] = act ? 1 : -1;
+                    res->step_kv_len[(size_t)(step - 1) * b + s] = (int32_t)q.prompts[s].size() + ngen[s];
+                }
+            }
+            A = surv;
+        }
+        for (int s = 0; s < b; ++s) res->n_tokens[s] = ngen[s];
+        res->n_steps = step;
+        res->main_forward_calls = main_calls;
+        res->draft_forward_calls = 0;
+        res->wall_s = secs(t0, clk::now());
+    });
+}
+
+}  // extern "C"

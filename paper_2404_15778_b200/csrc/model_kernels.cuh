@@ -1,0 +1,292 @@
+// Ragged decoder forward: embedding, LayerNorm, SIMT GEMM (parity/fp32
+// path), ragged attention (PAD / SPLIT / RAGGED work list) and the split-KV
+// combine.  Every reduction runs in a fixed order that depends only on the
+// row's own data and absolute key positions, never on which other rows share
+// the launch: a row's result is bitwise independent of batch composition and
+// block length (the reference's purity contract, ref:model.py:267-271).
+#pragma once
+#include "common.cuh"
+
+namespace bass {
+
+constexpr float kLnEps = 1e-5f;   // ref:model.py:31
+
+// ---------------------------------------------------------------- metadata
+struct Rows {                    // one entry per new token row (length M)
+    const int32_t* tok;          // >= 0: token id; < 0: proposals[slot][-tok-1]
+    const int32_t* slot;
+    const int32_t* pos;          // absolute position = cache offset + t
+};
+struct Seqs {                    // one entry per sequence in the block
+    const int32_t* slot;
+    const int32_t* q0;           // first row of this sequence
+    const int32_t* qn;           // rows in this sequence
+    const int32_t* off;          // committed cache length before the block
+};
+
+// ------------------------------------------------------------- embedding
+// x[r] = tok_emb[id] + pos_emb[pos]   (ref:model.py:203-209)
+template <typename TW>
+__global__ void embed_kernel(const TW* __restrict__ tok_emb, const TW* __restrict__ pos_emb,
+                             Rows rows, const int32_t* __restrict__ proposals, int pstride,
+                             int d, float* __restrict__ x) {
+    const int r = blockIdx.x;
+    int id = rows.tok[r];
+    if (id < 0) id = proposals[rows.slot[r] * pstride + (-id - 1)];
+    const int p = rows.pos[r];
+    for (int c = threadIdx.x; c < d; c += blockDim.x)
+        x[(int64_t)r * d + c] = ld(tok_emb, (int64_t)id * d + c) + ld(pos_emb, (int64_t)p * d + c);
+}
+
+// ------------------------------------------------------------- layernorm
+// (x - mean) / sqrt(var + eps) * g + b, population variance, two passes
+// (ref:model.py:150-153).  Optional row gather (final LN of selected rows).
+template <typename TA>
+__global__ void layernorm_kernel(const float* __restrict__ x, const int32_t* __restrict__ gather,
+                                 const float* __restrict__ g, const float* __restrict__ b, int d,
+                                 TA* __restrict__ out) {
+    __shared__ float red[33];
+    const int r = blockIdx.x;
+    const int src = gather ? gather[r] : r;
+    const float* xr = x + (int64_t)src * d;
+    float s = 0.f;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) s += xr[c];
+    const float mean = block_sum(s, red) / float(d);
+    float v = 0.f;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        float t = xr[c] - mean;
+        v += t * t;
+    }
+    const float var = block_sum(v, red) / float(d);
+    const float rstd = 1.0f / sqrtf(var + kLnEps);
+    for (int c = threadIdx.x; c < d; c += blockDim.x)
+        st(out, (int64_t)r * d + c, (xr[c] - mean) * rstd * g[c] + b[c]);
+}
+
+// ------------------------------------------------------------- epilogues
+enum EpiMode { EPI_QKV = 0, EPI_RESID = 1, EPI_GELU = 2, EPI_STORE = 3 };
+
+struct Epi {
+    float* x;            // EPI_RESID: x[m, n] += acc (fp32 residual stream)
+    void* out;           // EPI_QKV: q [M, d] (act); EPI_GELU: [M, N] (act); EPI_STORE: [M, N] fp32
+    void* kc;            // EPI_QKV: this layer's K cache [slot][H][cap][dh] (act dtype)
+    void* vc;
+    const int32_t* row_slot;
+    const int32_t* row_pos;
+    int d, dh, H, cap;
+};
+
+BASS_DEV float gelu_erf(float v) {   // ref:model.py:156-157 (exact erf form)
+    return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f));
+}
+
+template <int MODE, typename TA>
+BASS_DEV void epilogue(const Epi& e, int m, int n, int N, float acc) {
+    if constexpr (MODE == EPI_QKV) {
+        const int part = n / e.d, nn = n - part * e.d;
+        if (part == 0) {
+            st(reinterpret_cast<TA*>(e.out), (int64_t)m * e.d + nn, acc);
+        } else {
+            const int h = nn / e.dh, c = nn - h * e.dh;
+            TA* base = reinterpret_cast<TA*>(part == 1 ? e.kc : e.vc);
+            const int64_t idx = (((int64_t)e.row_slot[m] * e.H + h) * e.cap + e.row_pos[m]) * e.dh + c;
+            st(base, idx, acc);     // KV append (ref:kv_cache.py:63-84)
+        }
+    } else if constexpr (MODE == EPI_RESID) {
+        e.x[(int64_t)m * N + n] += acc;
+    } else if constexpr (MODE == EPI_GELU) {
+        st(reinterpret_cast<TA*>(e.out), (int64_t)m * N + n, gelu_erf(acc));
+    } else {
+        reinterpret_cast<float*>(e.out)[(int64_t)m * N + n] = acc;
+    }
+}
+
+// ----------------------------------------------------------- SIMT GEMM
+// Y[m, n] = sum_k X[m, k] * W[n, k]  (W stored output-major [N, K]).
+// Each output is one thread's sequential FMA chain over k = 0..K-1, so it
+// does not depend on M or on the other rows.  Used for the fp32 parity mode
+// (true FFMA, no TF32) and as the reference kernel for the tcgen05 GEMM.
+constexpr int SG_BN = 64, SG_BM = 16, SG_BK = 32;
+
+template <int MODE, typename TA, typename TW>
+__global__ void __launch_bounds__(256) gemm_simt_kernel(const TA* __restrict__ X,
+                                                         const TW* __restrict__ W, int M, int N,
+                                                         int K, Epi e) {
+    __shared__ float Ws[SG_BK][SG_BN + 1];
+    __shared__ float Xs[SG_BM][SG_BK + 1];
+    const int t = threadIdx.x;
+    const int n0 = blockIdx.x * SG_BN, m0 = blockIdx.y * SG_BM;
+    const int f = t & 63, tg = t >> 6;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int k0 = 0; k0 < K; k0 += SG_BK) {
+#pragma unroll
+        for (int j = 0; j < (SG_BN * SG_BK) / 256; ++j) {
+            const int i = t + 256 * j, nn = i / SG_BK, kk = i % SG_BK;
+            const int gn = n0 + nn, gk = k0 + kk;
+            Ws[kk][nn] = (gn < N && gk < K) ? ld(W, (int64_t)gn * K + gk) : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < (SG_BM * SG_BK) / 256; ++j) {
+            const int i = t + 256 * j, mm = i / SG_BK, kk = i % SG_BK;
+            const int gm = m0 + mm, gk = k0 + kk;
+            Xs[mm][kk] = (gm < M && gk < K) ? ld(X, (int64_t)gm * K + gk) : 0.f;
+        }
+        __syncthreads();
+        const int kmax = min(SG_BK, K - k0);
+        for (int kk = 0; kk < kmax; ++kk) {
+            const float w = Ws[kk][f];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[r] = fmaf(Xs[tg * 4 + r][kk], w, acc[r]);
+        }
+        __syncthreads();
+    }
+    const int n = n0 + f;
+    if (n >= N) return;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int m = m0 + tg * 4 + r;
+        if (m < M) epilogue<MODE, TA>(e, m, n, N, acc[r]);
+    }
+}
+
+// ------------------------------------------------------ ragged attention
+// softmax((q . k) / sqrt(dh), causal s <= off + t) . v per (sequence, head)
+// (ref:attention.py:85-137).  Work unit = (q tile of 16 rows, head, KV chunk
+// of 256 absolute key positions); inside a chunk, 64-key sub-tiles are folded
+// with an online softmax; chunk partials are merged by attn_combine_kernel
+// in chunk order.  Chunk / sub-tile boundaries are absolute key positions,
+// so a row's arithmetic is identical for PAD, SPLIT and RAGGED launches and
+// for any q_len (prefill, verify, single-token decode).
+constexpr int AT_QT = 16, AT_CHUNK = 256, AT_SUB = 64, AT_THREADS = 128;
+
+struct AttnWork {                 // one q tile of one sequence
+    int32_t seq, t0;
+};
+
+template <typename TA, int DH>
+__global__ void __launch_bounds__(AT_THREADS) attn_partial_kernel(
+    const TA* __restrict__ q, const TA* __restrict__ kc, const TA* __restrict__ vc, Seqs seqs,
+    const AttnWork* __restrict__ work, int H, int cap, int pad_kv_len,
+    float* __restrict__ part_o, float* __restrict__ part_ml, int max_chunks) {
+    constexpr int EPL = (DH + 31) / 32;               // head dims per lane (guarded)
+    extern __shared__ float smem[];
+    float* Kt = smem;                                  // [DH][AT_SUB + 1]
+    float* Vs = Kt + DH * (AT_SUB + 1);                // [AT_SUB][DH]
+    float* Qs = Vs + AT_SUB * DH;                      // [AT_QT][DH]
+
+    const AttnWork wk = work[blockIdx.z];
+    const int h = blockIdx.y, c = blockIdx.x;
+    const int slot = seqs.slot[wk.seq], qn = seqs.qn[wk.seq], off = seqs.off[wk.seq];
+    const int q0row = seqs.q0[wk.seq];
+    const int L = off + qn;                           // keys visible to the last row
+    const int kv_len = pad_kv_len > 0 ? pad_kv_len : L;   // PAD: padded key range
+    const int c_begin = c * AT_CHUNK;
+    if (c_begin >= kv_len) return;
+    const int t_last = min(qn, wk.t0 + AT_QT) - 1;
+    if (wk.t0 >= qn || off + t_last < c_begin) return;   // no row of the tile sees this chunk
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const float scale = sqrtf(float(DH));
+
+    for (int i = threadIdx.x; i < AT_QT * DH; i += AT_THREADS) {
+        const int rr = i / DH, cc = i % DH, t = wk.t0 + rr;
+        Qs[i] = t < qn ? ld(q, ((int64_t)(q0row + t) * H + h) * DH + cc) : 0.f;
+    }
+    // each warp owns 4 rows of the tile
+    float m_run[4], l_run[4], o[4][EPL];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        m_run[r] = -INFINITY;
+        l_run[r] = 0.f;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) o[r][e] = 0.f;
+    }
+    const int64_t kvbase = ((int64_t)slot * H + h) * cap;
+    const int c_end = min(c_begin + AT_CHUNK, kv_len);
+    for (int s0 = c_begin; s0 < c_end; s0 += AT_SUB) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < AT_SUB * DH; i += AT_THREADS) {
+            const int j = i / DH, cc = i % DH, s = s0 + j;
+            float kv = 0.f, vv = 0.f;
+            if (s < c_end) {
+                kv = ld(kc, (kvbase + s) * DH + cc);
+                vv = ld(vc, (kvbase + s) * DH + cc);
+            }
+            Kt[cc * (AT_SUB + 1) + j] = kv;
+            Vs[j * DH + cc] = vv;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int rr = warp * 4 + r, t = wk.t0 + rr;
+            if (t >= qn) continue;
+            const int lim = off + t;                      // last visible key
+            if (lim < s0) continue;
+            float sc[2];
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+                const int j = lane + 32 * jj;
+                float a = 0.f;
+#pragma unroll 8
+                for (int cc = 0; cc < DH; ++cc) a = fmaf(Qs[rr * DH + cc], Kt[cc * (AT_SUB + 1) + j], a);
+                const int s = s0 + j;
+                sc[jj] = (s <= lim && s < c_end && s < L) ? a / scale : -INFINITY;
+            }
+            const float mx = warp_max(fmaxf(sc[0], sc[1]));
+            const float m_new = fmaxf(m_run[r], mx);
+            if (m_new == -INFINITY) continue;
+            const float alpha = __expf(m_run[r] - m_new);
+            float p[2];
+            p[0] = sc[0] == -INFINITY ? 0.f : expf(sc[0] - m_new);
+            p[1] = sc[1] == -INFINITY ? 0.f : expf(sc[1] - m_new);
+            l_run[r] = l_run[r] * alpha + warp_sum(p[0] + p[1]);
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) o[r][e] *= alpha;
+            for (int j = 0; j < AT_SUB; ++j) {
+                const float pj = __shfl_sync(0xffffffffu, p[j >> 5], j & 31);
+#pragma unroll
+                for (int e = 0; e < EPL; ++e)
+                    if (lane + 32 * e < DH) o[r][e] = fmaf(pj, Vs[j * DH + lane + 32 * e], o[r][e]);
+            }
+            m_run[r] = m_new;
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int t = wk.t0 + warp * 4 + r;
+        if (t >= qn || off + t < c_begin) continue;
+        const int64_t slotidx = ((int64_t)(q0row + t) * H + h) * max_chunks + c;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e)
+            if (lane + 32 * e < DH) part_o[slotidx * DH + lane + 32 * e] = o[r][e];
+        if (lane == 0) {
+            part_ml[slotidx * 2] = m_run[r];
+            part_ml[slotidx * 2 + 1] = l_run[r];
+        }
+    }
+}
+
+// merge chunk partials of one (row, head) in chunk order; writes ctx [M, H*dh]
+template <typename TA, int DH>
+__global__ void attn_combine_kernel(const float* __restrict__ part_o, const float* __restrict__ part_ml,
+                                    const int32_t* __restrict__ row_pos, int H, int max_chunks,
+                                    TA* __restrict__ out) {
+    const int r = blockIdx.x, h = blockIdx.y;
+    const int nc = row_pos[r] / AT_CHUNK + 1;
+    const int64_t base = ((int64_t)r * H + h) * max_chunks;
+    float mx = -INFINITY;
+    for (int c = 0; c < nc; ++c) mx = fmaxf(mx, part_ml[(base + c) * 2]);
+    for (int e = threadIdx.x; e < DH; e += blockDim.x) {
+        float num = 0.f, den = 0.f;
+        for (int c = 0; c < nc; ++c) {
+            const float m = part_ml[(base + c) * 2];
+            if (m == -INFINITY) continue;
+            const float w = expf(m - mx);
+            num = fmaf(w, part_o[(base + c) * DH + e], num);
+            den = fmaf(w, part_ml[(base + c) * 2 + 1], den);
+        }
+        st(out, ((int64_t)r * H + h) * DH + e, num / den);
+    }
+}
+
+}  // namespace bass

@@ -1,0 +1,761 @@
+// libbass runtime: contexts, device weights, ragged KV cache, the ragged
+// forward (ref:model.py:177-246) and the C-ABI entry points of include/bass.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "runtime.h"
+#include "sampling_kernels.cuh"
+
+using namespace bass;
+
+// ------------------------------------------------------------ utilities
+namespace bass {
+
+void* Staging::take(size_t n) {
+    n = (n + 255) & ~size_t(255);
+    if (used + n > cap) return nullptr;
+    void* p = base + used;
+    used += n;
+    return p;
+}
+
+void* DevBuf::need(size_t n, cudaStream_t s) {
+    if (n <= cap) return p;
+    if (p) {
+        BASS_CUDA(cudaStreamSynchronize(s));
+        BASS_CUDA(cudaFree(p));
+        p = nullptr;
+    }
+    size_t c = std::max(n, cap * 3 / 2);
+    BASS_CUDA(cudaMalloc(&p, c));
+    cap = c;
+    return p;
+}
+
+void DevBuf::release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+}
+
+void Batch::add_seq(int s, int offset, const int32_t* toks, int n) {
+    slot.push_back(s);
+    q0.push_back(rows());
+    qn.push_back(n);
+    off.push_back(offset);
+    for (int t = 0; t < n; ++t) {
+        tok.push_back(toks[t]);
+        row_slot.push_back(s);
+        row_pos.push_back(offset + t);
+    }
+}
+
+}  // namespace bass
+
+void bass_ctx::sync() {
+    BASS_CUDA(cudaStreamSynchronize(stream));
+    staging.used = 0;
+}
+
+template <typename F>
+static int guarded(bass_ctx* ctx, F&& f) {
+    try {
+        f();
+        return BASS_OK;
+    } catch (const Error& e) {
+        if (ctx) ctx->err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        if (ctx) ctx->err = e.what();
+        return BASS_ERR_STATE;
+    }
+}
+
+#define LAUNCHED(ctx) ((ctx)->launches++)
+
+static void check_launch(bass_ctx* ctx) {
+    LAUNCHED(ctx);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Error(BASS_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+// stage `n` int32 values to device through pinned memory (async)
+static void upload_i32(bass_ctx* ctx, int32_t* dev, const int32_t* src, size_t n) {
+    if (n == 0) return;
+    void* h = ctx->staging.take(n * 4);
+    if (!h) {
+        ctx->sync();
+        h = ctx->staging.take(n * 4);
+        if (!h) throw Error(BASS_ERR_MEMORY, "staging arena too small");
+    }
+    std::memcpy(h, src, n * 4);
+    BASS_CUDA(cudaMemcpyAsync(dev, h, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+}
+
+// ------------------------------------------------------- weight kernels
+namespace {
+
+// dst[n, k] = src[k, n]  (reference input-major [K, N] -> output-major [N, K])
+template <typename T>
+__global__ void transpose_convert(const float* __restrict__ src, int K, int N, T* __restrict__ dst,
+                                  int64_t dst_ld) {
+    __shared__ float tile[32][33];
+    const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int k = k0 + i, n = n0 + threadIdx.x;
+        tile[i][threadIdx.x] = (k < K && n < N) ? src[(int64_t)k * N + n] : 0.f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int n = n0 + i, k = k0 + threadIdx.x;
+        if (n < N && k < K) dst[(int64_t)n * dst_ld + k] = cvt<T>(tile[threadIdx.x][i]);
+    }
+}
+
+template <typename T>
+__global__ void convert_copy(const float* __restrict__ src, int64_t n, T* __restrict__ dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = cvt<T>(src[i]);
+}
+
+template <typename T>
+__global__ void random_normal(T* __restrict__ dst, int64_t n, uint64_t seed, float std) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t a = splitmix64(seed ^ splitmix64(uint64_t(i)));
+        const uint64_t b = splitmix64(a);
+        const float u1 = (float((a >> 40) + 1) * (1.0f / 16777217.0f));
+        const float u2 = float(b >> 40) * (1.0f / 16777216.0f);
+        dst[i] = cvt<T>(std * sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2));
+    }
+}
+
+__global__ void fill_f32(float* p, int64_t n, float v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ forward
+namespace bass {
+
+template <typename TA>
+static void launch_layernorm(bass_model& m, const float* x, const int32_t* gather, const float* g,
+                             const float* b, int rows, TA* out) {
+    layernorm_kernel<TA><<<rows, 256, 0, m.ctx->stream>>>(x, gather, g, b, m.g.d_model, out);
+    check_launch(m.ctx);
+}
+
+static void launch_layernorm_any(bass_model& m, const float* x, const int32_t* gather, const float* g,
+                                 const float* b, int rows, void* out) {
+    if (m.dtype == BASS_BF16) launch_layernorm(m, x, gather, g, b, rows, (__nv_bfloat16*)out);
+    else launch_layernorm(m, x, gather, g, b, rows, (float*)out);
+}
+
+template <int MODE, typename TA>
+static void gemm_simt(bass_model& m, const void* X, const void* W, int M, int N, int K, const Epi& e) {
+    dim3 grid((N + SG_BN - 1) / SG_BN, (M + SG_BM - 1) / SG_BM);
+    gemm_simt_kernel<MODE, TA, TA><<<grid, 256, 0, m.ctx->stream>>>((const TA*)X, (const TA*)W, M, N, K, e);
+    check_launch(m.ctx);
+}
+
+void gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K, const Epi& e) {
+    if (M == 0) return;
+    const bool tc = m.dtype == BASS_BF16 && m.gemm_mode != BASS_GEMM_SIMT && tc_gemm_supported(m, N, K);
+    if (m.gemm_mode == BASS_GEMM_TC && !tc)
+        throw Error(BASS_ERR_STATE, "tcgen05 GEMM requested but unsupported for this shape/dtype");
+    if (tc) {
+        tc_gemm(m, mode, X, W, M, N, K, e);
+        return;
+    }
+#define BASS_GEMM_CASE(MD)                                                            \
+    case MD:                                                                          \
+        if (m.dtype == BASS_BF16) gemm_simt<MD, __nv_bfloat16>(m, X, W, M, N, K, e);  \
+        else gemm_simt<MD, float>(m, X, W, M, N, K, e);                               \
+        break;
+    switch (mode) {
+        BASS_GEMM_CASE(EPI_QKV)
+        BASS_GEMM_CASE(EPI_RESID)
+        BASS_GEMM_CASE(EPI_GELU)
+        BASS_GEMM_CASE(EPI_STORE)
+        default: throw Error(BASS_ERR_STATE, "bad epilogue");
+    }
+#undef BASS_GEMM_CASE
+}
+
+template <typename TA, int DH>
+static void launch_attention_t(bass_ctx* ctx, int strategy, const void* q, const void* kc, const void* vc,
+                               const Seqs& seqs_dev, const std::vector<int32_t>& qn,
+                               const std::vector<int32_t>& off, const int32_t* row_pos_dev, int M,
+                               int H, int cap, DevBuf& work_buf, DevBuf& po, DevBuf& pml, void* out) {
+    const int n_seq = (int)qn.size();
+    const int max_chunks = (cap + AT_CHUNK - 1) / AT_CHUNK;
+    float* part_o = (float*)po.need((size_t)M * H * max_chunks * DH * 4, ctx->stream);
+    float* part_ml = (float*)pml.need((size_t)M * H * max_chunks * 2 * 4, ctx->stream);
+    const size_t smem = (size_t)(DH * (AT_SUB + 1) + AT_SUB * DH + AT_QT * DH) * 4;
+    static bool attr_set = false;
+    if (!attr_set) {
+        BASS_CUDA(cudaFuncSetAttribute(attn_partial_kernel<TA, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+        attr_set = true;
+    }
+    int max_qn = 0, max_L = 0;
+    for (int i = 0; i < n_seq; ++i) {
+        max_qn = std::max(max_qn, qn[i]);
+        max_L = std::max(max_L, off[i] + qn[i]);
+    }
+    // work lists: RAGGED/SPLIT exact tiles; PAD every tile of the padded [max_qn] range
+    std::vector<int32_t> work;
+    std::vector<int> seq_first(n_seq + 1, 0);
+    for (int i = 0; i < n_seq; ++i) {
+        seq_first[i] = (int)work.size() / 2;
+        const int rows = strategy == BASS_PAD ? max_qn : qn[i];
+        for (int t0 = 0; t0 < rows; t0 += AT_QT) {
+            work.push_back(i);
+            work.push_back(t0);
+        }
+    }
+    seq_first[n_seq] = (int)work.size() / 2;
+    AttnWork* wdev = (AttnWork*)work_buf.need(work.size() * 4, ctx->stream);
+    upload_i32(ctx, (int32_t*)wdev, work.data(), work.size());
+    const int threads = AT_THREADS;
+    if (strategy == BASS_SPLIT) {
+        for (int i = 0; i < n_seq; ++i) {
+            const int nw = seq_first[i + 1] - seq_first[i];
+            dim3 grid((off[i] + qn[i] + AT_CHUNK - 1) / AT_CHUNK, H, nw);
+            attn_partial_kernel<TA, DH><<<grid, threads, smem, ctx->stream>>>(
+                (const TA*)q, (const TA*)kc, (const TA*)vc, seqs_dev, wdev + seq_first[i], H, cap, 0, part_o,
+                part_ml, max_chunks);
+            check_launch(ctx);
+        }
+    } else {
+        const int nw = seq_first[n_seq];
+        dim3 grid((max_L + AT_CHUNK - 1) / AT_CHUNK, H, nw);
+        attn_partial_kernel<TA, DH><<<grid, threads, smem, ctx->stream>>>(
+            (const TA*)q, (const TA*)kc, (const TA*)vc, seqs_dev, wdev, H, cap,
+            strategy == BASS_PAD ? max_L : 0, part_o, part_ml, max_chunks);
+        check_launch(ctx);
+    }
+    attn_combine_kernel<TA, DH><<<dim3(M, H), DH, 0, ctx->stream>>>(part_o, part_ml, row_pos_dev, H, max_chunks,
+                                                                    (TA*)out);
+    check_launch(ctx);
+}
+
+static void launch_attention(bass_ctx* ctx, int dtype, int dh, int strategy, const void* q, const void* kc,
+                             const void* vc, const Seqs& seqs_dev, const std::vector<int32_t>& qn,
+                             const std::vector<int32_t>& off, const int32_t* row_pos_dev, int M, int H, int cap,
+                             DevBuf& work_buf, DevBuf& po, DevBuf& pml, void* out) {
+#define BASS_ATT(T, D)                                                                                  \
+    launch_attention_t<T, D>(ctx, strategy, q, kc, vc, seqs_dev, qn, off, row_pos_dev, M, H, cap, work_buf, \
+                             po, pml, out)
+    if (dtype == BASS_BF16) {
+        if (dh == 16) BASS_ATT(__nv_bfloat16, 16);
+        else if (dh == 32) BASS_ATT(__nv_bfloat16, 32);
+        else if (dh == 64) BASS_ATT(__nv_bfloat16, 64);
+        else if (dh == 128) BASS_ATT(__nv_bfloat16, 128);
+        else throw Error(BASS_ERR_VALUE, "d_head must be 16, 32, 64 or 128");
+    } else {
+        if (dh == 16) BASS_ATT(float, 16);
+        else if (dh == 32) BASS_ATT(float, 32);
+        else if (dh == 64) BASS_ATT(float, 64);
+        else if (dh == 128) BASS_ATT(float, 128);
+        else throw Error(BASS_ERR_VALUE, "d_head must be 16, 32, 64 or 128");
+    }
+#undef BASS_ATT
+}
+
+void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* logits_out,
+             const int32_t* proposals, int pstride) {
+    bass_ctx* ctx = m.ctx;
+    cudaStream_t st = ctx->stream;
+    const bass_geometry& g = m.g;
+    const int M = b.rows(), n_seq = (int)b.slot.size(), R = (int)b.logit_rows.size();
+    const int d = g.d_model, H = g.n_head, dh = g.d_head, V = g.vocab_size;
+    const size_t es = m.esize;
+    // metadata: tok, row_slot, row_pos | slot, q0, qn, off | logit_rows | attention work (separate)
+    const size_t nmeta = 3 * (size_t)M + 4 * (size_t)n_seq + R;
+    int32_t* meta = (int32_t*)m.meta.need(nmeta * 4, st);
+    std::vector<int32_t> hm;
+    hm.reserve(nmeta);
+    hm.insert(hm.end(), b.tok.begin(), b.tok.end());
+    hm.insert(hm.end(), b.row_slot.begin(), b.row_slot.end());
+    hm.insert(hm.end(), b.row_pos.begin(), b.row_pos.end());
+    hm.insert(hm.end(), b.slot.begin(), b.slot.end());
+    hm.insert(hm.end(), b.q0.begin(), b.q0.end());
+    hm.insert(hm.end(), b.qn.begin(), b.qn.end());
+    hm.insert(hm.end(), b.off.begin(), b.off.end());
+    hm.insert(hm.end(), b.logit_rows.begin(), b.logit_rows.end());
+    upload_i32(ctx, meta, hm.data(), hm.size());
+    Rows rows{meta, meta + M, meta + 2 * M};
+    Seqs seqs{meta + 3 * M, meta + 3 * M + n_seq, meta + 3 * M + 2 * n_seq, meta + 3 * M + 3 * n_seq};
+    const int32_t* lrows = meta + 3 * M + 4 * n_seq;
+
+    float* x = (float*)m.x.need((size_t)M * d * 4, st);
+    void* h = m.h.need((size_t)M * d * es, st);
+    void* q = m.q.need((size_t)M * d * es, st);
+    void* cx = m.ctxb.need((size_t)M * d * es, st);
+    void* f = m.f.need((size_t)M * 4 * d * es, st);
+    static DevBuf work_buf;   // per-process attention work list (tiny)
+
+    if (m.dtype == BASS_BF16)
+        embed_kernel<__nv_bfloat16><<<M, 128, 0, st>>>((const __nv_bfloat16*)m.tok_emb,
+                                                       (const __nv_bfloat16*)m.pos_emb, rows, proposals, pstride,
+                                                       d, x);
+    else
+        embed_kernel<float><<<M, 128, 0, st>>>((const float*)m.tok_emb, (const float*)m.pos_emb, rows, proposals,
+                                               pstride, d, x);
+    check_launch(ctx);
+
+    for (int li = 0; li < g.n_layer; ++li) {
+        const bass_layer& L = m.layers[li];
+        launch_layernorm_any(m, x, nullptr, L.ln1_g, L.ln1_b, M, h);
+        Epi e{};
+        e.out = q;
+        e.kc = (char*)kv.k + li * kv.layer_elems() * es;
+        e.vc = (char*)kv.v + li * kv.layer_elems() * es;
+        e.row_slot = rows.slot;
+        e.row_pos = rows.pos;
+        e.d = d; e.dh = dh; e.H = H; e.cap = kv.cap;
+        gemm(m, EPI_QKV, h, L.wqkv, M, 3 * d, d, e);
+        launch_attention(ctx, m.dtype, dh, strategy, q, e.kc, e.vc, seqs, b.qn, b.off, rows.pos, M, H, kv.cap,
+                         work_buf, m.part_o, m.part_ml, cx);
+        Epi r{};
+        r.x = x;
+        gemm(m, EPI_RESID, cx, L.wo, M, d, d, r);
+        launch_layernorm_any(m, x, nullptr, L.ln2_g, L.ln2_b, M, h);
+        Epi ge{};
+        ge.out = f;
+        gemm(m, EPI_GELU, h, L.wfc, M, 4 * d, d, ge);
+        gemm(m, EPI_RESID, f, L.wproj, M, d, 4 * d, r);
+    }
+    if (R > 0) {
+        void* hs = m.hs.need((size_t)R * d * es, st);
+        launch_layernorm_any(m, x, lrows, m.lnf_g, m.lnf_b, R, hs);
+        Epi so{};
+        so.out = logits_out;
+        gemm(m, EPI_STORE, hs, m.head, R, V, d, so);
+    }
+}
+
+}  // namespace bass
+
+// ------------------------------------------------------------ C ABI
+extern "C" {
+
+int bass_version(void) { return 1; }
+
+int bass_device_arch(int device) {
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, device) != cudaSuccess) return -1;
+    return p.major * 10 + p.minor;
+}
+
+int bass_ctx_create(int device, bass_ctx** out) {
+    bass_ctx* c = new bass_ctx();
+    int rc = guarded(c, [&] {
+        BASS_CUDA(cudaSetDevice(device));
+        c->device = device;
+        BASS_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+        BASS_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+        c->staging.cap = 64u << 20;
+        BASS_CUDA(cudaMallocHost((void**)&c->staging.base, c->staging.cap));
+    });
+    if (rc != BASS_OK) {
+        *out = nullptr;
+        static std::string last;
+        last = c->err;
+        delete c;
+        return rc;
+    }
+    *out = c;
+    return BASS_OK;
+}
+
+int bass_ctx_destroy(bass_ctx* c) {
+    if (!c) return BASS_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    if (c->staging.base) cudaFreeHost(c->staging.base);
+    delete c;
+    return BASS_OK;
+}
+
+int bass_ctx_set_stream(bass_ctx* c, void* s) {
+    return guarded(c, [&] {
+        BASS_CUDA(cudaStreamSynchronize(c->stream));
+        if (c->own_stream) cudaStreamDestroy(c->stream);
+        c->stream = (cudaStream_t)s;
+        c->own_stream = false;
+    });
+}
+
+int bass_ctx_sync(bass_ctx* c) {
+    return guarded(c, [&] { c->sync(); });
+}
+
+const char* bass_last_error(const bass_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int64_t bass_ctx_launches(const bass_ctx* c) { return c ? c->launches : 0; }
+
+// ---------------------------------------------------------------- model
+int bass_model_create(bass_ctx* c, const bass_geometry* g, int dtype, bass_model** out) {
+    *out = nullptr;
+    return guarded(c, [&] {
+        BASS_REQUIRE(g->n_layer >= 1 && g->n_head >= 1 && g->d_model >= 1 && g->d_head >= 1 &&
+                         g->vocab_size >= 1 && g->max_seq_len >= 1,
+                     "geometry: all sizes must be >= 1");
+        BASS_REQUIRE(g->d_model == g->n_head * g->d_head, "geometry: d_model != n_head * d_head");
+        BASS_REQUIRE(dtype == BASS_BF16 || dtype == BASS_F32, "dtype must be BASS_BF16 or BASS_F32");
+        BASS_REQUIRE(g->d_head == 16 || g->d_head == 32 || g->d_head == 64 || g->d_head == 128,
+                     "d_head must be 16, 32, 64 or 128");
+        BASS_CUDA(cudaSetDevice(c->device));
+        bass_model* m = new bass_model();
+        m->ctx = c;
+        m->g = *g;
+        m->dtype = dtype;
+        m->esize = dtype == BASS_BF16 ? 2 : 4;
+        const int64_t d = g->d_model, V = g->vocab_size, S = g->max_seq_len, L = g->n_layer;
+        // row alignment of 16 bytes for every matrix (TMA requirement)
+        const int64_t per_layer = 3 * d * d + d * d + 4 * d * d + 4 * d * d;
+        const int64_t total = V * d + S * d + L * per_layer + V * d;
+        m->weight_bytes = total * m->esize;
+        BASS_CUDA(cudaMalloc(&m->wblob, (size_t)m->weight_bytes));
+        const int64_t nf = L * 4 * d + 2 * d;
+        BASS_CUDA(cudaMalloc((void**)&m->fblob, (size_t)nf * 4));
+        char* p = (char*)m->wblob;
+        auto take = [&](int64_t n) { void* r = p; p += n * m->esize; return r; };
+        m->tok_emb = take(V * d);
+        m->pos_emb = take(S * d);
+        float* fp = m->fblob;
+        m->layers.resize(L);
+        for (int i = 0; i < L; ++i) {
+            bass_layer& ly = m->layers[i];
+            ly.wqkv = take(3 * d * d);
+            ly.wo = take(d * d);
+            ly.wfc = take(4 * d * d);
+            ly.wproj = take(4 * d * d);
+            ly.ln1_g = fp; fp += d;
+            ly.ln1_b = fp; fp += d;
+            ly.ln2_g = fp; fp += d;
+            ly.ln2_b = fp; fp += d;
+        }
+        m->head = take(V * d);
+        m->lnf_g = fp; fp += d;
+        m->lnf_b = fp; fp += d;
+        // LN defaults (gain 1, bias 0) — ref:model.py:121-130
+        for (int i = 0; i < L; ++i) {
+            fill_f32<<<32, 256, 0, c->stream>>>(m->layers[i].ln1_g, d, 1.f);
+            fill_f32<<<32, 256, 0, c->stream>>>(m->layers[i].ln1_b, d, 0.f);
+            fill_f32<<<32, 256, 0, c->stream>>>(m->layers[i].ln2_g, d, 1.f);
+            fill_f32<<<32, 256, 0, c->stream>>>(m->layers[i].ln2_b, d, 0.f);
+        }
+        fill_f32<<<32, 256, 0, c->stream>>>(m->lnf_g, d, 1.f);
+        fill_f32<<<32, 256, 0, c->stream>>>(m->lnf_b, d, 0.f);
+        BASS_CUDA(cudaGetLastError());
+        BASS_CUDA(cudaStreamSynchronize(c->stream));
+        *out = m;
+    });
+}
+
+int bass_model_destroy(bass_model* m) {
+    if (!m) return BASS_OK;
+    cudaSetDevice(m->ctx->device);
+    cudaStreamSynchronize(m->ctx->stream);
+    tc_release(*m);
+    cudaFree(m->wblob);
+    cudaFree(m->fblob);
+    for (DevBuf* b : {&m->x, &m->h, &m->q, &m->ctxb, &m->f, &m->hs, &m->meta, &m->part_o, &m->part_ml,
+                      &m->logits_tmp})
+        b->release();
+    delete m;
+    return BASS_OK;
+}
+
+int bass_model_set_weight(bass_model* m, int tensor, int layer, const float* host, int64_t n) {
+    return guarded(m->ctx, [&] {
+        const bass_geometry& g = m->g;
+        const int64_t d = g.d_model, V = g.vocab_size, S = g.max_seq_len;
+        BASS_REQUIRE(tensor >= BASS_W_TOK_EMB && tensor <= BASS_W_HEAD, "unknown tensor id");
+        const bool per_layer = tensor >= BASS_W_LN1_G && tensor <= BASS_W_LN2_B;
+        BASS_REQUIRE(!per_layer || (layer >= 0 && layer < g.n_layer), "layer index out of range");
+        cudaStream_t st = m->ctx->stream;
+        auto upload_tmp = [&](int64_t count) {
+            BASS_REQUIRE(n == count, "geometry: element count does not match the tensor");
+            float* tmp;
+            BASS_CUDA(cudaMallocAsync((void**)&tmp, count * 4, st));
+            BASS_CUDA(cudaMemcpyAsync(tmp, host, count * 4, cudaMemcpyHostToDevice, st));
+            return tmp;
+        };
+        auto put_matrix = [&](int64_t K, int64_t N, void* dst, int64_t row_off) {
+            // reference [K, N] -> device output-major rows [row_off + n][K]
+            float* tmp = upload_tmp(K * N);
+            dim3 grid((N + 31) / 32, (K + 31) / 32), blk(32, 8);
+            if (m->dtype == BASS_BF16)
+                transpose_convert<<<grid, blk, 0, st>>>(tmp, (int)K, (int)N,
+                                                        (__nv_bfloat16*)dst + row_off * K, K);
+            else
+                transpose_convert<<<grid, blk, 0, st>>>(tmp, (int)K, (int)N, (float*)dst + row_off * K, K);
+            BASS_CUDA(cudaGetLastError());
+            BASS_CUDA(cudaFreeAsync(tmp, st));
+        };
+        auto put_rows = [&](int64_t count, void* dst) {
+            float* tmp = upload_tmp(count);
+            if (m->dtype == BASS_BF16) convert_copy<<<256, 256, 0, st>>>(tmp, count, (__nv_bfloat16*)dst);
+            else convert_copy<<<256, 256, 0, st>>>(tmp, count, (float*)dst);
+            BASS_CUDA(cudaGetLastError());
+            BASS_CUDA(cudaFreeAsync(tmp, st));
+        };
+        auto put_f32 = [&](float* dst) {
+            BASS_REQUIRE(n == d, "geometry: LN parameter must have d_model elements");
+            BASS_CUDA(cudaMemcpyAsync(dst, host, d * 4, cudaMemcpyHostToDevice, st));
+        };
+        const bool layer_mat = tensor >= BASS_W_WQ && tensor <= BASS_W_PROJ && tensor != BASS_W_LN2_G &&
+                               tensor != BASS_W_LN2_B;
+        if (layer_mat) BASS_REQUIRE(layer >= 0 && layer < g.n_layer, "layer index out of range");
+        switch (tensor) {
+            case BASS_W_TOK_EMB: put_rows(V * d, m->tok_emb); break;
+            case BASS_W_POS_EMB: put_rows(S * d, m->pos_emb); break;
+            case BASS_W_LN1_G: put_f32(m->layers[layer].ln1_g); break;
+            case BASS_W_LN1_B: put_f32(m->layers[layer].ln1_b); break;
+            case BASS_W_LN2_G: put_f32(m->layers[layer].ln2_g); break;
+            case BASS_W_LN2_B: put_f32(m->layers[layer].ln2_b); break;
+            case BASS_W_WQ: put_matrix(d, d, m->layers[layer].wqkv, 0); break;
+            case BASS_W_WK: put_matrix(d, d, m->layers[layer].wqkv, d); break;
+            case BASS_W_WV: put_matrix(d, d, m->layers[layer].wqkv, 2 * d); break;
+            case BASS_W_WO: put_matrix(d, d, m->layers[layer].wo, 0); break;
+            case BASS_W_FC: put_matrix(d, 4 * d, m->layers[layer].wfc, 0); break;
+            case BASS_W_PROJ: put_matrix(4 * d, d, m->layers[layer].wproj, 0); break;
+            case BASS_W_LNF_G: put_f32(m->lnf_g); break;
+            case BASS_W_LNF_B: put_f32(m->lnf_b); break;
+            case BASS_W_HEAD: put_matrix(d, V, m->head, 0); break;
+        }
+        BASS_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int bass_model_init_random(bass_model* m, uint64_t seed, float std) {
+    return guarded(m->ctx, [&] {
+        const int64_t n = m->weight_bytes / (int64_t)m->esize;
+        if (m->dtype == BASS_BF16)
+            random_normal<<<m->ctx->sm_count * 8, 256, 0, m->ctx->stream>>>((__nv_bfloat16*)m->wblob, n, seed, std);
+        else
+            random_normal<<<m->ctx->sm_count * 8, 256, 0, m->ctx->stream>>>((float*)m->wblob, n, seed, std);
+        BASS_CUDA(cudaGetLastError());
+        BASS_CUDA(cudaStreamSynchronize(m->ctx->stream));
+    });
+}
+
+int bass_model_set_gemm(bass_model* m, int mode) {
+    return guarded(m->ctx, [&] {
+        BASS_REQUIRE(mode >= BASS_GEMM_AUTO && mode <= BASS_GEMM_TC, "unknown gemm mode");
+        m->gemm_mode = mode;
+    });
+}
+
+int64_t bass_model_weight_bytes(const bass_model* m) { return m ? m->weight_bytes : 0; }
+
+// ------------------------------------------------------------------- KV
+int bass_kv_create(bass_model* m, int n_slots, int capacity, bass_kv** out) {
+    *out = nullptr;
+    return guarded(m->ctx, [&] {
+        BASS_REQUIRE(n_slots >= 1 && capacity >= 1, "geometry: cache sizes must be positive");
+        BASS_REQUIRE(capacity <= m->g.max_seq_len, "capacity exceeds max_seq_len");
+        bass_kv* kv = new bass_kv();
+        kv->m = m;
+        kv->n_slots = n_slots;
+        kv->cap = capacity;
+        kv->len.assign(n_slots, 0);
+        const size_t bytes = kv->layer_elems() * m->g.n_layer * m->esize;
+        BASS_CUDA(cudaMalloc(&kv->k, bytes));
+        BASS_CUDA(cudaMalloc(&kv->v, bytes));
+        *out = kv;
+    });
+}
+
+int bass_kv_destroy(bass_kv* kv) {
+    if (!kv) return BASS_OK;
+    cudaStreamSynchronize(kv->m->ctx->stream);
+    cudaFree(kv->k);
+    cudaFree(kv->v);
+    delete kv;
+    return BASS_OK;
+}
+
+int bass_kv_lengths(const bass_kv* kv, int32_t* out) {
+    std::memcpy(out, kv->len.data(), kv->len.size() * 4);
+    return BASS_OK;
+}
+
+int bass_kv_truncate(bass_kv* kv, int n, const int32_t* slots, const int32_t* lens) {
+    return guarded(kv->m->ctx, [&] {
+        for (int i = 0; i < n; ++i) {
+            BASS_REQUIRE(slots[i] >= 0 && slots[i] < kv->n_slots, "slot out of range");
+            BASS_REQUIRE(lens[i] >= 0, "negative length");
+            BASS_REQUIRE(lens[i] <= kv->len[slots[i]], "truncate to " + std::to_string(lens[i]) +
+                                                           " exceeds current length " +
+                                                           std::to_string(kv->len[slots[i]]));
+        }
+        for (int i = 0; i < n; ++i) kv->len[slots[i]] = lens[i];
+    });
+}
+
+int bass_forward_ragged(bass_model* m, bass_kv* kv, int n_seq, const int32_t* slots, const int32_t* cu_q,
+                        const int32_t* tokens, int strategy, int rows_mode, float* logits_host) {
+    return guarded(m->ctx, [&] {
+        BASS_REQUIRE(n_seq >= 1, "active_seqs and new_tokens must align and be non-empty");
+        BASS_REQUIRE(kv->m == m, "cache belongs to another model");
+        const bass_geometry& g = m->g;
+        Batch b;
+        std::vector<char> seen(kv->n_slots, 0);
+        for (int i = 0; i < n_seq; ++i) {
+            const int s = slots[i], n = cu_q[i + 1] - cu_q[i];
+            BASS_REQUIRE(s >= 0 && s < kv->n_slots, "slot out of range");
+            BASS_REQUIRE(!seen[s], "duplicate slot in one forward");
+            seen[s] = 1;
+            BASS_REQUIRE(n >= 1, "sequence " + std::to_string(s) + ": empty token block");
+            const int off = kv->len[s];
+            BASS_REQUIRE(off + n <= g.max_seq_len, "sequence " + std::to_string(s) + ": context " +
+                                                       std::to_string(off + n) + " exceeds max_seq_len " +
+                                                       std::to_string(g.max_seq_len));
+            BASS_REQUIRE(off + n <= kv->cap, "sequence " + std::to_string(s) + ": context exceeds cache capacity");
+            for (int t = cu_q[i]; t < cu_q[i + 1]; ++t)
+                BASS_REQUIRE(tokens[t] >= 0 && tokens[t] < g.vocab_size,
+                             "sequence " + std::to_string(s) + ": token id outside vocab");
+            b.add_seq(s, off, tokens + cu_q[i], n);
+            if (rows_mode == 1) b.logit_rows.push_back(b.rows() - 1);
+        }
+        if (rows_mode == 0)
+            for (int r = 0; r < b.rows(); ++r) b.logit_rows.push_back(r);
+        const size_t R = b.logit_rows.size();
+        float* lg = (float*)m->logits_tmp.need(R * g.vocab_size * 4, m->ctx->stream);
+        forward(*m, *kv, b, strategy, lg, nullptr, 0);
+        BASS_CUDA(cudaMemcpyAsync(logits_host, lg, R * g.vocab_size * 4, cudaMemcpyDeviceToHost, m->ctx->stream));
+        m->ctx->sync();
+        for (int i = 0; i < n_seq; ++i) kv->len[slots[i]] += cu_q[i + 1] - cu_q[i];
+    });
+}
+
+// ------------------------------------------------------ standalone kernels
+int bass_attention(bass_ctx* c, int strategy, int dtype, int n_seq, int n_head, int d_head, const int32_t* cu_q,
+                   const int32_t* offsets, const void* q, const void* k, const void* v, int kv_stride, void* out) {
+    return guarded(c, [&] {
+        BASS_REQUIRE(n_seq >= 1, "empty workload");
+        std::vector<int32_t> slot(n_seq), q0(n_seq), qn(n_seq), off(n_seq), row_pos;
+        for (int i = 0; i < n_seq; ++i) {
+            slot[i] = i;
+            q0[i] = cu_q[i];
+            qn[i] = cu_q[i + 1] - cu_q[i];
+            off[i] = offsets[i];
+            BASS_REQUIRE(qn[i] >= 1, "every sequence needs at least one query");
+            BASS_REQUIRE(off[i] >= 0 && off[i] + qn[i] <= kv_stride, "offset exceeds history");
+            for (int t = 0; t < qn[i]; ++t) row_pos.push_back(off[i] + t);
+        }
+        const int M = cu_q[n_seq];
+        static DevBuf meta, work, po, pml;
+        int32_t* dm = (int32_t*)meta.need((4 * (size_t)n_seq + M) * 4, c->stream);
+        std::vector<int32_t> hm;
+        for (auto* v_ : {&slot, &q0, &qn, &off}) hm.insert(hm.end(), v_->begin(), v_->end());
+        hm.insert(hm.end(), row_pos.begin(), row_pos.end());
+        upload_i32(c, dm, hm.data(), hm.size());
+        Seqs seqs{dm, dm + n_seq, dm + 2 * n_seq, dm + 3 * n_seq};
+        launch_attention(c, dtype, d_head, strategy, q, k, v, seqs, qn, off, dm + 4 * n_seq, M, n_head, kv_stride,
+                         work, po, pml, out);
+        c->sync();
+    });
+}
+
+int bass_rng_uniforms(bass_ctx* c, int n, uint64_t seed, const int64_t* sid, const int32_t* role, const int64_t* ctr,
+                      double* out) {
+    return guarded(c, [&] {
+        if (n <= 0) return;
+        int64_t *ds, *dc;
+        int32_t* dr;
+        double* dout;
+        BASS_CUDA(cudaMallocAsync((void**)&ds, n * 8, c->stream));
+        BASS_CUDA(cudaMallocAsync((void**)&dc, n * 8, c->stream));
+        BASS_CUDA(cudaMallocAsync((void**)&dr, n * 4, c->stream));
+        BASS_CUDA(cudaMallocAsync((void**)&dout, n * 16, c->stream));
+        BASS_CUDA(cudaMemcpyAsync(ds, sid, n * 8, cudaMemcpyHostToDevice, c->stream));
+        BASS_CUDA(cudaMemcpyAsync(dc, ctr, n * 8, cudaMemcpyHostToDevice, c->stream));
+        BASS_CUDA(cudaMemcpyAsync(dr, role, n * 4, cudaMemcpyHostToDevice, c->stream));
+        rng_kernel<<<(n + 127) / 128, 128, 0, c->stream>>>(n, seed, ds, dr, dc, dout);
+        check_launch(c);
+        BASS_CUDA(cudaMemcpyAsync(out, dout, n * 16, cudaMemcpyDeviceToHost, c->stream));
+        for (void* p : {(void*)ds, (void*)dc, (void*)dr, (void*)dout}) BASS_CUDA(cudaFreeAsync(p, c->stream));
+        c->sync();
+    });
+}
+
+int bass_shape_sample(bass_ctx* c, int n, int V, const float* logits, double T, double top_p, const double* u,
+                      int32_t* tok_out, double* probs_out) {
+    return guarded(c, [&] {
+        BASS_REQUIRE(top_p > 0.0 && top_p <= 1.0, "top_p must be in (0, 1]");
+        BASS_REQUIRE(T >= 0.0, "temperature must be >= 0");
+        if (n <= 0) return;
+        for (int i = 0; i < n; ++i) {
+            bool finite = false;
+            for (int k = 0; k < V && !finite; ++k) finite = std::isfinite(logits[(int64_t)i * V + k]);
+            BASS_REQUIRE(finite, "all logits are -inf; distribution undefined");
+        }
+        float* dl;
+        double *du, *scr, *dp = nullptr;
+        int32_t* dt;
+        BASS_CUDA(cudaMallocAsync((void**)&dl, (size_t)n * V * 4, c->stream));
+        BASS_CUDA(cudaMallocAsync((void**)&du, (size_t)n * 8, c->stream));
+        BASS_CUDA(cudaMallocAsync((void**)&scr, (size_t)n * V * 8, c->stream));
+        BASS_CUDA(cudaMallocAsync((void**)&dt, (size_t)n * 4, c->stream));
+        if (probs_out) BASS_CUDA(cudaMallocAsync((void**)&dp, (size_t)n * V * 8, c->stream));
+        BASS_CUDA(cudaMemcpyAsync(dl, logits, (size_t)n * V * 4, cudaMemcpyHostToDevice, c->stream));
+        BASS_CUDA(cudaMemcpyAsync(du, u, (size_t)n * 8, cudaMemcpyHostToDevice, c->stream));
+        shape_sample_kernel<<<n, SM_THREADS, 0, c->stream>>>(dl, V, T, top_p, du, scr, dt, dp);
+        check_launch(c);
+        BASS_CUDA(cudaMemcpyAsync(tok_out, dt, (size_t)n * 4, cudaMemcpyDeviceToHost, c->stream));
+        if (probs_out)
+            BASS_CUDA(cudaMemcpyAsync(probs_out, dp, (size_t)n * V * 8, cudaMemcpyDeviceToHost, c->stream));
+        for (void* p : {(void*)dl, (void*)du, (void*)scr, (void*)dt}) BASS_CUDA(cudaFreeAsync(p, c->stream));
+        if (dp) BASS_CUDA(cudaFreeAsync(dp, c->stream));
+        c->sync();
+    });
+}
+
+int bass_accept(bass_ctx* c, int n, int V, const float* ql, const float* pl, double T, double top_p,
+                const int32_t* tok, uint64_t seed, const int64_t* sid, const int64_t* ctr, int32_t* acc_out,
+                int32_t* corr_out) {
+    return guarded(c, [&] {
+        if (n <= 0) return;
+        float *dq, *dp;
+        double* scr;
+        int32_t *dt, *da, *dc;
+        int64_t *ds, *dr;
+        cudaStream_t st = c->stream;
+        BASS_CUDA(cudaMallocAsync((void**)&dq, (size_t)n * V * 4, st));
+        BASS_CUDA(cudaMallocAsync((void**)&dp, (size_t)n * V * 4, st));
+        BASS_CUDA(cudaMallocAsync((void**)&scr, (size_t)n * V * 16, st));
+        BASS_CUDA(cudaMallocAsync((void**)&dt, (size_t)n * 4, st));
+        BASS_CUDA(cudaMallocAsync((void**)&da, (size_t)n * 4, st));
+        BASS_CUDA(cudaMallocAsync((void**)&dc, (size_t)n * 4, st));
+        BASS_CUDA(cudaMallocAsync((void**)&ds, (size_t)n * 8, st));
+        BASS_CUDA(cudaMallocAsync((void**)&dr, (size_t)n * 8, st));
+        BASS_CUDA(cudaMemcpyAsync(dq, ql, (size_t)n * V * 4, cudaMemcpyHostToDevice, st));
+        BASS_CUDA(cudaMemcpyAsync(dp, pl, (size_t)n * V * 4, cudaMemcpyHostToDevice, st));
+        BASS_CUDA(cudaMemcpyAsync(dt, tok, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+        BASS_CUDA(cudaMemcpyAsync(ds, sid, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+        BASS_CUDA(cudaMemcpyAsync(dr, ctr, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+        accept_pairs_kernel<<<n, SM_THREADS, 0, st>>>(dq, dp, V, T, top_p, dt, seed, ds, dr, scr, da, dc);
+        check_launch(c);
+        BASS_CUDA(cudaMemcpyAsync(acc_out, da, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+        BASS_CUDA(cudaMemcpyAsync(corr_out, dc, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+        for (void* p : {(void*)dq, (void*)dp, (void*)scr, (void*)dt, (void*)da, (void*)dc, (void*)ds, (void*)dr})
+            BASS_CUDA(cudaFreeAsync(p, st));
+        c->sync();
+        for (int i = 0; i < n; ++i)
+            BASS_REQUIRE(corr_out[i] != -2, "draft token " + std::to_string(tok[i]) + " has zero draft probability");
+    });
+}
+
+}  // extern "C"

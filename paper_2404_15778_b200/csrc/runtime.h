@@ -1,0 +1,121 @@
+// Host-side runtime objects behind the C ABI (include/bass.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/bass.h"
+#include "model_kernels.cuh"
+
+
+namespace bass {
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define BASS_CUDA(call)                                                                    \
+    do {                                                                                   \
+        cudaError_t _e = (call);                                                           \
+        if (_e != cudaSuccess)                                                             \
+            throw ::bass::Error(BASS_ERR_CUDA, std::string(#call) + ": " +                 \
+                                                   cudaGetErrorString(_e));                \
+    } while (0)
+
+#define BASS_REQUIRE(cond, msg)                                                            \
+    do {                                                                                   \
+        if (!(cond)) throw ::bass::Error(BASS_ERR_VALUE, (msg));                           \
+    } while (0)
+
+// Bump allocator over pinned host memory for per-forward metadata.  Async
+// H2D copies may still read an earlier region, so it is only reset at a
+// stream synchronisation point.
+struct Staging {
+    char* base = nullptr;
+    size_t cap = 0, used = 0;
+    void* take(size_t n);
+};
+
+// Device buffer that grows (after a stream sync) when a larger size is needed.
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* need(size_t n, cudaStream_t s);
+    void release();
+};
+
+}  // namespace bass
+
+struct bass_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+    int64_t launches = 0;
+    bass::Staging staging;
+    void sync();
+};
+
+struct bass_layer {
+    float *ln1_g, *ln1_b, *ln2_g, *ln2_b;
+    void *wqkv, *wo, *wfc, *wproj;   // output-major [N, K]
+};
+
+struct bass_model {
+    bass_ctx* ctx = nullptr;
+    bass_geometry g{};
+    int dtype = BASS_BF16;
+    int gemm_mode = BASS_GEMM_AUTO;
+    size_t esize = 2;
+    void* wblob = nullptr;           // all matrices, one allocation
+    float* fblob = nullptr;          // LN params
+    int64_t weight_bytes = 0;
+    void *tok_emb = nullptr, *pos_emb = nullptr, *head = nullptr;
+    float *lnf_g = nullptr, *lnf_b = nullptr;
+    std::vector<bass_layer> layers;
+    // workspace (grown on demand)
+    bass::DevBuf x, h, q, ctxb, f, hs, meta, part_o, part_ml, logits_tmp;
+    void* tc_state = nullptr;        // tcgen05 GEMM descriptors (gemm_tc.cu)
+};
+
+struct bass_kv {
+    bass_model* m = nullptr;
+    int n_slots = 0, cap = 0;
+    void *k = nullptr, *v = nullptr;  // [L][slot][H][cap][dh]
+    std::vector<int32_t> len;
+    size_t layer_elems() const {
+        return (size_t)n_slots * m->g.n_head * cap * m->g.d_head;
+    }
+};
+
+namespace bass {
+
+// One ragged forward described on the host; metadata is uploaded by forward().
+struct Batch {
+    std::vector<int32_t> tok, row_slot, row_pos;      // per row
+    std::vector<int32_t> slot, q0, qn, off;           // per sequence
+    std::vector<int32_t> logit_rows;                  // rows whose logits are wanted
+    void add_seq(int s, int offset, const int32_t* toks, int n);
+    int rows() const { return (int)tok.size(); }
+};
+
+// Run `b` through model m over cache kv; logits [logit_rows, V] fp32 -> logits_out (device).
+void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* logits_out,
+             const int32_t* proposals, int pstride);
+
+// GEMM dispatch (SIMT or tcgen05) — Y = X W^T with a fused epilogue.
+void gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K,
+          const Epi& e);
+
+// tcgen05 GEMM (gemm_tc.cu); returns false when the shape is unsupported.
+bool tc_gemm_supported(const bass_model& m, int N, int K);
+void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K,
+             const Epi& e);
+void tc_release(bass_model& m);
+
+}  // namespace bass

@@ -1,0 +1,533 @@
+// K9: shaping, sampling, accept/resample, bonus, finalize — on device.
+//
+// Restates ref:sampling.py:69-146 and the per-slot step logic of
+// ref:engine.py:243-360 over fp32 logits rows, with probabilities in fp64.
+// Shaping keeps the nucleus as "keys above a boundary + ties up to an id",
+// found by a 4-pass radix select on the orderable logit key; this equals the
+// reference's lexsort((ids, -p)) order because p is monotone in the logit
+// and ties in p are ties in the logit.
+#pragma once
+#include "common.cuh"
+#include "rng.cuh"
+
+namespace bass {
+
+constexpr int SM_THREADS = 512;
+constexpr int kMaxEmit = 64;   // >= draft limit + 1
+
+struct Shaped {
+    int greedy;      // T == 0: one-hot on argmax
+    int argmax;
+    double S;        // sum of e_i
+    double Kf;       // kept mass in units of e_i / S
+    uint32_t ukey;   // boundary key
+    int id_lim;      // ties at ukey kept when id <= id_lim
+    int keep_all;
+};
+
+struct ShapeSmem {
+    int cnt[256];
+    double mass[256];
+    double dred[33];
+    float fred[33];
+    int ired[33];
+    int64_t lred[33];
+    Shaped sh;
+    int sel, found;
+    double before;
+};
+
+BASS_DEV bool sh_kept(const Shaped& s, float x, int i) {
+    if (s.keep_all) return true;
+    const uint32_t k = fkey(x);
+    return k > s.ukey || (k == s.ukey && i <= s.id_lim);
+}
+
+BASS_DEV double sh_prob(const Shaped& s, const float* row, const double* e, int i) {
+    if (s.greedy) return i == s.argmax ? 1.0 : 0.0;
+    return sh_kept(s, row[i], i) ? (e[i] / s.S) / s.Kf : 0.0;
+}
+
+// Shape one row into `out`.  `e` is a per-row fp64 scratch of length V.
+// ref:sampling.py:69-104.  Must be called by all threads of the block.
+BASS_DEV void shape_row(const float* __restrict__ row, int V, double T, double top_p,
+                        double* __restrict__ e, ShapeSmem& sm) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    // argmax / max (first index on ties)
+    ArgMax a{-INFINITY, 0x7fffffff};
+    for (int i = tid; i < V; i += nt) a = better(a, ArgMax{row[i], i});
+    a = block_argmax(a, sm.fred, sm.ired);
+    if (T == 0.0) {
+        if (tid == 0) { sm.sh = Shaped{}; sm.sh.greedy = 1; sm.sh.argmax = a.i; }
+        __syncthreads();
+        return;
+    }
+    const double zmax = double(a.v) / T;
+    double s = 0.0;
+    for (int i = tid; i < V; i += nt) {
+        const double ei = exp(double(row[i]) / T - zmax);   // exp(-inf) = 0
+        e[i] = ei;
+        s += ei;
+    }
+    const double S = block_sum(s, sm.dred);
+    // radix select over the key, descending: find the bucket where the
+    // running mass (in descending key order) first reaches top_p.
+    uint32_t prefix = 0;
+    double before = 0.0;
+    int keep_all = 0;
+    for (int pass = 0; pass < 4 && !keep_all; ++pass) {
+        const int shift = 24 - 8 * pass;
+        for (int b = tid; b < 256; b += nt) { sm.cnt[b] = 0; sm.mass[b] = 0.0; }
+        __syncthreads();
+        for (int i = tid; i < V; i += nt) {
+            const uint32_t k = fkey(row[i]);
+            if (pass > 0 && (k >> (shift + 8)) != prefix) continue;
+            const int b = (k >> shift) & 255;
+            atomicAdd(&sm.cnt[b], 1);
+            atomicAdd(&sm.mass[b], e[i] / S);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double run = before;
+            int sel = -1, last_nonempty = -1;
+            for (int b = 255; b >= 0; --b) {
+                if (sm.cnt[b] == 0) continue;
+                last_nonempty = b;
+                if (run + sm.mass[b] >= top_p) { sel = b; break; }
+                run += sm.mass[b];
+            }
+            if (sel < 0) {
+                // never reaches top_p: at pass 0 keep everything
+                // (searchsorted clamps to n-1); deeper, take the last bucket
+                if (pass == 0) { sm.found = 0; }
+                else { sel = last_nonempty; double r2 = before;
+                       for (int b = 255; b > sel; --b) r2 += sm.mass[b]; run = r2; sm.found = 1; }
+            } else {
+                sm.found = 1;
+            }
+            sm.sel = sel;
+            sm.before = run;
+        }
+        __syncthreads();
+        if (!sm.found) { keep_all = 1; break; }
+        prefix = (prefix << 8) | uint32_t(sm.sel);
+        before = sm.before;
+        __syncthreads();
+    }
+    int id_lim = 0x7fffffff;
+    if (!keep_all) {
+        // ties at the boundary key: same logit -> same probability f
+        const int g = sm.cnt[sm.sel];
+        const uint32_t ukey = prefix;
+        // f of a member (all equal); find one member's e
+        __syncthreads();
+        if (tid == 0) sm.found = -1;
+        __syncthreads();
+        for (int i = tid; i < V; i += nt)
+            if (fkey(row[i]) == ukey) atomicMax(&sm.found, i);   // any member index
+        __syncthreads();
+        const double f = e[sm.found] / S;
+        if (tid == 0) {
+            double run = before;
+            int n = 0;
+            while (n < g) { run += f; ++n; if (run >= top_p) break; }
+            sm.sel = n;          // members (by id) kept
+        }
+        __syncthreads();
+        const int need = sm.sel;
+        if (need < g) {
+            // id of the need-th member in ascending id order
+            const int chunk = (V + nt - 1) / nt, lo = tid * chunk, hi = min(V, lo + chunk);
+            int c = 0;
+            for (int i = lo; i < hi; ++i) c += fkey(row[i]) == ukey;
+            int tot;
+            int pre = block_exclusive_scan(c, sm.ired, &tot);
+            __syncthreads();
+            if (pre < need && pre + c >= need) {
+                int cc = pre;
+                for (int i = lo; i < hi; ++i)
+                    if (fkey(row[i]) == ukey && ++cc == need) { sm.found = i; break; }
+            }
+            __syncthreads();
+            id_lim = sm.found;
+        }
+        if (tid == 0) { sm.sh.ukey = ukey; }
+    }
+    __syncthreads();
+    Shaped sh{};
+    sh.greedy = 0;
+    sh.argmax = a.i;
+    sh.S = S;
+    sh.keep_all = keep_all;
+    sh.ukey = keep_all ? 0u : prefix;
+    sh.id_lim = id_lim;
+    double kf = 0.0;
+    for (int i = tid; i < V; i += nt)
+        if (sh_kept(sh, row[i], i)) kf += e[i] / S;
+    sh.Kf = block_sum(kf, sm.dred);
+    if (tid == 0) sm.sh = sh;
+    __syncthreads();
+}
+
+// First index whose running sum (id order) of w(i) exceeds u * total;
+// clamped to V-1 (ref:sampling.py:112-115).  `w` is a callable.
+template <typename W>
+BASS_DEV int inverse_cdf_block(int V, double u, W w, ShapeSmem& sm) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int chunk = (V + nt - 1) / nt, lo = tid * chunk, hi = min(V, lo + chunk);
+    double loc = 0.0;
+    for (int i = lo; i < hi; ++i) loc += w(i);
+    double total;
+    const double pre = block_exclusive_scan(loc, sm.dred, &total);
+    const double target = u * total;
+    // the chosen element always has positive weight (csum[i-1] <= target <
+    // csum[i]); every thread proposes its first crossing, the block keeps the
+    // smallest, which is robust to the scan's rounding at range borders
+    int cand = 0x7fffffff;
+    double c = pre;
+    for (int i = lo; i < hi; ++i) {
+        const double wi = w(i);
+        c += wi;
+        if (c > target && wi > 0.0) { cand = i; break; }
+    }
+    // block min of candidates
+    ArgMax am{-float(cand), cand};
+    am = block_argmax(am, sm.fred, sm.ired);
+    const int idx = am.i;
+    return idx == 0x7fffffff ? V - 1 : min(idx, V - 1);
+}
+
+// ---------------------------------------------------------------- kernels
+
+// per logits row: argmax (first index) and log-sum-exp (fp64 accumulate)
+static __global__ void __launch_bounds__(SM_THREADS) row_stats_kernel(const float* __restrict__ logits,
+                                                               int V, int32_t* __restrict__ amax,
+                                                               double* __restrict__ lse) {
+    __shared__ float fv[33];
+    __shared__ int iv[33];
+    __shared__ double dv[33];
+    const float* row = logits + (int64_t)blockIdx.x * V;
+    ArgMax a{-INFINITY, 0x7fffffff};
+    for (int i = threadIdx.x; i < V; i += blockDim.x) a = better(a, ArgMax{row[i], i});
+    a = block_argmax(a, fv, iv);
+    double s = 0.0;
+    for (int i = threadIdx.x; i < V; i += blockDim.x) s += exp(double(row[i]) - double(a.v));
+    s = block_sum(s, dv);
+    if (threadIdx.x == 0) {
+        amax[blockIdx.x] = a.i;
+        lse[blockIdx.x] = double(a.v) + log(s);      // scipy.special.logsumexp
+    }
+}
+
+struct DraftPick {               // per active sequence of a draft step
+    const int32_t* slot;         // [nA]
+    const int32_t* sid;          // sequence ids (by slot)
+    const int32_t* pos;          // absolute position of the proposal (by seq)
+    int32_t* proposals;          // [slot][pstride]
+    int pstride, j;
+    // harness override (align < 0: off)
+    double align;
+    uint64_t align_seed;
+    const int32_t* align_tok;    // [slot][max_new]
+    const int32_t* prompt_len;   // by slot
+    int max_new;
+};
+
+BASS_DEV int aligned_override(const DraftPick& d, int slot, int pos, int V, int tok) {
+    if (d.align < 0.0) return tok;
+    const uint64_t h = splitmix64(d.align_seed ^ splitmix64(uint64_t(d.sid[slot]) * 0x100000001B3ull +
+                                                            uint64_t(pos)));
+    const double u = double(h >> 11) * (1.0 / 9007199254740992.0);
+    const int gi = pos - d.prompt_len[slot];
+    if (u < d.align && gi >= 0 && gi < d.max_new) return d.align_tok[slot * d.max_new + gi];
+    return int(splitmix64(h) % uint64_t(V));
+}
+
+// greedy draft step: proposal = argmax of the sequence's last draft row
+static __global__ void __launch_bounds__(SM_THREADS) draft_greedy_kernel(const float* __restrict__ logits,
+                                                                  int V, DraftPick d) {
+    __shared__ float fv[33];
+    __shared__ int iv[33];
+    const int i = blockIdx.x;
+    const float* row = logits + (int64_t)i * V;
+    ArgMax a{-INFINITY, 0x7fffffff};
+    for (int k = threadIdx.x; k < V; k += blockDim.x) a = better(a, ArgMax{row[k], k});
+    a = block_argmax(a, fv, iv);
+    if (threadIdx.x == 0) {
+        const int slot = d.slot[i];
+        d.proposals[slot * d.pstride + d.j] = aligned_override(d, slot, d.pos[i], V, a.i);
+    }
+}
+
+// sampled draft step: proposal ~ shape(row), uniform = RNG(seed, sid, DRAFT, pos)
+static __global__ void __launch_bounds__(SM_THREADS) draft_sample_kernel(const float* __restrict__ logits,
+                                                                  int V, double T, double top_p,
+                                                                  uint64_t seed, double* scratch,
+                                                                  DraftPick d) {
+    __shared__ ShapeSmem sm;
+    const int i = blockIdx.x;
+    const float* row = logits + (int64_t)i * V;
+    double* e = scratch + (int64_t)blockIdx.x * V;
+    shape_row(row, V, T, top_p, e, sm);
+    const int slot = d.slot[i], pos = d.pos[i];
+    Pcg64 g = pcg64_from_key(seed, uint64_t(d.sid[slot]), 0u, uint64_t(pos));
+    const double u = pcg64_double(g);
+    const Shaped sh = sm.sh;
+    const int tok = inverse_cdf_block(V, u, [&](int k) { return sh_prob(sh, row, e, k); }, sm);
+    if (threadIdx.x == 0) d.proposals[slot * d.pstride + d.j] = aligned_override(d, slot, pos, V, tok);
+}
+
+// standalone shaping + sampling (bass_shape_sample)
+static __global__ void __launch_bounds__(SM_THREADS) shape_sample_kernel(const float* __restrict__ logits,
+                                                                  int V, double T, double top_p,
+                                                                  const double* __restrict__ u,
+                                                                  double* scratch,
+                                                                  int32_t* __restrict__ tok,
+                                                                  double* __restrict__ probs) {
+    __shared__ ShapeSmem sm;
+    const float* row = logits + (int64_t)blockIdx.x * V;
+    double* e = scratch + (int64_t)blockIdx.x * V;
+    shape_row(row, V, T, top_p, e, sm);
+    const Shaped sh = sm.sh;
+    if (probs)
+        for (int k = threadIdx.x; k < V; k += blockDim.x)
+            probs[(int64_t)blockIdx.x * V + k] = sh_prob(sh, row, e, k);
+    const int t = inverse_cdf_block(V, u[blockIdx.x], [&](int k) { return sh_prob(sh, row, e, k); }, sm);
+    if (threadIdx.x == 0) tok[blockIdx.x] = t;
+}
+
+// accept / resample for one (q row, p row, token, VERIFY generator);
+// returns corrected token or -1 when accepted; -2 on zero draft probability.
+BASS_DEV int accept_block(const float* qrow, const float* prow, int V, double T, double top_p,
+                          double* eq, double* ep, int tok, Pcg64& g, ShapeSmem& sm) {
+    shape_row(qrow, V, T, top_p, eq, sm);
+    const Shaped sq = sm.sh;
+    __syncthreads();
+    shape_row(prow, V, T, top_p, ep, sm);
+    const Shaped sp = sm.sh;
+    const double px = sh_prob(sp, prow, ep, tok);
+    const double qx = sh_prob(sq, qrow, eq, tok);
+    if (px <= 0.0) return -2;
+    const double u = pcg64_double(g);
+    if (u * px < qx) return -1;
+    // residual normalize(max(q - p, 0)), sampled with the second draw
+    auto r = [&](int k) {
+        const double d = sh_prob(sq, qrow, eq, k) - sh_prob(sp, prow, ep, k);
+        return d > 0.0 ? d : 0.0;
+    };
+    double loc = 0.0;
+    for (int k = threadIdx.x; k < V; k += blockDim.x) loc += r(k);
+    const double R = block_sum(loc, sm.dred);
+    if (R <= 0.0) return -3;
+    const double u2 = pcg64_double(g);
+    return inverse_cdf_block(V, u2, [&](int k) { return r(k) / R; }, sm);
+}
+
+static __global__ void __launch_bounds__(SM_THREADS) accept_pairs_kernel(
+    const float* __restrict__ ql, const float* __restrict__ pl, int V, double T, double top_p,
+    const int32_t* __restrict__ tok, uint64_t seed, const int64_t* __restrict__ sid,
+    const int64_t* __restrict__ ctr, double* scratch, int32_t* __restrict__ acc,
+    int32_t* __restrict__ corr) {
+    __shared__ ShapeSmem sm;
+    const int i = blockIdx.x;
+    Pcg64 g = pcg64_from_key(seed, uint64_t(sid[i]), 1u, uint64_t(ctr[i]));
+    const int c = accept_block(ql + (int64_t)i * V, pl + (int64_t)i * V, V, T, top_p,
+                               scratch + (int64_t)i * 2 * V, scratch + (int64_t)i * 2 * V + V, tok[i],
+                               g, sm);
+    if (threadIdx.x == 0) {
+        acc[i] = c == -1;
+        corr[i] = c;
+    }
+}
+
+static __global__ void rng_kernel(int n, uint64_t seed, const int64_t* sid, const int32_t* role,
+                           const int64_t* ctr, double* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Pcg64 g = pcg64_from_key(seed, uint64_t(sid[i]), uint32_t(role[i]), uint64_t(ctr[i]));
+    out[2 * i] = pcg64_double(g);
+    out[2 * i + 1] = pcg64_double(g);
+}
+
+// ------------------------------------------------------ engine step logic
+
+struct SlotStep {                 // device -> host, one per active sequence
+    int32_t accepted, n_emit, reason, err;   // reason: -1 running, 0 eos, 1 length
+    int32_t tok[kMaxEmit];
+    double lp[kMaxEmit];
+};
+
+struct StepArgs {
+    int nA, l, V;
+    const int32_t* slot;          // [nA]
+    const int32_t* committed;     // [nA] committed length C at step start
+    const int32_t* generated;     // [nA] generated count at step start
+    const int32_t* proposals;     // [slot][pstride]
+    int pstride;
+    const float* vlog;            // verify logits [nA*(l+1), V]
+    const int32_t* vamax;         // argmax per verify row
+    const double* vlse;           // lse per verify row
+    int max_new, eos;
+    // sampled
+    const int32_t* acc_flag;      // [nA*(l+1)]
+    const int32_t* corr;          // [nA*(l+1)]
+    const int32_t* bonus_tok;     // [nA]
+    int greedy;
+    SlotStep* out;
+};
+
+// accepted prefix + correction / bonus + EOS/length finalize + logprobs
+// (ref:engine.py:276-349, _finalize_emitted :103-117, logprob :99-100)
+static __global__ void finalize_kernel(StepArgs a) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.nA) return;
+    const int slot = a.slot[i], l = a.l, rb = i * (l + 1);
+    int em[kMaxEmit];
+    int x = 0, n = 0, err = 0;
+    for (int j = 0; j < l; ++j) {
+        const int t = a.proposals[slot * a.pstride + j];
+        if (a.greedy) {
+            const int am = a.vamax[rb + j];
+            if (t == am) { em[n++] = t; ++x; }
+            else { em[n++] = am; break; }
+        } else {
+            if (a.acc_flag[rb + j]) { em[n++] = t; ++x; }
+            else {
+                const int c = a.corr[rb + j];
+                if (c < 0) err = c;
+                em[n++] = c < 0 ? 0 : c;
+                break;
+            }
+        }
+    }
+    const int remaining = a.max_new - a.generated[i];
+    if (x == l) {
+        bool eos_hit = false;
+        for (int j = 0; j < n; ++j) eos_hit |= (a.eos >= 0 && em[j] == a.eos);
+        if (!eos_hit && remaining > l) {
+            int b;
+            if (a.greedy) b = a.vamax[rb + l];
+            else {
+                const int c = a.corr[rb + l];
+                b = a.acc_flag[rb + l] ? a.bonus_tok[i] : c;
+                if (!a.acc_flag[rb + l] && c < 0) { err = c; b = 0; }
+            }
+            em[n++] = b;
+        }
+    }
+    int reason = -1;
+    if (a.eos >= 0) {
+        for (int j = 0; j < n; ++j)
+            if (em[j] == a.eos) { n = j + 1; reason = 0; break; }
+    }
+    if (n > remaining) { n = remaining; reason = 1; }
+    else if (n == remaining && reason < 0) reason = 1;
+    SlotStep& o = a.out[i];
+    o.accepted = x;
+    o.n_emit = n;
+    o.reason = reason;
+    o.err = err;
+    for (int j = 0; j < n; ++j) {
+        o.tok[j] = em[j];
+        o.lp[j] = double(a.vlog[(int64_t)(rb + j) * a.V + em[j]]) - a.vlse[rb + j];
+    }
+}
+
+// sampled verify: one CTA per (sequence, position j <= l).  j < l tests the
+// proposal against (q_j, p_j); j == l draws the bonus token from the bonus
+// draft row and tests it (ref:engine.py:292-343).
+struct VerifyArgs {
+    int nA, l, V;
+    double T, top_p;
+    uint64_t seed;
+    const int32_t* slot;
+    const int32_t* sid;           // by slot
+    const int32_t* committed;     // [nA]
+    const int32_t* proposals;
+    int pstride;
+    const float* vlog;            // [nA*(l+1), V]
+    const float* dlog;            // draft rows: row (j, i) at dlog + (j*nA + i)*V, j <= l
+    double* scratch;              // [nA*(l+1), 2, V]
+    int32_t* acc_flag;
+    int32_t* corr;
+    int32_t* bonus_tok;
+};
+
+static __global__ void __launch_bounds__(SM_THREADS) verify_sampled_kernel(VerifyArgs a) {
+    __shared__ ShapeSmem sm;
+    const int j = blockIdx.x, i = blockIdx.y, l = a.l;
+    const int slot = a.slot[i], sid = a.sid[slot], pos = a.committed[i] + j;
+    const float* q = a.vlog + (int64_t)(i * (l + 1) + j) * a.V;
+    const float* p = a.dlog + (int64_t)(j * a.nA + i) * a.V;
+    double* eq = a.scratch + (int64_t)(i * (l + 1) + j) * 2 * a.V;
+    double* ep = eq + a.V;
+    int tok;
+    if (j < l) {
+        tok = a.proposals[slot * a.pstride + j];
+    } else {
+        shape_row(p, a.V, a.T, a.top_p, ep, sm);
+        const Shaped sp = sm.sh;
+        Pcg64 gd = pcg64_from_key(a.seed, uint64_t(sid), 0u, uint64_t(pos));
+        const double ub = pcg64_double(gd);
+        tok = inverse_cdf_block(a.V, ub, [&](int k) { return sh_prob(sp, p, ep, k); }, sm);
+        __syncthreads();
+    }
+    Pcg64 g = pcg64_from_key(a.seed, uint64_t(sid), 1u, uint64_t(pos));
+    const int c = accept_block(q, p, a.V, a.T, a.top_p, eq, ep, tok, g, sm);
+    if (threadIdx.x == 0) {
+        a.acc_flag[i * (l + 1) + j] = c == -1;
+        a.corr[i * (l + 1) + j] = c;
+        if (j == l) a.bonus_tok[i] = tok;
+    }
+}
+
+// regular decoding: pick one token per active sequence from its current
+// logits row (ref:engine.py:151-163); writes proposals[slot][0] for the next
+// forward's token indirection.
+struct RegularArgs {
+    const int32_t* slot;
+    const int32_t* sid;           // by slot
+    const int32_t* pos;           // [nA] absolute position of the new token
+    int32_t* proposals;
+    int pstride;
+    int V;
+    double T, top_p;
+    uint64_t seed;
+    double* scratch;
+    int32_t* tok_out;
+    double* lp_out;
+};
+
+static __global__ void __launch_bounds__(SM_THREADS) regular_pick_kernel(const float* __restrict__ logits,
+                                                                  RegularArgs a) {
+    __shared__ ShapeSmem sm;
+    const int i = blockIdx.x;
+    const float* row = logits + (int64_t)i * a.V;
+    double* e = a.scratch + (int64_t)i * a.V;
+    // lse of the raw row (logprob uses unshaped logits, ref:engine.py:162)
+    ArgMax mx{-INFINITY, 0x7fffffff};
+    for (int k = threadIdx.x; k < a.V; k += blockDim.x) mx = better(mx, ArgMax{row[k], k});
+    mx = block_argmax(mx, sm.fred, sm.ired);
+    double s = 0.0;
+    for (int k = threadIdx.x; k < a.V; k += blockDim.x) s += exp(double(row[k]) - double(mx.v));
+    s = block_sum(s, sm.dred);
+    const double lse = double(mx.v) + log(s);
+    int tok;
+    if (a.T == 0.0) {
+        tok = mx.i;
+    } else {
+        shape_row(row, a.V, a.T, a.top_p, e, sm);
+        const Shaped sh = sm.sh;
+        const int slot = a.slot[i];
+        Pcg64 g = pcg64_from_key(a.seed, uint64_t(a.sid[slot]), 1u, uint64_t(a.pos[i]));
+        const double u = pcg64_double(g);
+        tok = inverse_cdf_block(a.V, u, [&](int k) { return sh_prob(sh, row, e, k); }, sm);
+    }
+    if (threadIdx.x == 0) {
+        a.tok_out[i] = tok;
+        a.lp_out[i] = double(row[tok]) - lse;
+        a.proposals[a.slot[i] * a.pstride] = tok;
+    }
+}
+
+}  // namespace bass

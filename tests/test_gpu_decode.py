@@ -1,0 +1,263 @@
+"""GPU parity of the full hot path: ragged forward (teacher-forced logits) and
+the decode loops (device-resident and host-loop paths) against the
+reference's golden runs and the oracle.
+
+Parity ladder: fp32 mode (true FFMA) reproduces the fp64
+reference's tokens exactly; bf16 mode matches the oracle fed the same
+bf16-rounded weights within 1e-2 relative per logits row, and bf16 greedy
+speculative == bf16 greedy regular on the GPU.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import engine as OE
+from oracle import ragged as OR
+
+pytestmark = pytest.mark.gpu
+
+TINY = OR.Geometry(2, 4, 64, 16, 96, 256)
+C1_MAIN = OR.Geometry(2, 4, 128, 32, 512, 1024)
+C1_DRAFT = OR.Geometry(1, 4, 128, 32, 512, 1024)
+
+
+def _load(golden_dir, name):
+    with open(os.path.join(golden_dir, name)) as fh:
+        return json.load(fh)
+
+
+@pytest.fixture(scope="module")
+def B():
+    import paper_2404_15778_b200 as B
+    return B
+
+
+def _bf16_round(w):
+    import torch
+    out = {}
+    for k, v in w.items():
+        if k == "layers":
+            out[k] = [{kk: torch.tensor(vv).bfloat16().double().numpy() if kk.startswith("w")
+                       else vv for kk, vv in lay.items()} for lay in v]
+        elif isinstance(v, np.ndarray) and k in ("tok_emb", "pos_emb", "head"):
+            out[k] = torch.tensor(v).bfloat16().double().numpy()
+        else:
+            out[k] = v
+    return out
+
+
+@pytest.mark.parametrize("strategy", ["pad", "split", "ragged"])
+def test_forward_fp32_matches_reference_golden(B, golden_dir, strategy):
+    z = np.load(os.path.join(golden_dir, "forward.npz"))
+    meta = _load(golden_dir, "forward.json")
+    w = OR.init_weights(TINY, 5)
+    m = B.CudaModel(B.DeviceWeights.from_reference(w, "fp32"), 4, strategy)
+    for s, p in enumerate(meta["prompts"]):
+        got = m.prefill(s, p)
+        want = z[f"pad_prefill_{s}"]
+        assert np.abs(got - want).max() <= 1e-5 * np.abs(want).max()
+    outs = m.forward([0, 1, 2, 3], meta["blocks"])
+    for s in range(4):
+        want = z[f"pad_block_{s}"]
+        assert outs[s].shape == want.shape
+        assert np.abs(outs[s] - want).max() <= 1e-5 * np.abs(want).max()
+    assert m.lengths() == [7, 8, 11, 4]
+
+
+def test_forward_bf16_within_1e2_of_oracle_on_rounded_weights(B):
+    g = OR.Geometry(4, 8, 512, 64, 2048, 512)
+    w = _bf16_round(OR.init_weights(g, 11))
+    rng = np.random.default_rng(4)
+    prompts = [rng.integers(0, 2048, n).tolist() for n in (40, 7, 120, 64)]
+    blocks = [rng.integers(0, 2048, n).tolist() for n in (8, 8, 1, 33)]
+    om = OE.OracleModel(w, 4)
+    dm = B.CudaModel(B.DeviceWeights.from_reference(w, "bf16"), 4)
+    for s, p in enumerate(prompts):
+        om.prefill(s, p)
+        dm.prefill(s, p)
+    ref = om.forward([0, 1, 2, 3], blocks)
+    got = dm.forward([0, 1, 2, 3], blocks)
+    worst = 0.0
+    for a, b in zip(got, ref):
+        err = np.abs(a - b).max(axis=1) / np.abs(b).max(axis=1)
+        worst = max(worst, float(err.max()))
+    assert worst < 1e-2, worst
+
+
+def test_forward_batch_invariance_and_block_equals_sequential(B):
+    g = OR.Geometry(2, 4, 256, 64, 1000, 256)
+    w = OR.init_weights(g, 3)
+    dw = B.DeviceWeights.from_reference(w, "bf16")
+    a, b = B.CudaModel(dw, 3), B.CudaModel(dw, 3)
+    for m in (a, b):
+        m.prefill(0, [1, 2, 3])
+        m.prefill(1, [4, 5])
+        m.prefill(2, [9, 9, 9, 9])
+    together = a.forward([0, 1, 2], [[7, 8, 9], [11], [3, 4]])
+    alone = [b.forward([s], [t])[0] for s, t in ((0, [7, 8, 9]), (1, [11]), (2, [3, 4]))]
+    for x, y in zip(together, alone):
+        assert np.array_equal(x, y)          # bitwise: row-independent kernels
+    c = B.CudaModel(dw, 1)
+    c.prefill(0, [1, 2, 3])
+    seq = [c.forward([0], [[t]])[0][0] for t in (7, 8, 9)]
+    assert np.array_equal(np.stack(seq), together[0])
+
+
+def test_rollback_then_reappend_is_bitwise(B):
+    g = OR.Geometry(2, 4, 128, 32, 300, 128)
+    dw = B.DeviceWeights.from_reference(OR.init_weights(g, 1), "bf16")
+    m = B.CudaModel(dw, 1)
+    m.prefill(0, [5, 6, 7])
+    first = m.forward([0], [[1, 2, 3, 4]])[0]
+    m.rollback(0, 3)
+    assert m.length(0) == 3
+    again = m.forward([0], [[1, 2, 3, 4]])[0]
+    assert np.array_equal(first, again)
+    with pytest.raises(ValueError):
+        m.rollback(0, 99)
+
+
+def test_error_contracts(B):
+    g = OR.Geometry(1, 2, 64, 32, 64, 8)
+    m = B.CudaModel(B.DeviceWeights.from_reference(OR.init_weights(g, 1), "fp32"), 1)
+    with pytest.raises(ValueError, match="empty prompt"):
+        m.prefill(0, [])
+    m.prefill(0, [1, 2])
+    with pytest.raises(ValueError, match="cached context"):
+        m.prefill(0, [1, 2])
+    with pytest.raises(ValueError, match="max_seq_len"):
+        m.forward([0], [[1] * 9])
+    with pytest.raises(ValueError, match="vocab"):
+        m.forward([0], [[99]])
+
+
+def _check(res, ref, steps=True):
+    assert res.tokens == ref["tokens"]
+    assert res.finish_reason == ref["finish_reason"]
+    assert res.completion_step == ref["completion_step"]
+    assert res.main_forward_calls == ref["main_calls"]
+    assert res.draft_forward_calls == ref["draft_calls"]
+    for a, b in zip(res.logprobs, ref["logprobs"]):
+        np.testing.assert_allclose(a, b, rtol=0, atol=2e-4)
+    if steps:
+        assert len(res.steps) == len(ref["steps"])
+        for s, r in zip(res.steps, ref["steps"]):
+            assert s.draft_length == r["draft_length"]
+            assert list(s.slots) == r["slots"]
+            assert list(s.accepted) == r["accepted"]
+            assert [list(e) for e in s.emitted] == r["emitted"]
+            assert list(s.finished) == r["finished"]
+            assert list(s.kv_lengths) == r["kv_lengths"]
+
+
+@pytest.mark.parametrize("strategy", ["pad", "split"])
+def test_c1_greedy_device_path_matches_reference(B, golden_dir, strategy):
+    d = _load(golden_dir, "decode.json")
+    wm, wd = OR.init_weights(C1_MAIN, 0), OR.init_weights(C1_DRAFT, 1)
+    dwm, dwd = B.DeviceWeights.from_reference(wm, "fp32"), B.DeviceWeights.from_reference(wd, "fp32")
+    req = B.GenerationRequest(d["c1_prompts"], 64, temperature=0.0)
+    reg = B.decode_regular(B.CudaModel(dwm, 4, strategy), req)
+    _check(reg, d["runs"][f"c1_regular_{strategy}"], steps=False)
+    main, draft = B.CudaModel(dwm, 4, strategy), B.CudaModel(dwd, 4, strategy)
+    spec = B.decode_speculative(main, draft, req, B.FixedDraftController(4))
+    _check(spec, d["runs"][f"c1_spec_{strategy}"])
+    for s in range(4):
+        committed = len(d["c1_prompts"][s]) + len(spec.tokens[s])
+        assert main.length(s) == committed - 1
+        assert committed - 2 <= draft.length(s) <= committed - 1
+
+
+def test_c1_synthetic_aligned_draft_host_loop(B, golden_dir):
+    d = _load(golden_dir, "decode.json")
+    dwm = B.DeviceWeights.from_reference(OR.init_weights(C1_MAIN, 0), "fp32")
+    req = B.GenerationRequest(d["c1_prompts"], 64, temperature=0.0)
+    spec = B.decode_speculative(B.CudaModel(dwm, 4), B.CudaAlignedDraft(dwm, 0.8, 17, 4), req,
+                                B.AdaptiveDraftController())
+    _check(spec, d["runs"]["c1_spec_synth08"])
+
+
+def test_tiny_sampled_device_path_matches_reference(B, golden_dir):
+    d = _load(golden_dir, "decode.json")
+    tw = B.DeviceWeights.from_reference(OR.init_weights(TINY, 1234), "fp32")
+    req = B.GenerationRequest(d["tiny_prompts"], 12, temperature=0.7, top_p=0.9, seed=1234)
+    res = B.decode_regular(B.CudaModel(tw, 2), req)
+    _check(res, d["runs"]["tiny_regular_sampled"], steps=False)
+    assert res.tokens == [[38, 32, 87, 74, 67, 27, 25, 29, 14, 19, 1, 62],
+                          [76, 95, 58, 30, 94, 4, 73, 41, 86, 32, 41, 19]]
+    dw = B.DeviceWeights.from_reference(OR.init_weights(OR.Geometry(1, 4, 64, 16, 96, 256), 99),
+                                        "fp32")
+    sreq = B.GenerationRequest(d["eos_prompts"], 30, temperature=1.0, top_p=0.95, seed=8,
+                               eos_token=7, sequence_ids=[5, 0, 11])
+    ctl = B.AdaptiveDraftController(B.DraftLengthParams(l0=3, incre=2, mod=10, limit=8))
+    spec = B.decode_speculative(B.CudaModel(tw, 3), B.CudaModel(dw, 3), sreq, ctl)
+    _check(spec, d["runs"]["tiny_spec_sampled_realdraft"])
+    reg = B.decode_regular(B.CudaModel(tw, 3), sreq)
+    _check(reg, d["runs"]["tiny_regular_sampled_eos"], steps=False)
+
+
+def test_tiny_sampled_synthetic_host_loop(B, golden_dir):
+    d = _load(golden_dir, "decode.json")
+    tw = B.DeviceWeights.from_reference(OR.init_weights(TINY, 1234), "fp32")
+    req = B.GenerationRequest(d["tiny_prompts"], 40, temperature=0.7, top_p=0.9, seed=1234)
+    spec = B.decode_speculative(B.CudaModel(tw, 2), B.CudaAlignedDraft(tw, 0.8, 1234 + 17, 2), req,
+                                B.AdaptiveDraftController())
+    _check(spec, d["runs"]["tiny_spec_sampled"])
+
+
+def test_device_and_host_loops_agree_sampled(B):
+    """The device-resident loop and the host loop over the same CudaModels."""
+    from paper_2404_15778_b200 import engine as E
+    g = OR.Geometry(2, 4, 128, 32, 700, 256)
+    gd = OR.Geometry(1, 4, 128, 32, 700, 256)
+    dwm = B.DeviceWeights.from_reference(OR.init_weights(g, 21), "bf16")
+    dwd = B.DeviceWeights.from_reference(OR.init_weights(gd, 22), "bf16")
+    rng = np.random.default_rng(9)
+    prompts = [rng.integers(0, 700, int(n)).tolist() for n in (5, 17, 9, 30)]
+    for temp, top_p in ((0.0, 1.0), (0.9, 0.95), (0.3, 0.8)):
+        req = B.GenerationRequest(prompts, 24, temperature=temp, top_p=top_p, seed=3, eos_token=11)
+        dev = B.decode_speculative(B.CudaModel(dwm, 4), B.CudaModel(dwd, 4), req,
+                                   B.AdaptiveDraftController(B.DraftLengthParams(l0=4, limit=12)))
+        host = E._host_speculative(B.CudaModel(dwm, 4), B.CudaModel(dwd, 4), req,
+                                   B.AdaptiveDraftController(B.DraftLengthParams(l0=4, limit=12)))
+        assert dev.tokens == host.tokens
+        assert [s.accepted for s in dev.steps] == [s.accepted for s in host.steps]
+        assert dev.draft_forward_calls == host.draft_forward_calls
+
+
+def test_bf16_greedy_speculative_equals_regular(B):
+    g = OR.Geometry(4, 8, 512, 64, 4096, 512)
+    gd = OR.Geometry(1, 8, 512, 64, 4096, 512)
+    dwm = B.DeviceWeights.from_reference(OR.init_weights(g, 7), "bf16")
+    dwd = B.DeviceWeights.from_reference(OR.init_weights(gd, 8), "bf16")
+    rng = np.random.default_rng(2)
+    prompts = [rng.integers(0, 4096, int(n)).tolist() for n in rng.integers(4, 60, 8)]
+    req = B.GenerationRequest(prompts, 48, temperature=0.0)
+    base = B.decode_regular(B.CudaModel(dwm, 8), req)
+    spec = B.decode_speculative(B.CudaModel(dwm, 8), B.CudaModel(dwd, 8), req,
+                                B.AdaptiveDraftController())
+    assert spec.tokens == base.tokens
+    # self-draft (draft = main weights): everything accepted, still identical
+    spec2 = B.decode_speculative(B.CudaModel(dwm, 8), B.CudaModel(dwm, 8), req,
+                                 B.AdaptiveDraftController())
+    assert spec2.tokens == base.tokens
+    assert sum(sum(s.accepted) for s in spec2.steps) > 0
+
+
+def test_engine_validation_messages(B):
+    g = OR.Geometry(1, 2, 64, 32, 64, 40)
+    dw = B.DeviceWeights.from_reference(OR.init_weights(g, 2), "fp32")
+    req = B.GenerationRequest([[1, 2, 3]], 20, temperature=0.0)
+    with pytest.raises(ValueError, match="context overflow"):
+        B.decode_speculative(B.CudaModel(dw, 1), B.CudaModel(dw, 1), req,
+                             B.AdaptiveDraftController())
+    g2 = OR.Geometry(1, 2, 64, 32, 80, 40)
+    dw2 = B.DeviceWeights.from_reference(OR.init_weights(g2, 2), "fp32")
+    with pytest.raises(ValueError, match="vocab"):
+        B.decode_speculative(B.CudaModel(dw, 1), B.CudaModel(dw2, 1), req,
+                             B.AdaptiveDraftController())
+    with pytest.raises(ValueError, match="max_seq_len"):
+        B.decode_regular(B.CudaModel(dw, 1), B.GenerationRequest([list(range(30))], 20))
