@@ -63,6 +63,14 @@ int         bass_ctx_sync(bass_ctx* ctx);
 const char* bass_last_error(const bass_ctx* ctx);
 /* number of kernels this context has launched so far (for gpu_launches) */
 int64_t     bass_ctx_launches(const bass_ctx* ctx);
+/* host<->device bytes this context has copied (per-step metadata, results) */
+int         bass_ctx_transfer_bytes(const bass_ctx* ctx, int64_t* h2d, int64_t* d2h);
+/* per-kernel-class device timing with CUDA events on the context stream:
+ * class 0 GEMM, 1 attention, 2 norm/embed, 3 sampling/accept.  enable resets
+ * the counters; read returns launches, total ms, algorithmic bytes, flops. */
+int         bass_ctx_profile(bass_ctx* ctx, int enable);
+int         bass_ctx_profile_read(bass_ctx* ctx, int cls, int64_t* launches,
+                                  double* ms, double* bytes, double* flops);
 
 /* Model weights live in device memory owned by the model.
  * Replaces ModelWeights/init_model (ref:model.py:87-132). */

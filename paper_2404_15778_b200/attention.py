@@ -52,9 +52,11 @@ def attend_device(ctx, q, k, v, cu_q, offsets, strategy=AttentionStrategy.RAGGED
     n_seq, H, stride, dh = k.shape
     cu = np.ascontiguousarray(np.asarray(cu_q, dtype=np.int32))
     off = np.ascontiguousarray(np.asarray(offsets, dtype=np.int32))
-    if out is None:
-        out = torch.empty_like(q)
     q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    if out is None:
+        out = torch.empty(q.shape, dtype=q.dtype, device=q.device)
+    if not out.is_contiguous():
+        raise ValueError("out must be contiguous")
     torch.cuda.synchronize(q.device)
     ctx.check(ctx.lib.bass_attention(ctx.handle, strategy_code(strategy), code, n_seq, H, dh,
                                      L.ptr(cu, C.c_int32), L.ptr(off, C.c_int32),

@@ -66,6 +66,7 @@ void up(bass_ctx* c, void* dev, const void* src, size_t bytes) {
     }
     std::memcpy(h, src, bytes);
     BASS_CUDA(cudaMemcpyAsync(dev, h, bytes, cudaMemcpyHostToDevice, c->stream));
+    c->h2d_bytes += (int64_t)bytes;
 }
 
 // Algorithm 1 (ref:draft_control.py:49-69)
@@ -207,6 +208,7 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
             BASS_REQUIRE(r->align_tokens != nullptr, "align_tokens required when align >= 0");
             int32_t* at = (int32_t*)e->align_tok.need((size_t)b * maxnew * 4, st);
             BASS_CUDA(cudaMemcpyAsync(at, r->align_tokens, (size_t)b * maxnew * 4, cudaMemcpyHostToDevice, st));
+            c->h2d_bytes += (int64_t)b * maxnew * 4;
             d_align = at;
         }
         // the caches continue from their current lengths (fresh providers: 0,
@@ -290,6 +292,7 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                 up(c, d_pos, pos.data(), nA * 4);
                 DraftPick dp{d_slot, d_sid, d_pos, e->proposals, bass_engine::kPstride, j,
                              r->align, r->align_seed, d_align, d_plen, maxnew};
+                ProfScope prof(c, BASS_PROF_SAMPLE, (double)nA * V * 4);
                 if (greedy) draft_greedy_kernel<<<nA, SM_THREADS, 0, st>>>(out, V, dp);
                 else draft_sample_kernel<<<nA, SM_THREADS, 0, st>>>(out, V, r->temperature, r->top_p, r->seed,
                                                                      scratch, dp);
@@ -313,11 +316,15 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                 main_calls += nA;
             }
             const int R = nA * (l + 1);
-            row_stats_kernel<<<R, SM_THREADS, 0, st>>>(vlog, V, vamax, vlse);
+            {
+                ProfScope prof(c, BASS_PROF_SAMPLE, (double)R * V * 4);
+                row_stats_kernel<<<R, SM_THREADS, 0, st>>>(vlog, V, vamax, vlse);
+            }
             launched(c);
             if (!greedy) {
                 VerifyArgs va{nA, l, V, r->temperature, r->top_p, r->seed, d_slot, d_sid, d_com,
                               e->proposals, bass_engine::kPstride, vlog, dlog, scratch, accf, corr, btok};
+                ProfScope prof(c, BASS_PROF_SAMPLE, (double)R * V * 8);
                 verify_sampled_kernel<<<dim3(l + 1, nA), SM_THREADS, 0, st>>>(va);
                 launched(c);
             }
@@ -325,6 +332,7 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                         maxnew, r->eos_token, accf, corr, btok, greedy ? 1 : 0, step_dev};
             finalize_kernel<<<(nA + 63) / 64, 64, 0, st>>>(sa);
             launched(c);
+            c->d2h_bytes += (int64_t)nA * sizeof(SlotStep);
             BASS_CUDA(cudaMemcpyAsync(e->step_host, step_dev, (size_t)nA * sizeof(SlotStep),
                                       cudaMemcpyDeviceToHost, st));
             c->sync();
@@ -454,8 +462,12 @@ int bass_regular_generate(bass_engine* e, const bass_gen_request* r, bass_gen_re
             up(c, d_pos, h.data() + nA, nA * 4);
             RegularArgs ra{d_slot, slot_tab, d_pos, e->proposals, bass_engine::kPstride, V, r->temperature,
                            r->top_p, r->seed, scratch, d_tok, d_lp};
-            regular_pick_kernel<<<nA, SM_THREADS, 0, st>>>(cur, ra);
+            {
+                ProfScope prof(c, BASS_PROF_SAMPLE, (double)nA * V * 4);
+                regular_pick_kernel<<<nA, SM_THREADS, 0, st>>>(cur, ra);
+            }
             launched(c);
+            c->d2h_bytes += (int64_t)nA * 12;
             BASS_CUDA(cudaMemcpyAsync(htok.data(), d_tok, nA * 4, cudaMemcpyDeviceToHost, st));
             BASS_CUDA(cudaMemcpyAsync(hlp.data(), d_lp, nA * 8, cudaMemcpyDeviceToHost, st));
             c->sync();

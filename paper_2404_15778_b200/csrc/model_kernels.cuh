@@ -207,8 +207,11 @@ __global__ void __launch_bounds__(AT_THREADS) attn_partial_kernel(
         __syncthreads();
         for (int i = threadIdx.x; i < AT_SUB * DH; i += AT_THREADS) {
             const int j = i / DH, cc = i % DH, s = s0 + j;
+            // keys past the sequence's own history are PAD's zero padding
+            // (ref:attention.py:116-121): never read, so stale cache rows
+            // (possibly NaN bit patterns) cannot leak through 0 * V.
             float kv = 0.f, vv = 0.f;
-            if (s < c_end) {
+            if (s < c_end && s < L) {
                 kv = ld(kc, (kvbase + s) * DH + cc);
                 vv = ld(vc, (kvbase + s) * DH + cc);
             }

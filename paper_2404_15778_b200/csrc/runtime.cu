@@ -55,9 +55,35 @@ void Batch::add_seq(int s, int offset, const int32_t* toks, int n) {
 
 }  // namespace bass
 
+cudaEvent_t bass_ctx::ev() {
+    if (!pool.empty()) {
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    BASS_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+void bass_ctx::resolve() {
+    for (const Pending& p : pending) {
+        float ms = 0.f;
+        BASS_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+        prof_ms[p.cls] += ms;
+        prof_bytes[p.cls] += p.bytes;
+        prof_flops[p.cls] += p.flops;
+        prof_n[p.cls] += 1;
+        pool.push_back(p.a);
+        pool.push_back(p.b);
+    }
+    pending.clear();
+}
+
 void bass_ctx::sync() {
     BASS_CUDA(cudaStreamSynchronize(stream));
     staging.used = 0;
+    if (!pending.empty()) resolve();
 }
 
 template <typename F>
@@ -93,6 +119,7 @@ static void upload_i32(bass_ctx* ctx, int32_t* dev, const int32_t* src, size_t n
     }
     std::memcpy(h, src, n * 4);
     BASS_CUDA(cudaMemcpyAsync(dev, h, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->h2d_bytes += (int64_t)n * 4;
 }
 
 // ------------------------------------------------------- weight kernels
@@ -145,6 +172,7 @@ namespace bass {
 template <typename TA>
 static void launch_layernorm(bass_model& m, const float* x, const int32_t* gather, const float* g,
                              const float* b, int rows, TA* out) {
+    ProfScope prof(m.ctx, BASS_PROF_NORM, (double)rows * m.g.d_model * (4.0 + sizeof(TA)));
     layernorm_kernel<TA><<<rows, 256, 0, m.ctx->stream>>>(x, gather, g, b, m.g.d_model, out);
     check_launch(m.ctx);
 }
@@ -162,8 +190,16 @@ static void gemm_simt(bass_model& m, const void* X, const void* W, int M, int N,
     check_launch(m.ctx);
 }
 
+// algorithmic bytes of one GEMM launch: weights + activations in + results out
+static double gemm_bytes(const bass_model& m, int mode, int M, int N, int K) {
+    const double es = (double)m.esize;
+    double out = mode == EPI_STORE ? 4.0 * M * N : mode == EPI_RESID ? 8.0 * M * N : es * M * N;
+    return es * N * K + es * M * K + out;
+}
+
 void gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K, const Epi& e) {
     if (M == 0) return;
+    ProfScope prof(m.ctx, BASS_PROF_GEMM, gemm_bytes(m, mode, M, N, K), 2.0 * M * N * K);
     const bool tc = m.dtype == BASS_BF16 && m.gemm_mode != BASS_GEMM_SIMT && tc_gemm_supported(m, N, K);
     if (m.gemm_mode == BASS_GEMM_TC && !tc)
         throw Error(BASS_ERR_STATE, "tcgen05 GEMM requested but unsupported for this shape/dtype");
@@ -221,6 +257,13 @@ static void launch_attention_t(bass_ctx* ctx, int strategy, const void* q, const
     seq_first[n_seq] = (int)work.size() / 2;
     AttnWork* wdev = (AttnWork*)work_buf.need(work.size() * 4, ctx->stream);
     upload_i32(ctx, (int32_t*)wdev, work.data(), work.size());
+    // algorithmic bytes: real K/V rows + Q in + O out
+    double abytes = 0.0, aflops = 0.0;
+    for (int i = 0; i < n_seq; ++i) {
+        abytes += (2.0 * H * (off[i] + qn[i]) * DH + 2.0 * H * qn[i] * DH) * sizeof(TA);
+        aflops += 4.0 * H * DH * qn[i] * (off[i] + 0.5 * (qn[i] + 1));
+    }
+    ProfScope prof(ctx, BASS_PROF_ATTN, abytes, aflops);
     const int threads = AT_THREADS;
     if (strategy == BASS_SPLIT) {
         for (int i = 0; i < n_seq; ++i) {
@@ -401,6 +444,34 @@ int bass_ctx_sync(bass_ctx* c) {
 const char* bass_last_error(const bass_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 int64_t bass_ctx_launches(const bass_ctx* c) { return c ? c->launches : 0; }
+
+int bass_ctx_transfer_bytes(const bass_ctx* c, int64_t* h2d, int64_t* d2h) {
+    *h2d = c->h2d_bytes;
+    *d2h = c->d2h_bytes;
+    return BASS_OK;
+}
+
+int bass_ctx_profile(bass_ctx* c, int enable) {
+    return guarded(c, [&] {
+        c->sync();
+        c->profile = enable != 0;
+        for (int i = 0; i < BASS_PROF_N; ++i) {
+            c->prof_ms[i] = c->prof_bytes[i] = c->prof_flops[i] = 0.0;
+            c->prof_n[i] = 0;
+        }
+    });
+}
+
+int bass_ctx_profile_read(bass_ctx* c, int cls, int64_t* launches, double* ms, double* bytes, double* flops) {
+    return guarded(c, [&] {
+        BASS_REQUIRE(cls >= 0 && cls < BASS_PROF_N, "unknown profile class");
+        c->sync();
+        *launches = c->prof_n[cls];
+        *ms = c->prof_ms[cls];
+        *bytes = c->prof_bytes[cls];
+        *flops = c->prof_flops[cls];
+    });
+}
 
 // ---------------------------------------------------------------- model
 int bass_model_create(bass_ctx* c, const bass_geometry* g, int dtype, bass_model** out) {

@@ -50,6 +50,10 @@ struct DevBuf {
 
 }  // namespace bass
 
+// Per-kernel-class device timing (CUDA events on the launching stream) with
+// the algorithmic bytes / flops of every timed launch; resolved at syncs.
+enum { BASS_PROF_GEMM = 0, BASS_PROF_ATTN = 1, BASS_PROF_NORM = 2, BASS_PROF_SAMPLE = 3, BASS_PROF_N = 4 };
+
 struct bass_ctx {
     int device = 0;
     int sm_count = 148;
@@ -57,9 +61,43 @@ struct bass_ctx {
     bool own_stream = false;
     std::string err;
     int64_t launches = 0;
+    int64_t h2d_bytes = 0, d2h_bytes = 0;
     bass::Staging staging;
+    // profiling
+    bool profile = false;
+    struct Pending { int cls; cudaEvent_t a, b; double bytes, flops; };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> pool;
+    double prof_ms[BASS_PROF_N] = {}, prof_bytes[BASS_PROF_N] = {}, prof_flops[BASS_PROF_N] = {};
+    int64_t prof_n[BASS_PROF_N] = {};
+    cudaEvent_t ev();
+    void resolve();
     void sync();
 };
+
+namespace bass {
+// RAII timer around one launch (no-op unless ctx->profile)
+struct ProfScope {
+    bass_ctx* c;
+    int cls;
+    double bytes, flops;
+    cudaEvent_t a = nullptr;
+    ProfScope(bass_ctx* c_, int cls_, double bytes_, double flops_ = 0)
+        : c(c_), cls(cls_), bytes(bytes_), flops(flops_) {
+        if (c->profile) {
+            a = c->ev();
+            cudaEventRecord(a, c->stream);
+        }
+    }
+    ~ProfScope() {
+        if (a) {
+            cudaEvent_t b = c->ev();
+            cudaEventRecord(b, c->stream);
+            c->pending.push_back({cls, a, b, bytes, flops});
+        }
+    }
+};
+}  // namespace bass
 
 struct bass_layer {
     float *ln1_g, *ln1_b, *ln2_g, *ln2_b;

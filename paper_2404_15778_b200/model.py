@@ -79,6 +79,31 @@ class CudaContext:
     def sync(self):
         self.check(self.lib.bass_ctx_sync(self.handle))
 
+    def set_stream(self, cuda_stream_ptr: int):
+        """Enqueue libbass work on a caller stream (e.g. torch.cuda.Stream.cuda_stream)."""
+        self.check(self.lib.bass_ctx_set_stream(self.handle, C.c_void_p(cuda_stream_ptr)))
+
+    def transfer_bytes(self) -> tuple[int, int]:
+        h, d = C.c_int64(), C.c_int64()
+        self.check(self.lib.bass_ctx_transfer_bytes(self.handle, C.byref(h), C.byref(d)))
+        return h.value, d.value
+
+    PROFILE_CLASSES = ("gemm", "attention", "norm", "sampling")
+
+    def profile(self, enable: bool):
+        """Start (and reset) / stop per-kernel-class CUDA-event timing."""
+        self.check(self.lib.bass_ctx_profile(self.handle, 1 if enable else 0))
+
+    def profile_read(self) -> dict:
+        out = {}
+        for i, name in enumerate(self.PROFILE_CLASSES):
+            n, ms, by, fl = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
+            self.check(self.lib.bass_ctx_profile_read(self.handle, i, C.byref(n), C.byref(ms),
+                                                      C.byref(by), C.byref(fl)))
+            out[name] = {"launches": n.value, "ms": ms.value, "bytes": by.value,
+                         "flops": fl.value}
+        return out
+
 
 def _dtype_code(dtype) -> int:
     if dtype in ("bf16", "bfloat16", L.BF16):
