@@ -106,6 +106,13 @@ int bass_forward_ragged(bass_model* m, bass_kv* kv, int n_seq,
                         const int32_t* tokens_host, int strategy,
                         int rows_mode, float* logits_host);
 
+/* Standalone projection GEMM with the forward's kernels (tests / microbench):
+ * Y[M, N] (fp32) = X[M, K] . W[N, K]^T with X, W in the model's dtype, all
+ * device pointers; gemm_mode BASS_GEMM_SIMT or BASS_GEMM_TC (tcgen05).
+ * ref:model.py:160-164 (_linear), output-major weights. */
+int bass_gemm(bass_model* m, int gemm_mode, int M, int N, int K,
+              const void* x_dev, const void* w_dev, float* y_dev);
+
 /* Standalone ragged attention (ref:attention.py:140-154 attend), for the
  * C4 sweep and kernel parity.  Layouts (device, dtype = BASS_BF16|F32):
  *   q, out : [cu_q[n], n_head, d_head]

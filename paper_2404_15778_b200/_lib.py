@@ -74,6 +74,7 @@ SIGNATURES = {
     "bass_kv_lengths": (C.c_int, [vp, i32p]),
     "bass_kv_truncate": (C.c_int, [vp, C.c_int, i32p, i32p]),
     "bass_forward_ragged": (C.c_int, [vp, vp, C.c_int, i32p, i32p, i32p, C.c_int, C.c_int, f32p]),
+    "bass_gemm": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp]),
     "bass_attention": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, i32p, i32p,
                                  vp, vp, vp, C.c_int, vp]),
     "bass_rng_uniforms": (C.c_int, [vp, C.c_int, C.c_uint64, i64p, i32p, i64p, f64p]),

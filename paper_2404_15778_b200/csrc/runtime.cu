@@ -712,6 +712,25 @@ int bass_forward_ragged(bass_model* m, bass_kv* kv, int n_seq, const int32_t* sl
 }
 
 // ------------------------------------------------------ standalone kernels
+int bass_gemm(bass_model* m, int mode, int M, int N, int K, const void* x, const void* w, float* y) {
+    return guarded(m->ctx, [&] {
+        BASS_REQUIRE(M >= 1 && N >= 1 && K >= 1, "geometry: GEMM sizes must be positive");
+        BASS_REQUIRE(mode == BASS_GEMM_SIMT || mode == BASS_GEMM_TC, "gemm mode must be SIMT or TC");
+        const int saved = m->gemm_mode;
+        m->gemm_mode = mode;
+        Epi e{};
+        e.out = y;
+        try {
+            gemm(*m, EPI_STORE, x, w, M, N, K, e);
+        } catch (...) {
+            m->gemm_mode = saved;
+            throw;
+        }
+        m->gemm_mode = saved;
+        m->ctx->sync();
+    });
+}
+
 int bass_attention(bass_ctx* c, int strategy, int dtype, int n_seq, int n_head, int d_head, const int32_t* cu_q,
                    const int32_t* offsets, const void* q, const void* k, const void* v, int kv_stride, void* out) {
     return guarded(c, [&] {

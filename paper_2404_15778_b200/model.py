@@ -177,6 +177,19 @@ class DeviceWeights:
         dw.ctx.check(dw.ctx.lib.bass_model_init_random(dw.handle, seed, std))
         return dw
 
+    def gemm(self, x, w, mode: int = L.GEMM_TC):
+        """Y = x @ w.T on the device with this model's GEMM kernels (torch
+        CUDA tensors in the model dtype, contiguous; returns fp32 [M, N])."""
+        import torch
+        M, K = x.shape
+        N = w.shape[0]
+        x, w = x.contiguous(), w.contiguous()
+        y = torch.empty((M, N), dtype=torch.float32, device=x.device)
+        torch.cuda.synchronize(x.device)
+        self.ctx.check(self.ctx.lib.bass_gemm(self.handle, mode, M, N, K, C.c_void_p(x.data_ptr()),
+                                              C.c_void_p(w.data_ptr()), C.c_void_p(y.data_ptr())))
+        return y
+
     def set_gemm(self, mode: int):
         self.ctx.check(self.ctx.lib.bass_model_set_gemm(self.handle, mode))
 
