@@ -90,6 +90,20 @@ SIGNATURES = {
 }
 
 _lib = None
+_alive = True
+
+
+def _at_exit():
+    global _alive
+    _alive = False   # process teardown: the driver reclaims device memory
+
+
+import atexit  # noqa: E402
+atexit.register(_at_exit)
+
+
+def alive() -> bool:
+    return _alive
 
 
 class BassError(RuntimeError):

@@ -17,6 +17,7 @@
 using namespace bass;
 
 struct bass_engine {
+    bass_ctx* ctx = nullptr;          // kept so destroy never touches a freed model
     bass_model* main = nullptr;
     bass_model* draft = nullptr;
     bass_kv* kv_main = nullptr;
@@ -126,6 +127,7 @@ int bass_engine_create(bass_model* mm, bass_kv* mkv, bass_model* dm, bass_kv* dk
         BASS_REQUIRE(mkv && mkv->m == mm, "main cache must belong to the main model");
         BASS_REQUIRE(dm == nullptr || (dkv && dkv->m == dm), "draft cache must belong to the draft model");
         bass_engine* e = new bass_engine();
+        e->ctx = mm->ctx;
         e->main = mm;
         e->draft = dm;
         e->kv_main = mkv;
@@ -142,7 +144,7 @@ int bass_engine_create(bass_model* mm, bass_kv* mkv, bass_model* dm, bass_kv* dk
 
 int bass_engine_destroy(bass_engine* e) {
     if (!e) return BASS_OK;
-    cudaStreamSynchronize(e->main->ctx->stream);
+    cudaStreamSynchronize(e->ctx->stream);
     cudaFree(e->proposals);
     cudaFreeHost(e->step_host);
     cudaFreeHost(e->small_host);

@@ -638,6 +638,7 @@ int bass_kv_create(bass_model* m, int n_slots, int capacity, bass_kv** out) {
         BASS_REQUIRE(capacity <= m->g.max_seq_len, "capacity exceeds max_seq_len");
         bass_kv* kv = new bass_kv();
         kv->m = m;
+        kv->ctx = m->ctx;
         kv->n_slots = n_slots;
         kv->cap = capacity;
         kv->len.assign(n_slots, 0);
@@ -650,7 +651,7 @@ int bass_kv_create(bass_model* m, int n_slots, int capacity, bass_kv** out) {
 
 int bass_kv_destroy(bass_kv* kv) {
     if (!kv) return BASS_OK;
-    cudaStreamSynchronize(kv->m->ctx->stream);
+    cudaStreamSynchronize(kv->ctx->stream);
     cudaFree(kv->k);
     cudaFree(kv->v);
     delete kv;

@@ -123,6 +123,7 @@ struct bass_model {
 
 struct bass_kv {
     bass_model* m = nullptr;
+    bass_ctx* ctx = nullptr;          // kept so destroy never touches a freed model
     int n_slots = 0, cap = 0;
     void *k = nullptr, *v = nullptr;  // [L][slot][H][cap][dh]
     std::vector<int32_t> len;

@@ -110,7 +110,7 @@ class CudaEngine:
 
     def __del__(self):
         try:
-            if getattr(self, "handle", None):
+            if getattr(self, "handle", None) and L.alive():
                 self.ctx.lib.bass_engine_destroy(self.handle)
                 self.handle = None
         except Exception:
@@ -211,15 +211,13 @@ def _device_pair(main, draft, controller) -> bool:
     return ok
 
 
-_ENGINES: dict = {}
-
-
 def _engine_for(main, draft):
-    key = (id(main), id(draft))
-    eng = _ENGINES.get(key)
-    if eng is None or eng.main is not main or eng.draft is not draft:
+    """One engine per (main, draft) pair, owned by the main provider."""
+    cache = main.__dict__.setdefault("_engines", {})
+    eng = cache.get(id(draft))
+    if eng is None or eng.draft is not draft:
         eng = CudaEngine(main, draft)
-        _ENGINES[key] = eng
+        cache[id(draft)] = eng
     return eng
 
 

@@ -199,7 +199,7 @@ class DeviceWeights:
 
     def __del__(self):
         try:
-            if getattr(self, "handle", None):
+            if getattr(self, "handle", None) and L.alive():
                 self.ctx.lib.bass_model_destroy(self.handle)
                 self.handle = None
         except Exception:
@@ -286,7 +286,7 @@ class CudaModel:
 
     def __del__(self):
         try:
-            if getattr(self, "kv", None):
+            if getattr(self, "kv", None) and L.alive():
                 self.ctx.lib.bass_kv_destroy(self.kv)
                 self.kv = None
         except Exception:
