@@ -11,6 +11,11 @@ namespace bass {
 
 constexpr int kWarp = 32;
 
+// Programmatic dependent launch: allow the next (PDL-launched) kernel in the
+// stream to start its prologue now; it still waits (griddepcontrol.wait) for
+// this grid's completion before touching our outputs.
+BASS_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // element access in either storage dtype; all math is fp32 (or fp64 for sampling)
 BASS_DEV float ld(const float* p, int64_t i) { return p[i]; }
 BASS_DEV float ld(const __nv_bfloat16* p, int64_t i) { return __bfloat162float(p[i]); }

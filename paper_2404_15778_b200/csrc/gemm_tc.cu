@@ -156,11 +156,25 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
     fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    // PDL: let the next kernel's CTAs start their own prologue / weight
+    // prefetch as soon as SMs free up
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (warp == 0) {
         if (lane == 0) {   // ---- TMA producer
-            for (int i = 0; i < nit; ++i) {
+            // Weights do not depend on the previous kernel: fill the ring with
+            // W tiles first, then wait for the producer of X (griddepcontrol)
+            const int pre = nit < C::STAGES ? nit : C::STAGES;
+            for (int i = 0; i < pre; ++i) {
+                const uint32_t full = su32(&bars[i]);
+                mbar_expect_tx(full, C::STAGE);
+                tma_2d(&tw, base + i * C::STAGE, full, (it0 + i) * BK, n0);
+            }
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            for (int i = 0; i < pre; ++i)
+                tma_2d(&tx, base + i * C::STAGE + C::W_BYTES, su32(&bars[i]), (it0 + i) * BK, m0);
+            for (int i = pre; i < nit; ++i) {
                 const int s = i % C::STAGES;
-                if (i >= C::STAGES) mbar_wait(su32(&bars[C::STAGES + s]), ((i / C::STAGES) - 1) & 1);
+                mbar_wait(su32(&bars[C::STAGES + s]), ((i / C::STAGES) - 1) & 1);
                 const uint32_t full = su32(&bars[s]);
                 const uint32_t st = base + s * C::STAGE;
                 mbar_expect_tx(full, C::STAGE);
@@ -190,6 +204,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
     }
 
     // ---- epilogue: TMEM lane = weight row n0 + 32*warp + lane; columns = tokens
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // previous kernel's writes visible
     mbar_wait(su32(&bars[2 * C::STAGES]), 0);
     fence_after();
     const int n = n0 + warp * 32 + lane;
@@ -293,23 +308,14 @@ static State& state(bass_model& m) {
 
 // Split count from (N, K) only — never from M — so a row's reduction order
 // (and hence its bits) does not depend on how many rows share the launch.
+// Policy: the largest split (<= 8, >= 4 k-blocks per CTA) that still fits in
+// one wave of co-resident CTAs (2 per SM); more tiles than that -> no split.
 static int choose_splits(int sm_count, int N, int K) {
     const int n_tiles = (N + BN - 1) / BN, k_iters = K / BK;
     const int slots = 2 * sm_count;
-    const double m_ref = 64.0;
-    double best = 1e300;
     int best_s = 1;
-    for (int s = 1; s <= 8; ++s) {
-        if (k_iters / s < 4) break;
-        const int units = n_tiles * s;
-        const double waves = (units + slots - 1) / slots;
-        const double per_cta = (double)BN * ((double)K / s) * 2.0 + (s > 1 ? m_ref * BN * 4.0 * 2.0 : 0.0);
-        const double cost = waves * per_cta;
-        if (cost < best * 0.999) {
-            best = cost;
-            best_s = s;
-        }
-    }
+    for (int s = 2; s <= 8; ++s)
+        if (n_tiles * s <= slots && k_iters / s >= 4) best_s = s;
     return best_s;
 }
 
@@ -322,8 +328,17 @@ static void launch(bass_model& m, const CUtensorMap& wm, const CUtensorMap& xm, 
         BASS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<TT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
         attr = true;
     }
-    dim3 grid((N + BN - 1) / BN, sp.S, (M + TT - 1) / TT);
-    gemm_tc_kernel<TT, MODE><<<grid, THREADS, C::SMEM, m.ctx->stream>>>(wm, xm, M, N, sp, e);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((N + BN - 1) / BN, sp.S, (M + TT - 1) / TT);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = m.ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    BASS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TT, MODE>, wm, xm, M, N, sp, e));
 }
 
 template <int TT>

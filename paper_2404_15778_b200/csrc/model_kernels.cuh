@@ -30,6 +30,7 @@ template <typename TW>
 __global__ void embed_kernel(const TW* __restrict__ tok_emb, const TW* __restrict__ pos_emb,
                              Rows rows, const int32_t* __restrict__ proposals, int pstride,
                              int d, float* __restrict__ x) {
+    pdl_trigger();
     const int r = blockIdx.x;
     int id = rows.tok[r];
     if (id < 0) id = proposals[rows.slot[r] * pstride + (-id - 1)];
@@ -41,26 +42,58 @@ __global__ void embed_kernel(const TW* __restrict__ tok_emb, const TW* __restric
 // ------------------------------------------------------------- layernorm
 // (x - mean) / sqrt(var + eps) * g + b, population variance, two passes
 // (ref:model.py:150-153).  Optional row gather (final LN of selected rows).
+// Single pass over HBM: the row is held in registers (NV float4 per thread,
+// all loads issued before the first reduction), so the kernel is bound by one
+// read of x and one write of the normalised row rather than by load latency.
+constexpr int LN_THREADS = 256, LN_NV = 8;   // d <= 8192 with 16-byte rows
+
 template <typename TA>
-__global__ void layernorm_kernel(const float* __restrict__ x, const int32_t* __restrict__ gather,
-                                 const float* __restrict__ g, const float* __restrict__ b, int d,
-                                 TA* __restrict__ out) {
+__global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(const float* __restrict__ x,
+                                                               const int32_t* __restrict__ gather,
+                                                               const float* __restrict__ g,
+                                                               const float* __restrict__ b, int d,
+                                                               TA* __restrict__ out) {
     __shared__ float red[33];
+    pdl_trigger();
     const int r = blockIdx.x;
     const int src = gather ? gather[r] : r;
-    const float* xr = x + (int64_t)src * d;
+    const float4* xr = reinterpret_cast<const float4*>(x + (int64_t)src * d);
+    const int n4 = d >> 2;
+    float4 v[LN_NV];
     float s = 0.f;
-    for (int c = threadIdx.x; c < d; c += blockDim.x) s += xr[c];
-    const float mean = block_sum(s, red) / float(d);
-    float v = 0.f;
-    for (int c = threadIdx.x; c < d; c += blockDim.x) {
-        float t = xr[c] - mean;
-        v += t * t;
+#pragma unroll
+    for (int i = 0; i < LN_NV; ++i) {
+        const int c = threadIdx.x + i * LN_THREADS;
+        v[i] = c < n4 ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    const float var = block_sum(v, red) / float(d);
+#pragma unroll
+    for (int i = 0; i < LN_NV; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+    const float mean = block_sum(s, red) / float(d);
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < LN_NV; ++i) {
+        const int c = threadIdx.x + i * LN_THREADS;
+        if (c < n4) {
+            const float a = v[i].x - mean, bb = v[i].y - mean, cc = v[i].z - mean, dd = v[i].w - mean;
+            q += (a * a + bb * bb) + (cc * cc + dd * dd);
+        }
+    }
+    const float var = block_sum(q, red) / float(d);
     const float rstd = 1.0f / sqrtf(var + kLnEps);
-    for (int c = threadIdx.x; c < d; c += blockDim.x)
-        st(out, (int64_t)r * d + c, (xr[c] - mean) * rstd * g[c] + b[c]);
+    const float4* g4 = reinterpret_cast<const float4*>(g);
+    const float4* b4 = reinterpret_cast<const float4*>(b);
+#pragma unroll
+    for (int i = 0; i < LN_NV; ++i) {
+        const int c = threadIdx.x + i * LN_THREADS;
+        if (c < n4) {
+            const float4 gg = g4[c], bv = b4[c];
+            const int64_t o = (int64_t)r * d + 4 * c;
+            st(out, o + 0, (v[i].x - mean) * rstd * gg.x + bv.x);
+            st(out, o + 1, (v[i].y - mean) * rstd * gg.y + bv.y);
+            st(out, o + 2, (v[i].z - mean) * rstd * gg.z + bv.z);
+            st(out, o + 3, (v[i].w - mean) * rstd * gg.w + bv.w);
+        }
+    }
 }
 
 // ------------------------------------------------------------- epilogues
@@ -174,6 +207,7 @@ __global__ void __launch_bounds__(AT_THREADS) attn_partial_kernel(
     float* Vs = Kt + DH * (AT_SUB + 1);                // [AT_SUB][DH]
     float* Qs = Vs + AT_SUB * DH;                      // [AT_QT][DH]
 
+    pdl_trigger();
     const AttnWork wk = work[blockIdx.z];
     const int h = blockIdx.y, c = blockIdx.x;
     const int slot = seqs.slot[wk.seq], qn = seqs.qn[wk.seq], off = seqs.off[wk.seq];
@@ -274,6 +308,7 @@ template <typename TA, int DH>
 __global__ void attn_combine_kernel(const float* __restrict__ part_o, const float* __restrict__ part_ml,
                                     const int32_t* __restrict__ row_pos, int H, int max_chunks,
                                     TA* __restrict__ out) {
+    pdl_trigger();
     const int r = blockIdx.x, h = blockIdx.y;
     const int nc = row_pos[r] / AT_CHUNK + 1;
     const int64_t base = ((int64_t)r * H + h) * max_chunks;

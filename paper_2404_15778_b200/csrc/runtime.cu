@@ -481,6 +481,8 @@ int bass_model_create(bass_ctx* c, const bass_geometry* g, int dtype, bass_model
                          g->vocab_size >= 1 && g->max_seq_len >= 1,
                      "geometry: all sizes must be >= 1");
         BASS_REQUIRE(g->d_model == g->n_head * g->d_head, "geometry: d_model != n_head * d_head");
+        BASS_REQUIRE(g->d_model % 4 == 0 && g->d_model <= 4 * LN_THREADS * LN_NV,
+                     "d_model must be a multiple of 4 and <= 8192");
         BASS_REQUIRE(dtype == BASS_BF16 || dtype == BASS_F32, "dtype must be BASS_BF16 or BASS_F32");
         BASS_REQUIRE(g->d_head == 16 || g->d_head == 32 || g->d_head == 64 || g->d_head == 128,
                      "d_head must be 16, 32, 64 or 128");

@@ -15,6 +15,43 @@ namespace bass {
 constexpr int SM_THREADS = 512;
 constexpr int kMaxEmit = 64;   // >= draft limit + 1
 
+// thread-local argmax over a row (16-byte loads, 4 in flight), first index on ties
+BASS_DEV ArgMax row_argmax_local(const float* __restrict__ row, int V) {
+    ArgMax a{-INFINITY, 0x7fffffff};
+    if ((V & 3) == 0 && (reinterpret_cast<uintptr_t>(row) & 15) == 0) {
+        const float4* r4 = reinterpret_cast<const float4*>(row);
+        const int n4 = V >> 2;
+#pragma unroll 4
+        for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+            const float4 v = __ldg(r4 + i);
+            a = better(a, ArgMax{v.x, 4 * i});
+            a = better(a, ArgMax{v.y, 4 * i + 1});
+            a = better(a, ArgMax{v.z, 4 * i + 2});
+            a = better(a, ArgMax{v.w, 4 * i + 3});
+        }
+    } else {
+        for (int i = threadIdx.x; i < V; i += blockDim.x) a = better(a, ArgMax{row[i], i});
+    }
+    return a;
+}
+
+// thread-local sum of exp(x - m) (fp32 exp, fp64 accumulation)
+BASS_DEV double row_sumexp_local(const float* __restrict__ row, int V, float m) {
+    double s = 0.0;
+    if ((V & 3) == 0 && (reinterpret_cast<uintptr_t>(row) & 15) == 0) {
+        const float4* r4 = reinterpret_cast<const float4*>(row);
+        const int n4 = V >> 2;
+#pragma unroll 4
+        for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+            const float4 v = __ldg(r4 + i);
+            s += double(expf(v.x - m)) + double(expf(v.y - m)) + double(expf(v.z - m)) + double(expf(v.w - m));
+        }
+    } else {
+        for (int i = threadIdx.x; i < V; i += blockDim.x) s += double(expf(row[i] - m));
+    }
+    return s;
+}
+
 struct Shaped {
     int greedy;      // T == 0: one-hot on argmax
     int argmax;
@@ -54,9 +91,7 @@ BASS_DEV void shape_row(const float* __restrict__ row, int V, double T, double t
                         double* __restrict__ e, ShapeSmem& sm) {
     const int tid = threadIdx.x, nt = blockDim.x;
     // argmax / max (first index on ties)
-    ArgMax a{-INFINITY, 0x7fffffff};
-    for (int i = tid; i < V; i += nt) a = better(a, ArgMax{row[i], i});
-    a = block_argmax(a, sm.fred, sm.ired);
+    const ArgMax a = block_argmax(row_argmax_local(row, V), sm.fred, sm.ired);
     if (T == 0.0) {
         if (tid == 0) { sm.sh = Shaped{}; sm.sh.greedy = 1; sm.sh.argmax = a.i; }
         __syncthreads();
@@ -207,12 +242,8 @@ static __global__ void __launch_bounds__(SM_THREADS) row_stats_kernel(const floa
     __shared__ int iv[33];
     __shared__ double dv[33];
     const float* row = logits + (int64_t)blockIdx.x * V;
-    ArgMax a{-INFINITY, 0x7fffffff};
-    for (int i = threadIdx.x; i < V; i += blockDim.x) a = better(a, ArgMax{row[i], i});
-    a = block_argmax(a, fv, iv);
-    double s = 0.0;
-    for (int i = threadIdx.x; i < V; i += blockDim.x) s += exp(double(row[i]) - double(a.v));
-    s = block_sum(s, dv);
+    ArgMax a = block_argmax(row_argmax_local(row, V), fv, iv);
+    const double s = block_sum(row_sumexp_local(row, V, a.v), dv);
     if (threadIdx.x == 0) {
         amax[blockIdx.x] = a.i;
         lse[blockIdx.x] = double(a.v) + log(s);      // scipy.special.logsumexp
@@ -250,9 +281,7 @@ static __global__ void __launch_bounds__(SM_THREADS) draft_greedy_kernel(const f
     __shared__ int iv[33];
     const int i = blockIdx.x;
     const float* row = logits + (int64_t)i * V;
-    ArgMax a{-INFINITY, 0x7fffffff};
-    for (int k = threadIdx.x; k < V; k += blockDim.x) a = better(a, ArgMax{row[k], k});
-    a = block_argmax(a, fv, iv);
+    const ArgMax a = block_argmax(row_argmax_local(row, V), fv, iv);
     if (threadIdx.x == 0) {
         const int slot = d.slot[i];
         d.proposals[slot * d.pstride + d.j] = aligned_override(d, slot, d.pos[i], V, a.i);
@@ -505,12 +534,8 @@ static __global__ void __launch_bounds__(SM_THREADS) regular_pick_kernel(const f
     const float* row = logits + (int64_t)i * a.V;
     double* e = a.scratch + (int64_t)i * a.V;
     // lse of the raw row (logprob uses unshaped logits, ref:engine.py:162)
-    ArgMax mx{-INFINITY, 0x7fffffff};
-    for (int k = threadIdx.x; k < a.V; k += blockDim.x) mx = better(mx, ArgMax{row[k], k});
-    mx = block_argmax(mx, sm.fred, sm.ired);
-    double s = 0.0;
-    for (int k = threadIdx.x; k < a.V; k += blockDim.x) s += exp(double(row[k]) - double(mx.v));
-    s = block_sum(s, sm.dred);
+    const ArgMax mx = block_argmax(row_argmax_local(row, a.V), sm.fred, sm.ired);
+    const double s = block_sum(row_sumexp_local(row, a.V, mx.v), sm.dred);
     const double lse = double(mx.v) + log(s);
     int tok;
     if (a.T == 0.0) {
