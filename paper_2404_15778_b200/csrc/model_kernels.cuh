@@ -307,10 +307,10 @@ __global__ void __launch_bounds__(AT_THREADS) attn_partial_kernel(
 template <typename TA, int DH>
 __global__ void attn_combine_kernel(const float* __restrict__ part_o, const float* __restrict__ part_ml,
                                     const int32_t* __restrict__ row_pos, int H, int max_chunks,
-                                    TA* __restrict__ out) {
+                                    int chunk, TA* __restrict__ out) {
     pdl_trigger();
     const int r = blockIdx.x, h = blockIdx.y;
-    const int nc = row_pos[r] / AT_CHUNK + 1;
+    const int nc = row_pos[r] / chunk + 1;
     const int64_t base = ((int64_t)r * H + h) * max_chunks;
     float mx = -INFINITY;
     for (int c = 0; c < nc; ++c) mx = fmaxf(mx, part_ml[(base + c) * 2]);

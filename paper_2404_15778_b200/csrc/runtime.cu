@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstring>
 
@@ -226,8 +227,29 @@ template <typename TA, int DH>
 static void launch_attention_t(bass_ctx* ctx, int strategy, const void* q, const void* kc, const void* vc,
                                const Seqs& seqs_dev, const std::vector<int32_t>& qn,
                                const std::vector<int32_t>& off, const int32_t* row_pos_dev, int M,
-                               int H, int cap, DevBuf& work_buf, DevBuf& po, DevBuf& pml, void* out) {
+                               int H, int cap, int n_slots, DevBuf& work_buf, DevBuf& po, DevBuf& pml,
+                               void* out) {
     const int n_seq = (int)qn.size();
+    if constexpr (std::is_same<TA, __nv_bfloat16>::value && DH == 128) {
+        if (tc_attention_supported(BASS_BF16, DH)) {   // TMA + tcgen05 path (attn_tc.cu)
+            const int mc = (cap + 127) / 128;
+            float* part_o = (float*)po.need((size_t)M * H * mc * DH * 4, ctx->stream);
+            float* part_ml = (float*)pml.need((size_t)M * H * mc * 2 * 4, ctx->stream);
+            double abytes = 0.0, aflops = 0.0;
+            for (int i = 0; i < n_seq; ++i) {
+                abytes += (2.0 * H * (off[i] + qn[i]) * DH + 2.0 * H * qn[i] * DH) * sizeof(TA);
+                aflops += 4.0 * H * DH * qn[i] * (off[i] + 0.5 * (qn[i] + 1));
+            }
+            ProfScope prof(ctx, BASS_PROF_ATTN, abytes, aflops);
+            int nq = 0;
+            tc_attention(ctx, strategy, q, M, kc, vc, n_slots, seqs_dev, qn, off, H, cap, work_buf, part_o, part_ml,
+                         mc, &nq);
+            attn_combine_kernel<TA, DH><<<dim3(M, H), DH, 0, ctx->stream>>>(part_o, part_ml, row_pos_dev, H, mc, 128,
+                                                                            (TA*)out);
+            check_launch(ctx);
+            return;
+        }
+    }
     const int max_chunks = (cap + AT_CHUNK - 1) / AT_CHUNK;
     float* part_o = (float*)po.need((size_t)M * H * max_chunks * DH * 4, ctx->stream);
     float* part_ml = (float*)pml.need((size_t)M * H * max_chunks * 2 * 4, ctx->stream);
@@ -283,17 +305,17 @@ static void launch_attention_t(bass_ctx* ctx, int strategy, const void* q, const
         check_launch(ctx);
     }
     attn_combine_kernel<TA, DH><<<dim3(M, H), DH, 0, ctx->stream>>>(part_o, part_ml, row_pos_dev, H, max_chunks,
-                                                                    (TA*)out);
+                                                                    AT_CHUNK, (TA*)out);
     check_launch(ctx);
 }
 
 static void launch_attention(bass_ctx* ctx, int dtype, int dh, int strategy, const void* q, const void* kc,
                              const void* vc, const Seqs& seqs_dev, const std::vector<int32_t>& qn,
                              const std::vector<int32_t>& off, const int32_t* row_pos_dev, int M, int H, int cap,
-                             DevBuf& work_buf, DevBuf& po, DevBuf& pml, void* out) {
+                             int n_slots, DevBuf& work_buf, DevBuf& po, DevBuf& pml, void* out) {
 #define BASS_ATT(T, D)                                                                                  \
-    launch_attention_t<T, D>(ctx, strategy, q, kc, vc, seqs_dev, qn, off, row_pos_dev, M, H, cap, work_buf, \
-                             po, pml, out)
+    launch_attention_t<T, D>(ctx, strategy, q, kc, vc, seqs_dev, qn, off, row_pos_dev, M, H, cap, n_slots, \
+                             work_buf, po, pml, out)
     if (dtype == BASS_BF16) {
         if (dh == 16) BASS_ATT(__nv_bfloat16, 16);
         else if (dh == 32) BASS_ATT(__nv_bfloat16, 32);
@@ -364,7 +386,7 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
         e.d = d; e.dh = dh; e.H = H; e.cap = kv.cap;
         gemm(m, EPI_QKV, h, L.wqkv, M, 3 * d, d, e);
         launch_attention(ctx, m.dtype, dh, strategy, q, e.kc, e.vc, seqs, b.qn, b.off, rows.pos, M, H, kv.cap,
-                         work_buf, m.part_o, m.part_ml, cx);
+                         kv.n_slots, work_buf, m.part_o, m.part_ml, cx);
         Epi r{};
         r.x = x;
         gemm(m, EPI_RESID, cx, L.wo, M, d, d, r);
@@ -647,6 +669,9 @@ int bass_kv_create(bass_model* m, int n_slots, int capacity, bass_kv** out) {
         const size_t bytes = kv->layer_elems() * m->g.n_layer * m->esize;
         BASS_CUDA(cudaMalloc(&kv->k, bytes));
         BASS_CUDA(cudaMalloc(&kv->v, bytes));
+        // finite contents everywhere: masked keys get P = 0, and 0 * (finite) = 0
+        BASS_CUDA(cudaMemset(kv->k, 0, bytes));
+        BASS_CUDA(cudaMemset(kv->v, 0, bytes));
         *out = kv;
     });
 }
@@ -757,7 +782,7 @@ int bass_attention(bass_ctx* c, int strategy, int dtype, int n_seq, int n_head, 
         upload_i32(c, dm, hm.data(), hm.size());
         Seqs seqs{dm, dm + n_seq, dm + 2 * n_seq, dm + 3 * n_seq};
         launch_attention(c, dtype, d_head, strategy, q, k, v, seqs, qn, off, dm + 4 * n_seq, M, n_head, kv_stride,
-                         work, po, pml, out);
+                         n_seq, work, po, pml, out);
         c->sync();
     });
 }

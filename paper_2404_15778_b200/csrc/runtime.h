@@ -157,4 +157,10 @@ void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N
              const Epi& e);
 void tc_release(bass_model& m);
 
+// tcgen05 attention (attn_tc.cu)
+bool tc_attention_supported(int dtype, int dh);
+void tc_attention(bass_ctx* ctx, int strategy, const void* q, int M, const void* kc, const void* vc, int n_slots,
+                  const Seqs& seqs_dev, const std::vector<int32_t>& qn, const std::vector<int32_t>& off, int H, int cap,
+                  DevBuf& work_buf, float* part_o, float* part_ml, int max_chunks, int* nq_out);
+
 }  // namespace bass

@@ -261,3 +261,38 @@ def test_engine_validation_messages(B):
                              B.AdaptiveDraftController())
     with pytest.raises(ValueError, match="max_seq_len"):
         B.decode_regular(B.CudaModel(dw, 1), B.GenerationRequest([list(range(30))], 20))
+
+
+def test_bf16_dh128_tcgen05_attention_path(B):
+    """d_head = 128 routes attention through the TMA + tcgen05 kernel: logits
+    within 1e-2 of the oracle (bf16-rounded weights), batch-invariant, and
+    greedy speculative == regular."""
+    g = OR.Geometry(3, 4, 512, 128, 1500, 600)
+    gd = OR.Geometry(1, 4, 512, 128, 1500, 600)
+    w = _bf16_round(OR.init_weights(g, 31))
+    rng = np.random.default_rng(6)
+    prompts = [rng.integers(0, 1500, n).tolist() for n in (150, 7, 300, 64)]
+    blocks = [rng.integers(0, 1500, n).tolist() for n in (9, 9, 1, 33)]
+    om = OE.OracleModel(w, 4)
+    dwm = B.DeviceWeights.from_reference(w, "bf16")
+    dm = B.CudaModel(dwm, 4)
+    for s, p in enumerate(prompts):
+        om.prefill(s, p)
+        dm.prefill(s, p)
+    ref = om.forward([0, 1, 2, 3], blocks)
+    got = dm.forward([0, 1, 2, 3], blocks)
+    for a, b in zip(got, ref):
+        err = np.abs(a - b).max(axis=1) / np.abs(b).max(axis=1)
+        assert float(err.max()) < 1e-2, float(err.max())
+    solo = B.CudaModel(dwm, 4)
+    solo.prefill(2, prompts[2])
+    assert np.array_equal(solo.forward([2], [blocks[2]])[0], got[2])
+    dwd = B.DeviceWeights.from_reference(OR.init_weights(gd, 32), "bf16")
+    req = B.GenerationRequest([p[:40] for p in prompts], 40, temperature=0.0)
+    base = B.decode_regular(B.CudaModel(dwm, 4), req)
+    spec = B.decode_speculative(B.CudaModel(dwm, 4), B.CudaModel(dwm, 4), req,
+                                B.AdaptiveDraftController())
+    assert spec.tokens == base.tokens
+    spec2 = B.decode_speculative(B.CudaModel(dwm, 4), B.CudaModel(dwd, 4), req,
+                                 B.AdaptiveDraftController())
+    assert spec2.tokens == base.tokens
