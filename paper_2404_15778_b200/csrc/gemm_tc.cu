@@ -223,36 +223,42 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
             }
         }
     } else {
+        // split-K: the S CTAs of this tile are one thread-block cluster.  Each
+        // writes its fp32 partial tile (L2-resident scratch), the cluster
+        // barrier publishes them, and CTA `split` reduces rows
+        // [split*R/S, (split+1)*R/S) of the tile in fixed split order.
+        const int rows = min(TT, M - m0);
+        const int nn = warp * 32 + lane;
+        float* blk = sp.ws + (int64_t)(n_tile * gridDim.z + group) * sp.S * TT * BN;
 #pragma unroll 1
         for (int c0 = 0; c0 < TT; c0 += 16) {
             float v[16];
             tmem_ld16(trow + c0, v);
-            if (n < N) {
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int m = m0 + c0 + j;
-                    if (m < M) sp.ws[((int64_t)split * M + m) * N + n] = v[j];
-                }
-            }
+            for (int j = 0; j < 16; ++j)
+                if (c0 + j < rows) blk[((int64_t)split * TT + c0 + j) * BN + nn] = v[j];
         }
         __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int* ctr = &sp.counters[n_tile * gridDim.z + group];
-            const int prev = atomicAdd(ctr, 1);
-            s_last = prev == sp.S - 1;
-            if (s_last) *ctr = 0;   // reset for the next launch (stream ordered)
-        }
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-            if (n < N) {
-                const int mend = min(M, m0 + TT);
-                for (int m = m0; m < mend; ++m) {
-                    float acc = 0.f;
-                    for (int s = 0; s < sp.S; ++s) acc += __ldcg(&sp.ws[((int64_t)s * M + m) * N + n]);
-                    epilogue<MODE, __nv_bfloat16>(e, m, n, N, acc);
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        const int r0 = split * rows / sp.S, r1 = (split + 1) * rows / sp.S;
+        if (n < N) {
+            int r = r0;
+            for (; r + 4 <= r1; r += 4) {   // 4 rows x S partials in flight
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                for (int s = 0; s < sp.S; ++s) {
+                    float p[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) p[u] = __ldcg(&blk[((int64_t)s * TT + r + u) * BN + nn]);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) acc[u] += p[u];
                 }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) epilogue<MODE, __nv_bfloat16>(e, m0 + r + u, n, N, acc[u]);
+            }
+            for (; r < r1; ++r) {
+                float acc = 0.f;
+                for (int s = 0; s < sp.S; ++s) acc += __ldcg(&blk[((int64_t)s * TT + r) * BN + nn]);
+                epilogue<MODE, __nv_bfloat16>(e, m0 + r, n, N, acc);
             }
         }
     }
@@ -333,11 +339,15 @@ static void launch(bass_model& m, const CUtensorMap& wm, const CUtensorMap& xm, 
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = m.ctx->stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;   // split-K CTAs of a tile = one cluster
+    at[1].val.clusterDim.x = 1;
+    at[1].val.clusterDim.y = sp.S;
+    at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = sp.S > 1 ? 2 : 1;
     BASS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TT, MODE>, wm, xm, M, N, sp, e));
 }
 
@@ -372,15 +382,8 @@ void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N
     if (si == S.splits.end()) si = S.splits.emplace(sk, choose_splits(m.ctx->sm_count, N, K)).first;
     Split sp{si->second, K / BK, nullptr, nullptr};
     if (sp.S > 1) {
-        cudaStream_t st = m.ctx->stream;
-        sp.ws = (float*)S.ws.need((size_t)sp.S * M * N * 4, st);
-        const size_t nctr = (size_t)((N + BN - 1) / BN) * ((M + TT - 1) / TT);
-        if (nctr > S.counters_n) {   // grown buffers start zeroed; kernels leave them zeroed
-            int* c = (int*)S.counters.need(nctr * 4, st);
-            BASS_CUDA(cudaMemsetAsync(c, 0, S.counters.cap, st));
-            S.counters_n = S.counters.cap / 4;
-        }
-        sp.counters = (int*)S.counters.p;
+        const size_t blocks = (size_t)((N + BN - 1) / BN) * ((M + TT - 1) / TT);
+        sp.ws = (float*)S.ws.need(blocks * sp.S * TT * BN * 4, m.ctx->stream);
     }
     switch (TT) {
         case 16: launch_mode<16>(m, mode, it->second, xm, M, N, K, sp, e); break;
