@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
+#include <utility>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -326,6 +328,50 @@ bool tc_attention_supported(int dtype, int dh) {
 void tc_attention(bass_ctx* ctx, int strategy, const void* q, int M, const void* kc, const void* vc, int n_slots,
                   const Seqs& seqs_dev, const std::vector<int32_t>& qn, const std::vector<int32_t>& off, int H, int cap,
                   DevBuf& work_buf, float* part_o, float* part_ml, int max_chunks, int* nq_out) {
+    AttnPlan plan;
+    tc_attention_plan(ctx, strategy, q, M, n_slots, qn, off, H, cap, work_buf, plan);
+    *nq_out = plan.NQ;
+    tc_attention_run(ctx, plan, kc, vc, seqs_dev, part_o, part_ml);
+}
+
+// K/V cache maps are stable per (layer buffer, rows): encode once per process
+static const CUtensorMap& kv_map(const void* ptr, int64_t rows) {
+    static std::map<std::pair<const void*, int64_t>, CUtensorMap> cache;
+    auto key = std::make_pair(ptr, rows);
+    auto it = cache.find(key);
+    if (it == cache.end()) it = cache.emplace(key, atc::map2d(ptr, rows, atc::DH, atc::DH, atc::CH)).first;
+    return it->second;
+}
+
+void tc_attention_run(bass_ctx* ctx, const AttnPlan& p, const void* kc, const void* vc, const Seqs& seqs_dev,
+                      float* part_o, float* part_ml) {
+    using namespace atc;
+    const int64_t kv_rows = (int64_t)p.n_slots * p.H * p.cap;
+    const CUtensorMap& tk = kv_map(kc, kv_rows);
+    const CUtensorMap& tv = kv_map(vc, kv_rows);
+    const Work* wd = static_cast<const Work*>(p.work);
+    auto go = [&](const Work* wp, int nw) {
+        if (nw == 0) return;
+        switch (p.NQ) {
+            case 16: launch<16>(ctx, p.tq, tk, tv, seqs_dev, wp, nw, p.H, p.cap, p.pad_len, part_o, part_ml, p.mc); break;
+            case 32: launch<32>(ctx, p.tq, tk, tv, seqs_dev, wp, nw, p.H, p.cap, p.pad_len, part_o, part_ml, p.mc); break;
+            case 64: launch<64>(ctx, p.tq, tk, tv, seqs_dev, wp, nw, p.H, p.cap, p.pad_len, part_o, part_ml, p.mc); break;
+            default: launch<128>(ctx, p.tq, tk, tv, seqs_dev, wp, nw, p.H, p.cap, p.pad_len, part_o, part_ml, p.mc); break;
+        }
+        ctx->launches++;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) throw Error(BASS_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
+    };
+    const int n_seq = (int)p.first.size() - 1;
+    if (p.strategy == BASS_SPLIT) {
+        for (int i = 0; i < n_seq; ++i) go(wd + p.first[i], p.first[i + 1] - p.first[i]);
+    } else {
+        go(wd, p.first[n_seq]);
+    }
+}
+
+void tc_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, int n_slots, const std::vector<int32_t>& qn,
+                       const std::vector<int32_t>& off, int H, int cap, DevBuf& work_buf, AttnPlan& plan) {
     using namespace atc;
     const int n_seq = (int)qn.size();
     int max_qn = 0, max_L = 0;
@@ -334,7 +380,6 @@ void tc_attention(bass_ctx* ctx, int strategy, const void* q, int M, const void*
         max_L = std::max(max_L, off[i] + qn[i]);
     }
     const int NQ = max_qn <= 16 ? 16 : max_qn <= 32 ? 32 : max_qn <= 64 ? 64 : 128;
-    *nq_out = NQ;
     std::vector<int32_t> w;
     std::vector<int> first(n_seq + 1, 0);
     for (int i = 0; i < n_seq; ++i) {
@@ -357,28 +402,17 @@ void tc_attention(bass_ctx* ctx, int strategy, const void* q, int M, const void*
     std::memcpy(h, w.data(), w.size() * 4);
     BASS_CUDA(cudaMemcpyAsync(wd, h, w.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
     ctx->h2d_bytes += (int64_t)w.size() * 4;
-    const CUtensorMap tq = map2d(q, M, (int64_t)H * DH, (int64_t)H * DH, NQ);
-    const int64_t kv_rows = (int64_t)n_slots * H * cap;
-    const CUtensorMap tk = map2d(kc, kv_rows, DH, DH, CH);
-    const CUtensorMap tv = map2d(vc, kv_rows, DH, DH, CH);
-    const int pad_len = strategy == BASS_PAD ? max_L : 0;
-    auto go = [&](const Work* wp, int nw) {
-        if (nw == 0) return;
-        switch (NQ) {
-            case 16: launch<16>(ctx, tq, tk, tv, seqs_dev, wp, nw, H, cap, pad_len, part_o, part_ml, max_chunks); break;
-            case 32: launch<32>(ctx, tq, tk, tv, seqs_dev, wp, nw, H, cap, pad_len, part_o, part_ml, max_chunks); break;
-            case 64: launch<64>(ctx, tq, tk, tv, seqs_dev, wp, nw, H, cap, pad_len, part_o, part_ml, max_chunks); break;
-            default: launch<128>(ctx, tq, tk, tv, seqs_dev, wp, nw, H, cap, pad_len, part_o, part_ml, max_chunks); break;
-        }
-        ctx->launches++;
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) throw Error(BASS_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
-    };
-    if (strategy == BASS_SPLIT) {
-        for (int i = 0; i < n_seq; ++i) go(wd + first[i], first[i + 1] - first[i]);
-    } else {
-        go(wd, first[n_seq]);
-    }
+    plan.tq = map2d(q, M, (int64_t)H * DH, (int64_t)H * DH, NQ);
+    plan.NQ = NQ;
+    plan.pad_len = strategy == BASS_PAD ? max_L : 0;
+    plan.strategy = strategy;
+    plan.H = H;
+    plan.cap = cap;
+    plan.n_slots = n_slots;
+    plan.mc = (cap + CH - 1) / CH;
+    plan.first = std::move(first);
+    plan.work = wd;
+    plan.valid = true;
 }
 
 }  // namespace bass

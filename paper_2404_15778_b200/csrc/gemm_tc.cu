@@ -302,6 +302,7 @@ static CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int box
 
 struct State {
     std::map<std::tuple<const void*, int, int>, CUtensorMap> wmaps;
+    std::map<std::tuple<const void*, int, int, int>, CUtensorMap> xmaps;   // (X, M, K, TT)
     std::map<std::pair<int, int>, int> splits;
     DevBuf ws, counters;
     size_t counters_n = 0;
@@ -376,7 +377,10 @@ void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N
     auto key = std::make_tuple(W, N, K);
     auto it = S.wmaps.find(key);
     if (it == S.wmaps.end()) it = S.wmaps.emplace(key, make_map(W, N, K, BN)).first;
-    const CUtensorMap xm = make_map(X, M, K, TT);
+    auto xkey = std::make_tuple(X, M, K, TT);
+    auto xit = S.xmaps.find(xkey);
+    if (xit == S.xmaps.end()) xit = S.xmaps.emplace(xkey, make_map(X, M, K, TT)).first;
+    const CUtensorMap& xm = xit->second;
     auto sk = std::make_pair(N, K);
     auto si = S.splits.find(sk);
     if (si == S.splits.end()) si = S.splits.emplace(sk, choose_splits(m.ctx->sm_count, N, K)).first;

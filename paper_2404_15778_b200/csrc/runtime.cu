@@ -374,6 +374,20 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
                                                pstride, d, x);
     check_launch(ctx);
 
+    // tcgen05 attention: one plan (work list, Q map) for all layers of this forward
+    AttnPlan plan;
+    double attn_bytes = 0.0, attn_flops = 0.0;
+    float *pa_o = nullptr, *pa_ml = nullptr;
+    if (m.dtype == BASS_BF16 && tc_attention_supported(BASS_BF16, dh)) {
+        tc_attention_plan(ctx, strategy, q, M, kv.n_slots, b.qn, b.off, H, kv.cap, work_buf, plan);
+        pa_o = (float*)m.part_o.need((size_t)M * H * plan.mc * dh * 4, st);
+        pa_ml = (float*)m.part_ml.need((size_t)M * H * plan.mc * 2 * 4, st);
+        for (int i = 0; i < n_seq; ++i) {
+            attn_bytes += (2.0 * H * (b.off[i] + b.qn[i]) * dh + 2.0 * H * b.qn[i] * dh) * es;
+            attn_flops += 4.0 * H * dh * b.qn[i] * (b.off[i] + 0.5 * (b.qn[i] + 1));
+        }
+    }
+
     for (int li = 0; li < g.n_layer; ++li) {
         const bass_layer& L = m.layers[li];
         launch_layernorm_any(m, x, nullptr, L.ln1_g, L.ln1_b, M, h);
@@ -385,8 +399,16 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
         e.row_pos = rows.pos;
         e.d = d; e.dh = dh; e.H = H; e.cap = kv.cap;
         gemm(m, EPI_QKV, h, L.wqkv, M, 3 * d, d, e);
-        launch_attention(ctx, m.dtype, dh, strategy, q, e.kc, e.vc, seqs, b.qn, b.off, rows.pos, M, H, kv.cap,
-                         kv.n_slots, work_buf, m.part_o, m.part_ml, cx);
+        if (plan.valid) {
+            ProfScope prof(ctx, BASS_PROF_ATTN, attn_bytes, attn_flops);
+            tc_attention_run(ctx, plan, e.kc, e.vc, seqs, pa_o, pa_ml);
+            attn_combine_kernel<__nv_bfloat16, 128><<<dim3(M, H), 128, 0, st>>>(pa_o, pa_ml, rows.pos, H, plan.mc,
+                                                                                128, (__nv_bfloat16*)cx);
+            check_launch(ctx);
+        } else {
+            launch_attention(ctx, m.dtype, dh, strategy, q, e.kc, e.vc, seqs, b.qn, b.off, rows.pos, M, H, kv.cap,
+                             kv.n_slots, work_buf, m.part_o, m.part_ml, cx);
+        }
         Epi r{};
         r.x = x;
         gemm(m, EPI_RESID, cx, L.wo, M, d, d, r);
