@@ -350,6 +350,9 @@ def main():
         "mean_accepted": statistics.mean(acc) if acc else 0.0,
         "mean_draft_len": statistics.mean(dl) if dl else 0.0,
         "steps_per_generation": steps_per_gen,
+        "host_ms_per_generation": {
+            "enqueue": statistics.mean(r[2].host_enqueue_s for r in results) * 1e3,
+            "sync_wait": statistics.mean(r[2].sync_wait_s for r in results) * 1e3},
         "e2e": {"value": tokens / host_s, "unit": "tokens/s",
                 "h2d_bytes_per_step": (h2d1 - h2d0) // max(args.steps, 1),
                 "d2h_bytes_per_step": (d2h1 - d2h0) // max(args.steps, 1)},

@@ -112,6 +112,12 @@ int bass_forward_ragged(bass_model* m, bass_kv* kv, int n_seq,
  * ref:model.py:160-164 (_linear), output-major weights. */
 int bass_gemm(bass_model* m, int gemm_mode, int M, int N, int K,
               const void* x_dev, const void* w_dev, float* y_dev);
+/* microbenchmark: `reps` back-to-back launches; launch i uses weight copy
+ * i % n_w (w_dev holds n_w contiguous [N, K] copies); device time per launch
+ * from CUDA events on the context stream */
+int bass_gemm_bench(bass_model* m, int gemm_mode, int M, int N, int K,
+                    const void* x_dev, const void* w_dev, float* y_dev,
+                    int reps, int n_w, double* ms_per_launch);
 
 /* Standalone ragged attention (ref:attention.py:140-154 attend), for the
  * C4 sweep and kernel parity.  Layouts (device, dtype = BASS_BF16|F32):
@@ -190,6 +196,8 @@ typedef struct {
     int64_t  main_forward_calls, draft_forward_calls;
     double   wall_s;
     int32_t  final_l_draft, final_s;
+    double   host_enqueue_s;  /* host time spent building/launching steps      */
+    double   sync_wait_s;     /* host time blocked on the per-step read-back    */
 } bass_gen_result;
 
 /* The engine drives the providers' own caches (main_kv / draft_kv), as the

@@ -47,7 +47,8 @@ class GenResult(C.Structure):
                 ("step_accepted", i32p), ("step_emitted", i32p), ("step_kv_len", i32p),
                 ("step_wall_s", f64p), ("main_forward_calls", C.c_int64),
                 ("draft_forward_calls", C.c_int64), ("wall_s", C.c_double),
-                ("final_l_draft", C.c_int32), ("final_s", C.c_int32)]
+                ("final_l_draft", C.c_int32), ("final_s", C.c_int32),
+                ("host_enqueue_s", C.c_double), ("sync_wait_s", C.c_double)]
 
 
 # name -> (restype, argtypes); every symbol include/bass.h declares
@@ -75,6 +76,8 @@ SIGNATURES = {
     "bass_kv_truncate": (C.c_int, [vp, C.c_int, i32p, i32p]),
     "bass_forward_ragged": (C.c_int, [vp, vp, C.c_int, i32p, i32p, i32p, C.c_int, C.c_int, f32p]),
     "bass_gemm": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp]),
+    "bass_gemm_bench": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, C.c_int,
+                                  C.c_int, f64p]),
     "bass_attention": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, i32p, i32p,
                                  vp, vp, vp, C.c_int, vp]),
     "bass_rng_uniforms": (C.c_int, [vp, C.c_int, C.c_uint64, i64p, i32p, i64p, f64p]),

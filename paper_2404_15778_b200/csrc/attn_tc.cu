@@ -87,8 +87,10 @@ __device__ __forceinline__ void ld16(uint32_t taddr, float* v) {
 }
 
 struct Work {
-    int32_t seq, t0, chunk, pad;
+    int32_t seq, t0, chunk, n;   // n: chunks walked by a fused CTA (0 in split mode)
 };
+
+constexpr int MAXC = 16;   // fused mode: at most 16 chunks (2048 keys) per CTA
 
 template <int NQ>
 struct Cfg {
@@ -96,9 +98,9 @@ struct Cfg {
     static constexpr int Q_TILE = NQ * 128;
     static constexpr int OFF_K = 0, OFF_V = 2 * KV_TILE, OFF_Q = 4 * KV_TILE, OFF_P = OFF_Q + 2 * Q_TILE;
     static constexpr int OFF_RED = OFF_P + 2 * Q_TILE;   // float red_max[4][NQ], red_sum[4][NQ], m[NQ]
-    static constexpr int OFF_BAR = OFF_RED + 9 * NQ * 4;
+    static constexpr int OFF_ML = OFF_RED + 9 * NQ * 4;   // fused: m, l per (chunk, column)
+    static constexpr int OFF_BAR = OFF_ML + 2 * MAXC * NQ * 4;
     static constexpr int SMEM = OFF_BAR + 64 + 1024;
-    static constexpr int TMEM_COLS = 2 * NQ < 32 ? 32 : 2 * NQ;
 };
 
 template <int NQ>
@@ -106,8 +108,12 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
                                                              const __grid_constant__ CUtensorMap tk,
                                                              const __grid_constant__ CUtensorMap tv, Seqs seqs,
                                                              const Work* __restrict__ work, int H, int cap,
-                                                             int pad_len, int v_swap, float* __restrict__ part_o,
-                                                             float* __restrict__ part_ml, int max_chunks) {
+                                                             int pad_len, int tmem_cols, float* __restrict__ part_o,
+                                                             float* __restrict__ part_ml, int max_chunks,
+                                                             __nv_bfloat16* __restrict__ out) {
+    // out == nullptr: split mode, one chunk per CTA, partial (m, l, o) out;
+    // out != nullptr: fused mode, the CTA walks wk.n chunks and merges them
+    // (same arithmetic as attn_combine_kernel) into ctx directly.
     using Cf = Cfg<NQ>;
     extern __shared__ uint8_t smem_raw[];
     pdl_trigger();
@@ -116,9 +122,11 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
     const int slot = seqs.slot[wk.seq], qn = seqs.qn[wk.seq], off = seqs.off[wk.seq], q0row = seqs.q0[wk.seq];
     const int L = off + qn;
     const int kv_len = pad_len > 0 ? pad_len : L;
-    const int c0 = wk.chunk * CH;
+    const bool fused = out != nullptr;
+    const int nch = fused ? wk.n : 1;
+    const int cfirst = wk.chunk * CH;
     const int t_last = min(qn, wk.t0 + NQ) - 1;
-    if (wk.t0 >= qn || c0 >= kv_len || off + t_last < c0) return;   // whole CTA idle (uniform)
+    if (wk.t0 >= qn || nch <= 0 || cfirst >= kv_len || off + t_last < cfirst) return;   // idle CTA (uniform)
 
     const uint32_t raw = su32(smem_raw);
     const uint32_t base = (raw + 1023) & ~1023u;
@@ -126,6 +134,8 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
     float* red_max = reinterpret_cast<float*>(sm + Cf::OFF_RED);
     float* red_sum = red_max + 4 * NQ;
     float* m_col = red_sum + 4 * NQ;
+    float* ml_m = reinterpret_cast<float*>(sm + Cf::OFF_ML);     // [MAXC][NQ] chunk maxima (fused)
+    float* ml_l = ml_m + MAXC * NQ;                               // [MAXC][NQ] chunk sums
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Cf::OFF_BAR);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -137,7 +147,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
-                     "r"(Cf::TMEM_COLS)
+                     "r"(tmem_cols)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -145,129 +155,174 @@ __global__ void __launch_bounds__(THREADS, 1) attn_tc_kernel(const __grid_consta
     __syncthreads();
     fence_after();
     const uint32_t tmem = *tmem_slot;
-
-    if (threadIdx.x == 0) {   // loads: K, V chunk (2 sub-tiles each), Q tile (2 sub-tiles)
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        const uint32_t b = su32(&bars[0]);
-        mbar_expect_tx(b, 4 * Cf::KV_TILE + 2 * Cf::Q_TILE);
-        const int kv_row = (slot * H + h) * cap + c0;
-        for (int s = 0; s < 2; ++s) {
-            tma_2d(&tk, base + Cf::OFF_K + s * Cf::KV_TILE, b, s * 64, kv_row);
-            tma_2d(&tv, base + Cf::OFF_V + s * Cf::KV_TILE, b, s * 64, kv_row);
-            tma_2d(&tq, base + Cf::OFF_Q + s * Cf::Q_TILE, b, h * DH + s * 64, q0row + wk.t0);
-        }
-        mbar_wait(b, 0);
-        fence_after();
-        // S^T = K . Q^T : A = K (K-major), B = Q (K-major), 8 k-steps of 16 over d
-        constexpr uint32_t ID1 = idesc(NQ, 0);
-#pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
-            const uint32_t sub = kk >> 2, in = (kk & 3) * 32;
-            const uint64_t a = sdesc(base + Cf::OFF_K + sub * Cf::KV_TILE + in, 16, 1024);
-            const uint64_t bq = sdesc(base + Cf::OFF_Q + sub * Cf::Q_TILE + in, 16, 1024);
-            umma(tmem, a, bq, ID1, kk > 0);
-        }
-        commit(su32(&bars[1]));
-    }
-    __syncwarp();
-    mbar_wait(su32(&bars[1]), 0);
-    fence_after();
-
-    // ---- softmax over the 128 keys of this chunk, per query column
     const int key = warp * 32 + lane;
-    const int kpos = c0 + key;
-    const float inv_scale = 1.0f / sqrtf((float)DH);
-    (void)inv_scale;
     const float scale = sqrtf((float)DH);
     const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-#pragma unroll 1
-    for (int j0 = 0; j0 < NQ; j0 += 16) {
-        float v[16];
-        ld16(trow + j0, v);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int t = wk.t0 + j0 + j;
-            const bool ok = t < qn && kpos <= off + t && kpos < L;
-            const float s = ok ? v[j] / scale : -INFINITY;
-            const float mx = warp_max(s);
-            if (lane == 0) red_max[warp * NQ + j0 + j] = mx;
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x < NQ) {
-        const int q = threadIdx.x;
-        m_col[q] = fmaxf(fmaxf(red_max[q], red_max[NQ + q]), fmaxf(red_max[2 * NQ + q], red_max[3 * NQ + q]));
-    }
-    __syncthreads();
     uint8_t* P = sm + Cf::OFF_P;
     const int psub = key >> 6, pin = key & 63;
-#pragma unroll 1
-    for (int j0 = 0; j0 < NQ; j0 += 16) {
-        float v[16];
-        ld16(trow + j0, v);
+
+    for (int ci = 0; ci < nch; ++ci) {
+        const uint32_t ph = ci & 1;
+        const int c0 = cfirst + ci * CH;
+        if (threadIdx.x == 0) {   // loads: K, V chunk (2 sub-tiles each); Q tile once
+            const uint32_t b = su32(&bars[0]);
+            if (ci == 0) {
+                asm volatile("griddepcontrol.wait;" ::: "memory");
+                mbar_expect_tx(b, 4 * Cf::KV_TILE + 2 * Cf::Q_TILE);
+            } else {
+                mbar_expect_tx(b, 4 * Cf::KV_TILE);
+            }
+            const int kv_row = (slot * H + h) * cap + c0;
+            for (int s = 0; s < 2; ++s) {
+                tma_2d(&tk, base + Cf::OFF_K + s * Cf::KV_TILE, b, s * 64, kv_row);
+                tma_2d(&tv, base + Cf::OFF_V + s * Cf::KV_TILE, b, s * 64, kv_row);
+                if (ci == 0) tma_2d(&tq, base + Cf::OFF_Q + s * Cf::Q_TILE, b, h * DH + s * 64, q0row + wk.t0);
+            }
+            mbar_wait(b, ph);
+            fence_after();
+            // S^T = K . Q^T : A = K (K-major), B = Q (K-major), 8 k-steps of 16 over d
+            constexpr uint32_t ID1 = idesc(NQ, 0);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int q = j0 + j, t = wk.t0 + q;
-            const bool ok = t < qn && kpos <= off + t && kpos < L;
-            const float m = m_col[q];
-            const float p = (ok && m != -INFINITY) ? expf(v[j] / scale - m) : 0.f;
-            const float ps = warp_sum(p);
-            if (lane == 0) red_sum[warp * NQ + q] = ps;
-            // P[q][key] in the K-major 128B-swizzled sub-tile psub
-            const uint32_t chunk = (uint32_t)(pin >> 3) ^ (uint32_t)(q & 7);
-            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(P + psub * Cf::Q_TILE + q * 128 + chunk * 16) +
-                                 (pin & 7);
-            *dst = __float2bfloat16_rn(p);
+            for (int kk = 0; kk < DH / 16; ++kk) {
+                const uint32_t sub = kk >> 2, in = (kk & 3) * 32;
+                const uint64_t a = sdesc(base + Cf::OFF_K + sub * Cf::KV_TILE + in, 16, 1024);
+                const uint64_t bq = sdesc(base + Cf::OFF_Q + sub * Cf::Q_TILE + in, 16, 1024);
+                umma(tmem, a, bq, ID1, kk > 0);
+            }
+            commit(su32(&bars[1]));
         }
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // P visible to the tensor core
-    fence_before();
-    __syncthreads();
-    if (threadIdx.x == 0) {
+        __syncwarp();
+        mbar_wait(su32(&bars[1]), ph);
         fence_after();
-        // O^T = V^T . P^T : A = V (MN-major: d contiguous), B = P (K-major over keys)
-        constexpr uint32_t ID2 = idesc(NQ, 1);
-        const uint32_t lbo = v_swap ? 1024 : Cf::KV_TILE, sbo = v_swap ? Cf::KV_TILE : 1024;
-#pragma unroll
-        for (int kk = 0; kk < CH / 16; ++kk) {
-            const uint64_t a = sdesc(base + Cf::OFF_V + kk * 2048, lbo, sbo);
-            const uint32_t sub = kk >> 2, in = (kk & 3) * 32;
-            const uint64_t bp = sdesc(base + Cf::OFF_P + sub * Cf::Q_TILE + in, 16, 1024);
-            umma(tmem + NQ, a, bp, ID2, kk > 0);
-        }
-        commit(su32(&bars[2]));
-    }
-    // column max / sum -> partial (m, l) for rows that see this chunk
-    if (threadIdx.x < NQ) {
-        const int q = threadIdx.x, t = wk.t0 + q;
-        if (t < qn && off + t >= c0) {
-            const float l = (red_sum[q] + red_sum[NQ + q]) + (red_sum[2 * NQ + q] + red_sum[3 * NQ + q]);
-            const int64_t idx = ((int64_t)(q0row + t) * H + h) * max_chunks + wk.chunk;
-            part_ml[idx * 2] = m_col[q];
-            part_ml[idx * 2 + 1] = l;
-        }
-    }
-    __syncwarp();
-    mbar_wait(su32(&bars[2]), 0);
-    fence_after();
-    // O^T lane = d (0..127), columns = query rows
+
+        // ---- softmax over the 128 keys of this chunk, per query column
+        const int kpos = c0 + key;
 #pragma unroll 1
-    for (int j0 = 0; j0 < NQ; j0 += 16) {
-        float v[16];
-        ld16(trow + NQ + j0, v);
+        for (int j0 = 0; j0 < NQ; j0 += 16) {
+            float v[16];
+            ld16(trow + j0, v);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int t = wk.t0 + j0 + j;
-            if (t < qn && off + t >= c0) {
+            for (int j = 0; j < 16; ++j) {
+                const int t = wk.t0 + j0 + j;
+                const bool ok = t < qn && kpos <= off + t && kpos < L;
+                const float s = ok ? v[j] / scale : -INFINITY;
+                const float mx = warp_max(s);
+                if (lane == 0) red_max[warp * NQ + j0 + j] = mx;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < NQ) {
+            const int q = threadIdx.x;
+            m_col[q] = fmaxf(fmaxf(red_max[q], red_max[NQ + q]), fmaxf(red_max[2 * NQ + q], red_max[3 * NQ + q]));
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int j0 = 0; j0 < NQ; j0 += 16) {
+            float v[16];
+            ld16(trow + j0, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int q = j0 + j, t = wk.t0 + q;
+                const bool ok = t < qn && kpos <= off + t && kpos < L;
+                const float m = m_col[q];
+                const float p = (ok && m != -INFINITY) ? expf(v[j] / scale - m) : 0.f;
+                const float ps = warp_sum(p);
+                if (lane == 0) red_sum[warp * NQ + q] = ps;
+                // P[q][key] in the K-major 128B-swizzled sub-tile psub
+                const uint32_t chunk = (uint32_t)(pin >> 3) ^ (uint32_t)(q & 7);
+                __nv_bfloat16* dst =
+                    reinterpret_cast<__nv_bfloat16*>(P + psub * Cf::Q_TILE + q * 128 + chunk * 16) + (pin & 7);
+                *dst = __float2bfloat16_rn(p);
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // P visible to the tensor core
+        fence_before();
+        __syncthreads();
+        const uint32_t ocol = fused ? (uint32_t)(NQ * (1 + ci)) : (uint32_t)NQ;
+        if (threadIdx.x == 0) {
+            fence_after();
+            // O^T = V^T . P^T : A = V (MN-major: d contiguous), B = P (K-major over keys)
+            constexpr uint32_t ID2 = idesc(NQ, 1);
+#pragma unroll
+            for (int kk = 0; kk < CH / 16; ++kk) {
+                const uint64_t a = sdesc(base + Cf::OFF_V + kk * 2048, Cf::KV_TILE, 1024);
+                const uint32_t sub = kk >> 2, in = (kk & 3) * 32;
+                const uint64_t bp = sdesc(base + Cf::OFF_P + sub * Cf::Q_TILE + in, 16, 1024);
+                umma(tmem + ocol, a, bp, ID2, kk > 0);
+            }
+            commit(su32(&bars[2]));
+        }
+        // column max / sum of this chunk
+        if (threadIdx.x < NQ) {
+            const int q = threadIdx.x, t = wk.t0 + q;
+            const float l = (red_sum[q] + red_sum[NQ + q]) + (red_sum[2 * NQ + q] + red_sum[3 * NQ + q]);
+            if (fused) {
+                ml_m[ci * NQ + q] = m_col[q];
+                ml_l[ci * NQ + q] = l;
+            } else if (t < qn && off + t >= c0) {
                 const int64_t idx = ((int64_t)(q0row + t) * H + h) * max_chunks + wk.chunk;
-                part_o[idx * DH + key] = v[j];
+                part_ml[idx * 2] = m_col[q];
+                part_ml[idx * 2 + 1] = l;
+            }
+        }
+        __syncwarp();
+        mbar_wait(su32(&bars[2]), ph);   // V, P and the S^T columns are free again
+        fence_after();
+    }
+    __syncthreads();
+
+    if (!fused) {
+        // O^T lane = d (0..127), columns = query rows -> partial o
+#pragma unroll 1
+        for (int j0 = 0; j0 < NQ; j0 += 16) {
+            float v[16];
+            ld16(trow + NQ + j0, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int t = wk.t0 + j0 + j;
+                if (t < qn && off + t >= cfirst) {
+                    const int64_t idx = ((int64_t)(q0row + t) * H + h) * max_chunks + wk.chunk;
+                    part_o[idx * DH + key] = v[j];
+                }
+            }
+        }
+    } else {
+        // merge the chunks in order, exactly as attn_combine_kernel does
+#pragma unroll 1
+        for (int j0 = 0; j0 < NQ; j0 += 16) {
+            float mx[16], num[16], den[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                mx[j] = -INFINITY;
+                num[j] = 0.f;
+                den[j] = 0.f;
+            }
+            for (int c = 0; c < nch; ++c)
+#pragma unroll
+                for (int j = 0; j < 16; ++j) mx[j] = fmaxf(mx[j], ml_m[c * NQ + j0 + j]);
+            for (int c = 0; c < nch; ++c) {
+                float v[16];
+                ld16(trow + NQ * (1 + c) + j0, v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const float m = ml_m[c * NQ + j0 + j];
+                    if (m == -INFINITY) continue;
+                    const float w = expf(m - mx[j]);
+                    num[j] = fmaf(w, v[j], num[j]);
+                    den[j] = fmaf(w, ml_l[c * NQ + j0 + j], den[j]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int t = wk.t0 + j0 + j;
+                if (t < qn) out[((int64_t)(q0row + t) * H + h) * DH + key] = __float2bfloat16_rn(num[j] / den[j]);
             }
         }
     }
     fence_before();
     __syncthreads();
     if (warp == 2)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cf::TMEM_COLS)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols)
                      : "memory");
 }
 
@@ -303,17 +358,22 @@ static CUtensorMap map2d(const void* ptr, int64_t rows, int64_t cols, int64_t ro
 
 template <int NQ>
 static void launch(bass_ctx* ctx, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                   const Seqs& seqs, const Work* work, int n_work, int H, int cap, int pad_len, float* po,
-                   float* pml, int max_chunks) {
+                   const Seqs& seqs, const Work* work, int n_work, int H, int cap, int pad_len, int tmem_cols,
+                   float* po, float* pml, int max_chunks, __nv_bfloat16* out) {
     using Cf = Cfg<NQ>;
     static bool attr = false;
     if (!attr) {
         BASS_CUDA(cudaFuncSetAttribute(attn_tc_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
         attr = true;
     }
-    static const int v_swap = getenv("BASS_ATTN_VSWAP") ? atoi(getenv("BASS_ATTN_VSWAP")) : 0;
     attn_tc_kernel<NQ><<<dim3(n_work, H), THREADS, Cf::SMEM, ctx->stream>>>(tq, tk, tv, seqs, work, H, cap, pad_len,
-                                                                           v_swap, po, pml, max_chunks);
+                                                                           tmem_cols, po, pml, max_chunks, out);
+}
+
+static int pow2_cols(int c) {
+    int p = 32;
+    while (p < c) p <<= 1;
+    return p;
 }
 
 }  // namespace atc
@@ -323,15 +383,14 @@ bool tc_attention_supported(int dtype, int dh) {
     return !off && dtype == BASS_BF16 && dh == atc::DH;
 }
 
-// Work list (seq, t0, chunk): RAGGED/SPLIT exact; PAD over the padded
-// [max q] x [max L] grid (idle tiles exit; padded keys computed and masked).
+// One-shot (plan + run) used by the standalone bass_attention path (split mode).
 void tc_attention(bass_ctx* ctx, int strategy, const void* q, int M, const void* kc, const void* vc, int n_slots,
                   const Seqs& seqs_dev, const std::vector<int32_t>& qn, const std::vector<int32_t>& off, int H, int cap,
                   DevBuf& work_buf, float* part_o, float* part_ml, int max_chunks, int* nq_out) {
     AttnPlan plan;
-    tc_attention_plan(ctx, strategy, q, M, n_slots, qn, off, H, cap, work_buf, plan);
+    tc_attention_plan(ctx, strategy, q, M, n_slots, qn, off, H, cap, work_buf, plan, /*allow_fused=*/false);
     *nq_out = plan.NQ;
-    tc_attention_run(ctx, plan, kc, vc, seqs_dev, part_o, part_ml);
+    tc_attention_run(ctx, plan, kc, vc, seqs_dev, part_o, part_ml, nullptr);
 }
 
 // K/V cache maps are stable per (layer buffer, rows): encode once per process
@@ -344,19 +403,20 @@ static const CUtensorMap& kv_map(const void* ptr, int64_t rows) {
 }
 
 void tc_attention_run(bass_ctx* ctx, const AttnPlan& p, const void* kc, const void* vc, const Seqs& seqs_dev,
-                      float* part_o, float* part_ml) {
+                      float* part_o, float* part_ml, void* out) {
     using namespace atc;
     const int64_t kv_rows = (int64_t)p.n_slots * p.H * p.cap;
     const CUtensorMap& tk = kv_map(kc, kv_rows);
     const CUtensorMap& tv = kv_map(vc, kv_rows);
     const Work* wd = static_cast<const Work*>(p.work);
+    __nv_bfloat16* o = p.fused ? static_cast<__nv_bfloat16*>(out) : nullptr;
     auto go = [&](const Work* wp, int nw) {
         if (nw == 0) return;
         switch (p.NQ) {
-            case 16: launch<16>(ctx, p.tq, tk, tv, seqs_dev, wp, nw, p.H, p.cap, p.pad_len, part_o, part_ml, p.mc); break;
-            case 32: launch<32>(ctx, p.tq, tk, tv, seqs_dev, wp, nw, p.H, p.cap, p.pad_len, part_o, part_ml, p.mc); break;
-            case 64: launch<64>(ctx, p.tq, tk, tv, seqs_dev, wp, nw, p.H, p.cap, p.pad_len, part_o, part_ml, p.mc); break;
-            default: launch<128>(ctx, p.tq, tk, tv, seqs_dev, wp, nw, p.H, p.cap, p.pad_len, part_o, part_ml, p.mc); break;
+            case 16: launch<16>(ctx, p.tq, tk, tv, seqs_dev, wp, nw, p.H, p.cap, p.pad_len, p.tmem_cols, part_o, part_ml, p.mc, o); break;
+            case 32: launch<32>(ctx, p.tq, tk, tv, seqs_dev, wp, nw, p.H, p.cap, p.pad_len, p.tmem_cols, part_o, part_ml, p.mc, o); break;
+            case 64: launch<64>(ctx, p.tq, tk, tv, seqs_dev, wp, nw, p.H, p.cap, p.pad_len, p.tmem_cols, part_o, part_ml, p.mc, o); break;
+            default: launch<128>(ctx, p.tq, tk, tv, seqs_dev, wp, nw, p.H, p.cap, p.pad_len, p.tmem_cols, part_o, part_ml, p.mc, o); break;
         }
         ctx->launches++;
         cudaError_t e = cudaGetLastError();
@@ -370,8 +430,13 @@ void tc_attention_run(bass_ctx* ctx, const AttnPlan& p, const void* kc, const vo
     }
 }
 
+// Work list.  Split mode: one item per (seq, q tile, 128-key chunk).  Fused
+// mode (all tiles see <= MAXC chunks and (1 + chunks) * NQ TMEM columns fit):
+// one item per (seq, q tile) walking its chunks.  RAGGED/SPLIT are exact;
+// PAD covers the padded [max q] x [max L] grid (padded keys computed, masked).
 void tc_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, int n_slots, const std::vector<int32_t>& qn,
-                       const std::vector<int32_t>& off, int H, int cap, DevBuf& work_buf, AttnPlan& plan) {
+                       const std::vector<int32_t>& off, int H, int cap, DevBuf& work_buf, AttnPlan& plan,
+                       bool allow_fused) {
     using namespace atc;
     const int n_seq = (int)qn.size();
     int max_qn = 0, max_L = 0;
@@ -380,20 +445,32 @@ void tc_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, int n_
         max_L = std::max(max_L, off[i] + qn[i]);
     }
     const int NQ = max_qn <= 16 ? 16 : max_qn <= 32 ? 32 : max_qn <= 64 ? 64 : 128;
+    auto chunks_seen = [&](int i, int t0) {   // chunks visible to the last row of a tile
+        const int len = strategy == BASS_PAD ? max_L : off[i] + std::min(qn[i], t0 + NQ);
+        return (len + CH - 1) / CH;
+    };
+    static const bool no_fuse = getenv("BASS_ATTN_SPLIT_ONLY") != nullptr;
+    int max_nch = 0;
+    for (int i = 0; i < n_seq; ++i)
+        for (int t0 = 0; t0 < (strategy == BASS_PAD ? max_qn : qn[i]); t0 += NQ)
+            max_nch = std::max(max_nch, chunks_seen(i, t0));
+    const bool fused = allow_fused && !no_fuse && max_nch <= MAXC && (1 + max_nch) * NQ <= 512;
     std::vector<int32_t> w;
     std::vector<int> first(n_seq + 1, 0);
     for (int i = 0; i < n_seq; ++i) {
         first[i] = (int)w.size() / 4;
         const int rows = strategy == BASS_PAD ? max_qn : qn[i];
-        const int len = strategy == BASS_PAD ? max_L : off[i] + qn[i];
-        for (int t0 = 0; t0 < rows; t0 += NQ)
-            for (int c = 0; c * CH < len; ++c) {
-                if (strategy != BASS_PAD && c * CH > off[i] + std::min(qn[i], t0 + NQ) - 1) break;
-                w.insert(w.end(), {i, t0, c, 0});
+        for (int t0 = 0; t0 < rows; t0 += NQ) {
+            const int nch = chunks_seen(i, t0);
+            if (fused) {
+                w.insert(w.end(), {i, t0, 0, nch});
+            } else {
+                for (int c = 0; c < nch; ++c) w.insert(w.end(), {i, t0, c, 0});
             }
+        }
     }
     first[n_seq] = (int)w.size() / 4;
-    Work* wd = (Work*)work_buf.need(w.size() * 4, ctx->stream);
+    Work* wd = (Work*)work_buf.need(std::max<size_t>(w.size(), 4) * 4, ctx->stream);
     void* h = ctx->staging.take(w.size() * 4);
     if (!h) {
         ctx->sync();
@@ -410,6 +487,8 @@ void tc_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, int n_
     plan.cap = cap;
     plan.n_slots = n_slots;
     plan.mc = (cap + CH - 1) / CH;
+    plan.fused = fused;
+    plan.tmem_cols = pow2_cols(fused ? (1 + max_nch) * NQ : 2 * NQ);
     plan.first = std::move(first);
     plan.work = wd;
     plan.valid = true;

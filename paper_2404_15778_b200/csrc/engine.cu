@@ -230,6 +230,7 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
             res->finish_wall_s[s] = 0.0;
         }
         int64_t main_calls = 0, draft_calls = 0;
+        double host_enqueue_s = 0.0, sync_wait_s = 0.0;
         int step = 0;
         const auto t0 = clk::now();
         const int Lmax = limit + 1;
@@ -337,7 +338,10 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
             c->d2h_bytes += (int64_t)nA * sizeof(SlotStep);
             BASS_CUDA(cudaMemcpyAsync(e->step_host, step_dev, (size_t)nA * sizeof(SlotStep),
                                       cudaMemcpyDeviceToHost, st));
+            const auto t_enq = clk::now();
+            host_enqueue_s += secs(ts, t_enq);
             c->sync();
+            sync_wait_s += secs(t_enq, clk::now());
             const double now = secs(t0, clk::now());
             // ---------------------------------------------- bookkeeping
             std::vector<int> acc(nA);
@@ -396,6 +400,8 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
         res->wall_s = secs(t0, clk::now());
         res->final_l_draft = ctl.l;
         res->final_s = ctl.s;
+        res->host_enqueue_s = host_enqueue_s;
+        res->sync_wait_s = sync_wait_s;
     });
 }
 

@@ -320,8 +320,9 @@ static State& state(bass_model& m) {
 static int choose_splits(int sm_count, int N, int K) {
     const int n_tiles = (N + BN - 1) / BN, k_iters = K / BK;
     const int slots = 2 * sm_count;
+    static const int cap_s = getenv("BASS_MAX_SPLIT") ? atoi(getenv("BASS_MAX_SPLIT")) : 8;
     int best_s = 1;
-    for (int s = 2; s <= 8; ++s)
+    for (int s = 2; s <= cap_s; ++s)
         if (n_tiles * s <= slots && k_iters / s >= 4) best_s = s;
     return best_s;
 }
@@ -347,6 +348,8 @@ static void launch(bass_model& m, const CUtensorMap& wm, const CUtensorMap& xm, 
     at[1].val.clusterDim.x = 1;
     at[1].val.clusterDim.y = sp.S;
     at[1].val.clusterDim.z = 1;
+    static const bool pdl = !(getenv("BASS_PDL") && atoi(getenv("BASS_PDL")) == 0);
+    at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = sp.S > 1 ? 2 : 1;
     BASS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TT, MODE>, wm, xm, M, N, sp, e));

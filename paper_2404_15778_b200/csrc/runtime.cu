@@ -401,10 +401,12 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
         gemm(m, EPI_QKV, h, L.wqkv, M, 3 * d, d, e);
         if (plan.valid) {
             ProfScope prof(ctx, BASS_PROF_ATTN, attn_bytes, attn_flops);
-            tc_attention_run(ctx, plan, e.kc, e.vc, seqs, pa_o, pa_ml);
-            attn_combine_kernel<__nv_bfloat16, 128><<<dim3(M, H), 128, 0, st>>>(pa_o, pa_ml, rows.pos, H, plan.mc,
-                                                                                128, (__nv_bfloat16*)cx);
-            check_launch(ctx);
+            tc_attention_run(ctx, plan, e.kc, e.vc, seqs, pa_o, pa_ml, cx);
+            if (!plan.fused) {
+                attn_combine_kernel<__nv_bfloat16, 128><<<dim3(M, H), 128, 0, st>>>(pa_o, pa_ml, rows.pos, H,
+                                                                                    plan.mc, 128, (__nv_bfloat16*)cx);
+                check_launch(ctx);
+            }
         } else {
             launch_attention(ctx, m.dtype, dh, strategy, q, e.kc, e.vc, seqs, b.qn, b.off, rows.pos, M, H, kv.cap,
                              kv.n_slots, work_buf, m.part_o, m.part_ml, cx);
@@ -762,6 +764,33 @@ int bass_forward_ragged(bass_model* m, bass_kv* kv, int n_seq, const int32_t* sl
 }
 
 // ------------------------------------------------------ standalone kernels
+int bass_gemm_bench(bass_model* m, int mode, int M, int N, int K, const void* x, const void* w, float* y, int reps,
+                    int n_w, double* ms_per_launch) {
+    return guarded(m->ctx, [&] {
+        BASS_REQUIRE(reps >= 1, "reps must be >= 1");
+        const int saved = m->gemm_mode;
+        m->gemm_mode = mode;
+        Epi e{};
+        e.out = y;
+        cudaEvent_t a, b;
+        BASS_CUDA(cudaEventCreate(&a));
+        BASS_CUDA(cudaEventCreate(&b));
+        // launch i streams weight copy i % n_w (n_w copies > L2 defeat caching)
+        const size_t wbytes = (size_t)N * K * m->esize;
+        for (int i = 0; i < n_w; ++i) gemm(*m, EPI_STORE, x, (const char*)w + i * wbytes, M, N, K, e);   // warm
+        BASS_CUDA(cudaEventRecord(a, m->ctx->stream));
+        for (int i = 0; i < reps; ++i) gemm(*m, EPI_STORE, x, (const char*)w + (i % n_w) * wbytes, M, N, K, e);
+        BASS_CUDA(cudaEventRecord(b, m->ctx->stream));
+        m->gemm_mode = saved;
+        m->ctx->sync();
+        float ms = 0.f;
+        BASS_CUDA(cudaEventElapsedTime(&ms, a, b));
+        *ms_per_launch = ms / reps;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    });
+}
+
 int bass_gemm(bass_model* m, int mode, int M, int N, int K, const void* x, const void* w, float* y) {
     return guarded(m->ctx, [&] {
         BASS_REQUIRE(M >= 1 && N >= 1 && K >= 1, "geometry: GEMM sizes must be positive");

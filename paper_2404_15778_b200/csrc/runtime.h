@@ -161,16 +161,17 @@ void tc_release(bass_model& m);
 // tcgen05 attention (attn_tc.cu).  A plan (work list + Q tensor map) is
 // built once per forward and reused by every layer.
 struct AttnPlan {
-    bool valid = false;
-    int NQ = 0, pad_len = 0, strategy = 0, H = 0, cap = 0, n_slots = 0, mc = 0;
+    bool valid = false, fused = false;   // fused: CTA walks all chunks, writes ctx directly
+    int NQ = 0, pad_len = 0, strategy = 0, H = 0, cap = 0, n_slots = 0, mc = 0, tmem_cols = 32;
     std::vector<int> first;
     void* work = nullptr;
     CUtensorMap tq;
 };
 void tc_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, int n_slots, const std::vector<int32_t>& qn,
-                       const std::vector<int32_t>& off, int H, int cap, DevBuf& work_buf, AttnPlan& plan);
+                       const std::vector<int32_t>& off, int H, int cap, DevBuf& work_buf, AttnPlan& plan,
+                       bool allow_fused = true);
 void tc_attention_run(bass_ctx* ctx, const AttnPlan& plan, const void* kc, const void* vc, const Seqs& seqs_dev,
-                      float* part_o, float* part_ml);
+                      float* part_o, float* part_ml, void* out);
 bool tc_attention_supported(int dtype, int dh);
 void tc_attention(bass_ctx* ctx, int strategy, const void* q, int M, const void* kc, const void* vc, int n_slots,
                   const Seqs& seqs_dev, const std::vector<int32_t>& qn, const std::vector<int32_t>& off, int H, int cap,

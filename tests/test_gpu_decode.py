@@ -296,3 +296,37 @@ def test_bf16_dh128_tcgen05_attention_path(B):
     spec2 = B.decode_speculative(B.CudaModel(dwm, 4), B.CudaModel(dwd, 4), req,
                                  B.AdaptiveDraftController())
     assert spec2.tokens == base.tokens
+
+
+_FUSED_PROBE = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2404_15778_b200 as B
+from oracle import ragged as OR
+g = OR.Geometry(2, 4, 512, 128, 1000, 2048)
+dw = B.DeviceWeights.from_reference(OR.init_weights(g, 41), "bf16")
+m = B.CudaModel(dw, 3)
+rng = np.random.default_rng(1)
+for s, n in enumerate((700, 90, 1500)):
+    m.prefill(s, rng.integers(0, 1000, n).tolist())
+out = m.forward([0, 1, 2], [rng.integers(0, 1000, n).tolist() for n in (12, 1, 40)])
+np.save(sys.argv[2], np.concatenate(out))
+"""
+
+
+def test_fused_and_split_attention_bitwise_equal(tmp_path):
+    """The fused (CTA walks all key chunks) and split (one CTA per chunk +
+    combine kernel) tcgen05 attention paths give identical bits."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    probe = tmp_path / "probe.py"
+    probe.write_text(_FUSED_PROBE)
+    outs = []
+    for env_extra in ({}, {"BASS_ATTN_SPLIT_ONLY": "1"}):
+        path = tmp_path / f"out{len(outs)}.npy"
+        env = dict(os.environ, **env_extra)
+        subprocess.run([sys.executable, str(probe), root, str(path)], check=True, env=env, timeout=240)
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1])
