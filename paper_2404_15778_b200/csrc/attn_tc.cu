@@ -366,8 +366,8 @@ static void launch(bass_ctx* ctx, const CUtensorMap& tq, const CUtensorMap& tk, 
         BASS_CUDA(cudaFuncSetAttribute(attn_tc_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
         attr = true;
     }
-    attn_tc_kernel<NQ><<<dim3(n_work, H), THREADS, Cf::SMEM, ctx->stream>>>(tq, tk, tv, seqs, work, H, cap, pad_len,
-                                                                           tmem_cols, po, pml, max_chunks, out);
+    BASS_CUDA(launch_pdl(attn_tc_kernel<NQ>, dim3(n_work, H), dim3(THREADS), (size_t)Cf::SMEM, ctx->stream, tq, tk, tv,
+                         seqs, work, H, cap, pad_len, tmem_cols, po, pml, max_chunks, out));
 }
 
 static int pow2_cols(int c) {

@@ -5,6 +5,8 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <utility>
+
 #define BASS_DEV __device__ __forceinline__
 
 namespace bass {
@@ -15,6 +17,27 @@ constexpr int kWarp = 32;
 // stream to start its prologue now; it still waits (griddepcontrol.wait) for
 // this grid's completion before touching our outputs.
 BASS_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// Wait until the preceding kernel in the stream has completed and its writes
+// are visible (no-op when the kernel was not launched with PDL).  Every
+// PDL-launched kernel calls this before its first dependent global access.
+BASS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Launch with programmatic stream serialization (PDL).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // element access in either storage dtype; all math is fp32 (or fp64 for sampling)
 BASS_DEV float ld(const float* p, int64_t i) { return p[i]; }

@@ -296,7 +296,8 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                 DraftPick dp{d_slot, d_sid, d_pos, e->proposals, bass_engine::kPstride, j,
                              r->align, r->align_seed, d_align, d_plen, maxnew};
                 ProfScope prof(c, BASS_PROF_SAMPLE, (double)nA * V * 4);
-                if (greedy) draft_greedy_kernel<<<nA, SM_THREADS, 0, st>>>(out, V, dp);
+                if (greedy) BASS_CUDA(launch_pdl(draft_greedy_kernel, dim3(nA), dim3(SM_THREADS), 0, st,
+                                                 (const float*)out, V, dp));
                 else draft_sample_kernel<<<nA, SM_THREADS, 0, st>>>(out, V, r->temperature, r->top_p, r->seed,
                                                                      scratch, dp);
                 launched(c);
@@ -321,7 +322,8 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
             const int R = nA * (l + 1);
             {
                 ProfScope prof(c, BASS_PROF_SAMPLE, (double)R * V * 4);
-                row_stats_kernel<<<R, SM_THREADS, 0, st>>>(vlog, V, vamax, vlse);
+                BASS_CUDA(launch_pdl(row_stats_kernel, dim3(R), dim3(SM_THREADS), 0, st, (const float*)vlog, V, vamax,
+                                     vlse));
             }
             launched(c);
             if (!greedy) {
@@ -333,7 +335,7 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
             }
             StepArgs sa{nA, l, V, d_slot, d_com, d_gen, e->proposals, bass_engine::kPstride, vlog, vamax, vlse,
                         maxnew, r->eos_token, accf, corr, btok, greedy ? 1 : 0, step_dev};
-            finalize_kernel<<<(nA + 63) / 64, 64, 0, st>>>(sa);
+            BASS_CUDA(launch_pdl(finalize_kernel, dim3((nA + 63) / 64), dim3(64), 0, st, sa));
             launched(c);
             c->d2h_bytes += (int64_t)nA * sizeof(SlotStep);
             BASS_CUDA(cudaMemcpyAsync(e->step_host, step_dev, (size_t)nA * sizeof(SlotStep),

@@ -320,7 +320,7 @@ static State& state(bass_model& m) {
 static int choose_splits(int sm_count, int N, int K) {
     const int n_tiles = (N + BN - 1) / BN, k_iters = K / BK;
     const int slots = 2 * sm_count;
-    static const int cap_s = getenv("BASS_MAX_SPLIT") ? atoi(getenv("BASS_MAX_SPLIT")) : 8;
+    static const int cap_s = getenv("BASS_MAX_SPLIT") ? atoi(getenv("BASS_MAX_SPLIT")) : 4;
     int best_s = 1;
     for (int s = 2; s <= cap_s; ++s)
         if (n_tiles * s <= slots && k_iters / s >= 4) best_s = s;

@@ -31,6 +31,7 @@ __global__ void embed_kernel(const TW* __restrict__ tok_emb, const TW* __restric
                              Rows rows, const int32_t* __restrict__ proposals, int pstride,
                              int d, float* __restrict__ x) {
     pdl_trigger();
+    pdl_wait();
     const int r = blockIdx.x;
     int id = rows.tok[r];
     if (id < 0) id = proposals[rows.slot[r] * pstride + (-id - 1)];
@@ -55,6 +56,7 @@ __global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(const float* __re
                                                                TA* __restrict__ out) {
     __shared__ float red[33];
     pdl_trigger();
+    pdl_wait();
     const int r = blockIdx.x;
     const int src = gather ? gather[r] : r;
     const float4* xr = reinterpret_cast<const float4*>(x + (int64_t)src * d);
@@ -208,6 +210,7 @@ __global__ void __launch_bounds__(AT_THREADS) attn_partial_kernel(
     float* Qs = Vs + AT_SUB * DH;                      // [AT_QT][DH]
 
     pdl_trigger();
+    pdl_wait();
     const AttnWork wk = work[blockIdx.z];
     const int h = blockIdx.y, c = blockIdx.x;
     const int slot = seqs.slot[wk.seq], qn = seqs.qn[wk.seq], off = seqs.off[wk.seq];
@@ -309,6 +312,7 @@ __global__ void attn_combine_kernel(const float* __restrict__ part_o, const floa
                                     const int32_t* __restrict__ row_pos, int H, int max_chunks,
                                     int chunk, TA* __restrict__ out) {
     pdl_trigger();
+    pdl_wait();
     const int r = blockIdx.x, h = blockIdx.y;
     const int nc = row_pos[r] / chunk + 1;
     const int64_t base = ((int64_t)r * H + h) * max_chunks;

@@ -174,7 +174,8 @@ template <typename TA>
 static void launch_layernorm(bass_model& m, const float* x, const int32_t* gather, const float* g,
                              const float* b, int rows, TA* out) {
     ProfScope prof(m.ctx, BASS_PROF_NORM, (double)rows * m.g.d_model * (4.0 + sizeof(TA)));
-    layernorm_kernel<TA><<<rows, 256, 0, m.ctx->stream>>>(x, gather, g, b, m.g.d_model, out);
+    BASS_CUDA(launch_pdl(layernorm_kernel<TA>, dim3(rows), dim3(256), 0, m.ctx->stream, x, gather, g, b,
+                         m.g.d_model, out));
     check_launch(m.ctx);
 }
 
@@ -244,8 +245,8 @@ static void launch_attention_t(bass_ctx* ctx, int strategy, const void* q, const
             int nq = 0;
             tc_attention(ctx, strategy, q, M, kc, vc, n_slots, seqs_dev, qn, off, H, cap, work_buf, part_o, part_ml,
                          mc, &nq);
-            attn_combine_kernel<TA, DH><<<dim3(M, H), DH, 0, ctx->stream>>>(part_o, part_ml, row_pos_dev, H, mc, 128,
-                                                                            (TA*)out);
+            BASS_CUDA(launch_pdl(attn_combine_kernel<TA, DH>, dim3(M, H), dim3(DH), 0, ctx->stream,
+                                 (const float*)part_o, (const float*)part_ml, row_pos_dev, H, mc, 128, (TA*)out));
             check_launch(ctx);
             return;
         }
@@ -304,8 +305,8 @@ static void launch_attention_t(bass_ctx* ctx, int strategy, const void* q, const
             strategy == BASS_PAD ? max_L : 0, part_o, part_ml, max_chunks);
         check_launch(ctx);
     }
-    attn_combine_kernel<TA, DH><<<dim3(M, H), DH, 0, ctx->stream>>>(part_o, part_ml, row_pos_dev, H, max_chunks,
-                                                                    AT_CHUNK, (TA*)out);
+    BASS_CUDA(launch_pdl(attn_combine_kernel<TA, DH>, dim3(M, H), dim3(DH), 0, ctx->stream, (const float*)part_o,
+                         (const float*)part_ml, row_pos_dev, H, max_chunks, (int)AT_CHUNK, (TA*)out));
     check_launch(ctx);
 }
 
@@ -366,12 +367,12 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
     static DevBuf work_buf;   // per-process attention work list (tiny)
 
     if (m.dtype == BASS_BF16)
-        embed_kernel<__nv_bfloat16><<<M, 128, 0, st>>>((const __nv_bfloat16*)m.tok_emb,
-                                                       (const __nv_bfloat16*)m.pos_emb, rows, proposals, pstride,
-                                                       d, x);
+        BASS_CUDA(launch_pdl(embed_kernel<__nv_bfloat16>, dim3(M), dim3(128), 0, st,
+                             (const __nv_bfloat16*)m.tok_emb, (const __nv_bfloat16*)m.pos_emb, rows, proposals,
+                             pstride, d, x));
     else
-        embed_kernel<float><<<M, 128, 0, st>>>((const float*)m.tok_emb, (const float*)m.pos_emb, rows, proposals,
-                                               pstride, d, x);
+        BASS_CUDA(launch_pdl(embed_kernel<float>, dim3(M), dim3(128), 0, st, (const float*)m.tok_emb,
+                             (const float*)m.pos_emb, rows, proposals, pstride, d, x));
     check_launch(ctx);
 
     // tcgen05 attention: one plan (work list, Q map) for all layers of this forward
@@ -403,8 +404,9 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
             ProfScope prof(ctx, BASS_PROF_ATTN, attn_bytes, attn_flops);
             tc_attention_run(ctx, plan, e.kc, e.vc, seqs, pa_o, pa_ml, cx);
             if (!plan.fused) {
-                attn_combine_kernel<__nv_bfloat16, 128><<<dim3(M, H), 128, 0, st>>>(pa_o, pa_ml, rows.pos, H,
-                                                                                    plan.mc, 128, (__nv_bfloat16*)cx);
+                BASS_CUDA(launch_pdl(attn_combine_kernel<__nv_bfloat16, 128>, dim3(M, H), dim3(128), 0, st,
+                                     (const float*)pa_o, (const float*)pa_ml, rows.pos, H, plan.mc, 128,
+                                     (__nv_bfloat16*)cx));
                 check_launch(ctx);
             }
         } else {

@@ -238,6 +238,8 @@ BASS_DEV int inverse_cdf_block(int V, double u, W w, ShapeSmem& sm) {
 static __global__ void __launch_bounds__(SM_THREADS) row_stats_kernel(const float* __restrict__ logits,
                                                                int V, int32_t* __restrict__ amax,
                                                                double* __restrict__ lse) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ float fv[33];
     __shared__ int iv[33];
     __shared__ double dv[33];
@@ -277,6 +279,8 @@ BASS_DEV int aligned_override(const DraftPick& d, int slot, int pos, int V, int 
 // greedy draft step: proposal = argmax of the sequence's last draft row
 static __global__ void __launch_bounds__(SM_THREADS) draft_greedy_kernel(const float* __restrict__ logits,
                                                                   int V, DraftPick d) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ float fv[33];
     __shared__ int iv[33];
     const int i = blockIdx.x;
@@ -294,6 +298,8 @@ static __global__ void __launch_bounds__(SM_THREADS) draft_sample_kernel(const f
                                                                   uint64_t seed, double* scratch,
                                                                   DraftPick d) {
     __shared__ ShapeSmem sm;
+    pdl_trigger();
+    pdl_wait();
     const int i = blockIdx.x;
     const float* row = logits + (int64_t)i * V;
     double* e = scratch + (int64_t)blockIdx.x * V;
@@ -408,6 +414,8 @@ struct StepArgs {
 // accepted prefix + correction / bonus + EOS/length finalize + logprobs
 // (ref:engine.py:276-349, _finalize_emitted :103-117, logprob :99-100)
 static __global__ void finalize_kernel(StepArgs a) {
+    pdl_trigger();
+    pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.nA) return;
     const int slot = a.slot[i], l = a.l, rb = i * (l + 1);
@@ -484,6 +492,8 @@ struct VerifyArgs {
 
 static __global__ void __launch_bounds__(SM_THREADS) verify_sampled_kernel(VerifyArgs a) {
     __shared__ ShapeSmem sm;
+    pdl_trigger();
+    pdl_wait();
     const int j = blockIdx.x, i = blockIdx.y, l = a.l;
     const int slot = a.slot[i], sid = a.sid[slot], pos = a.committed[i] + j;
     const float* q = a.vlog + (int64_t)(i * (l + 1) + j) * a.V;
@@ -530,6 +540,8 @@ struct RegularArgs {
 static __global__ void __launch_bounds__(SM_THREADS) regular_pick_kernel(const float* __restrict__ logits,
                                                                   RegularArgs a) {
     __shared__ ShapeSmem sm;
+    pdl_trigger();
+    pdl_wait();
     const int i = blockIdx.x;
     const float* row = logits + (int64_t)i * a.V;
     double* e = a.scratch + (int64_t)i * a.V;
