@@ -449,7 +449,7 @@ void tc_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, int n_
         const int len = strategy == BASS_PAD ? max_L : off[i] + std::min(qn[i], t0 + NQ);
         return (len + CH - 1) / CH;
     };
-    static const bool no_fuse = getenv("BASS_ATTN_SPLIT_ONLY") != nullptr;
+    static const bool no_fuse = getenv("BASS_ATTN_SPLIT_ONLY") && atoi(getenv("BASS_ATTN_SPLIT_ONLY")) == 1;
     int max_nch = 0;
     for (int i = 0; i < n_seq; ++i)
         for (int t0 = 0; t0 < (strategy == BASS_PAD ? max_qn : qn[i]); t0 += NQ)
