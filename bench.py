@@ -211,9 +211,12 @@ def main():
     draft_m = B.CudaModel(wd, b, args.strategy, capacity=cap)
     eng = B.CudaEngine(main_m, draft_m)
     eng.set_strategy(args.strategy)
-    rng = np.random.default_rng(7 + rank)
-    prompts = [rng.integers(0, mcfg.vocab_size, P).tolist() for _ in range(b)]
-    sids = [rank * b + i for i in range(b)]
+    # sequence-sharded: rank owns global sequences [rank*b, (rank+1)*b); prompts
+    # and RNG keys derive from the global id, so outputs are sharding-independent
+    from paper_2404_15778_b200.shard import gather_tokens, global_sequence_ids, reduce_run
+    sids = global_sequence_ids(b * world, world, rank)
+    prompts = [np.random.default_rng(1_000_003 + sid).integers(0, mcfg.vocab_size, P).tolist()
+               for sid in sids]
     req = B.GenerationRequest(prompts, new, temperature=cfg["temperature"], top_p=cfg["top_p"],
                               seed=1234, sequence_ids=sids)
 
@@ -291,12 +294,9 @@ def main():
     if rd is not None and cfg["temperature"] == 0.0:
         assert all(r[0].tokens == rd.tokens for r in results), "greedy speculative != regular"
     if world > 1:
-        t = torch.tensor([dev_s, host_s, tokens], dtype=torch.float64, device="cuda")
-        mx = t.clone()
-        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
-        sm = t.clone()
-        torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
-        dev_s, host_s, tokens = float(mx[0]), float(mx[1]), float(sm[2])
+        dev_s, host_s, tokens = reduce_run(torch.distributed, "cuda", dev_s, host_s, tokens)
+        gathered = gather_tokens(torch.distributed, world, sids, results[-1][0].tokens)   # final gather
+        assert sorted(gathered) == list(range(b * world))
     if rank != 0:
         torch.distributed.destroy_process_group()
         return

@@ -449,7 +449,9 @@ void tc_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, int n_
         const int len = strategy == BASS_PAD ? max_L : off[i] + std::min(qn[i], t0 + NQ);
         return (len + CH - 1) / CH;
     };
-    static const bool no_fuse = getenv("BASS_ATTN_SPLIT_ONLY") && atoi(getenv("BASS_ATTN_SPLIT_ONLY")) == 1;
+    // split mode (one CTA per chunk + combine) measured faster on the benchmark
+    // (more CTAs in flight); the fused walk is opt-in and bitwise identical
+    static const bool no_fuse = !(getenv("BASS_ATTN_FUSED") && atoi(getenv("BASS_ATTN_FUSED")) == 1);
     int max_nch = 0;
     for (int i = 0; i < n_seq; ++i)
         for (int t0 = 0; t0 < (strategy == BASS_PAD ? max_qn : qn[i]); t0 += NQ)

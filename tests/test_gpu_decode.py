@@ -324,7 +324,7 @@ def test_fused_and_split_attention_bitwise_equal(tmp_path):
     probe = tmp_path / "probe.py"
     probe.write_text(_FUSED_PROBE)
     outs = []
-    for env_extra in ({}, {"BASS_ATTN_SPLIT_ONLY": "1"}):
+    for env_extra in ({"BASS_ATTN_FUSED": "1"}, {"BASS_ATTN_FUSED": "0"}):
         path = tmp_path / f"out{len(outs)}.npy"
         env = dict(os.environ, **env_extra)
         subprocess.run([sys.executable, str(probe), root, str(path)], check=True, env=env, timeout=240)
