@@ -310,11 +310,12 @@ __global__ void __launch_bounds__(AT_THREADS) attn_partial_kernel(
 template <typename TA, int DH>
 __global__ void attn_combine_kernel(const float* __restrict__ part_o, const float* __restrict__ part_ml,
                                     const int32_t* __restrict__ row_pos, int H, int max_chunks,
-                                    int chunk, TA* __restrict__ out) {
+                                    int chunk, TA* __restrict__ out, int skip_single = 0) {
     pdl_trigger();
     pdl_wait();
     const int r = blockIdx.x, h = blockIdx.y;
     const int nc = row_pos[r] / chunk + 1;
+    if (skip_single && nc == 1) return;   // already written normalised by the attention kernel
     const int64_t base = ((int64_t)r * H + h) * max_chunks;
     float mx = -INFINITY;
     for (int c = 0; c < nc; ++c) mx = fmaxf(mx, part_ml[(base + c) * 2]);

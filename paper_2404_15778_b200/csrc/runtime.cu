@@ -224,6 +224,12 @@ void gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, i
 #undef BASS_GEMM_CASE
 }
 
+// BASS_ATTN_MODE=chunk selects the earlier one-chunk-per-CTA kernel (attn_tc.cu)
+static bool attn_stream_mode() {
+    static const bool chunk = getenv("BASS_ATTN_MODE") && std::string(getenv("BASS_ATTN_MODE")) == "chunk";
+    return !chunk;
+}
+
 template <typename TA, int DH>
 static void launch_attention_t(bass_ctx* ctx, int strategy, const void* q, const void* kc, const void* vc,
                                const Seqs& seqs_dev, const std::vector<int32_t>& qn,
@@ -242,11 +248,25 @@ static void launch_attention_t(bass_ctx* ctx, int strategy, const void* q, const
                 aflops += 4.0 * H * DH * qn[i] * (off[i] + 0.5 * (qn[i] + 1));
             }
             ProfScope prof(ctx, BASS_PROF_ATTN, abytes, aflops);
+            if (attn_stream_mode()) {
+                AttnPlan plan;
+                stream_attention_plan(ctx, strategy, q, M, n_slots, qn, off, H, cap, work_buf, plan);
+                float* so = (float*)po.need((size_t)M * H * plan.mc * DH * 4, ctx->stream);
+                float* sml = (float*)pml.need((size_t)M * H * plan.mc * 2 * 4, ctx->stream);
+                stream_attention_run(ctx, plan, kc, vc, seqs_dev, so, sml, out);
+                if (plan.needs_combine) {
+                    BASS_CUDA(launch_pdl(attn_combine_kernel<TA, DH>, dim3(M, H), dim3(DH), 0, ctx->stream,
+                                         (const float*)so, (const float*)sml, row_pos_dev, H, plan.mc,
+                                         stream_split_len(), (TA*)out, 1));
+                    check_launch(ctx);
+                }
+                return;
+            }
             int nq = 0;
             tc_attention(ctx, strategy, q, M, kc, vc, n_slots, seqs_dev, qn, off, H, cap, work_buf, part_o, part_ml,
                          mc, &nq);
             BASS_CUDA(launch_pdl(attn_combine_kernel<TA, DH>, dim3(M, H), dim3(DH), 0, ctx->stream,
-                                 (const float*)part_o, (const float*)part_ml, row_pos_dev, H, mc, 128, (TA*)out));
+                                 (const float*)part_o, (const float*)part_ml, row_pos_dev, H, mc, 128, (TA*)out, 0));
             check_launch(ctx);
             return;
         }
@@ -306,7 +326,7 @@ static void launch_attention_t(bass_ctx* ctx, int strategy, const void* q, const
         check_launch(ctx);
     }
     BASS_CUDA(launch_pdl(attn_combine_kernel<TA, DH>, dim3(M, H), dim3(DH), 0, ctx->stream, (const float*)part_o,
-                         (const float*)part_ml, row_pos_dev, H, max_chunks, (int)AT_CHUNK, (TA*)out));
+                         (const float*)part_ml, row_pos_dev, H, max_chunks, (int)AT_CHUNK, (TA*)out, 0));
     check_launch(ctx);
 }
 
@@ -380,7 +400,10 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
     double attn_bytes = 0.0, attn_flops = 0.0;
     float *pa_o = nullptr, *pa_ml = nullptr;
     if (m.dtype == BASS_BF16 && tc_attention_supported(BASS_BF16, dh)) {
-        tc_attention_plan(ctx, strategy, q, M, kv.n_slots, b.qn, b.off, H, kv.cap, work_buf, plan);
+        if (attn_stream_mode())
+            stream_attention_plan(ctx, strategy, q, M, kv.n_slots, b.qn, b.off, H, kv.cap, work_buf, plan);
+        else
+            tc_attention_plan(ctx, strategy, q, M, kv.n_slots, b.qn, b.off, H, kv.cap, work_buf, plan);
         pa_o = (float*)m.part_o.need((size_t)M * H * plan.mc * dh * 4, st);
         pa_ml = (float*)m.part_ml.need((size_t)M * H * plan.mc * 2 * 4, st);
         for (int i = 0; i < n_seq; ++i) {
@@ -402,12 +425,22 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
         gemm(m, EPI_QKV, h, L.wqkv, M, 3 * d, d, e);
         if (plan.valid) {
             ProfScope prof(ctx, BASS_PROF_ATTN, attn_bytes, attn_flops);
-            tc_attention_run(ctx, plan, e.kc, e.vc, seqs, pa_o, pa_ml, cx);
-            if (!plan.fused) {
-                BASS_CUDA(launch_pdl(attn_combine_kernel<__nv_bfloat16, 128>, dim3(M, H), dim3(128), 0, st,
-                                     (const float*)pa_o, (const float*)pa_ml, rows.pos, H, plan.mc, 128,
-                                     (__nv_bfloat16*)cx));
-                check_launch(ctx);
+            if (plan.stream) {
+                stream_attention_run(ctx, plan, e.kc, e.vc, seqs, pa_o, pa_ml, cx);
+                if (plan.needs_combine) {
+                    BASS_CUDA(launch_pdl(attn_combine_kernel<__nv_bfloat16, 128>, dim3(M, H), dim3(128), 0, st,
+                                         (const float*)pa_o, (const float*)pa_ml, rows.pos, H, plan.mc,
+                                         stream_split_len(), (__nv_bfloat16*)cx, 1));
+                    check_launch(ctx);
+                }
+            } else {
+                tc_attention_run(ctx, plan, e.kc, e.vc, seqs, pa_o, pa_ml, cx);
+                if (!plan.fused) {
+                    BASS_CUDA(launch_pdl(attn_combine_kernel<__nv_bfloat16, 128>, dim3(M, H), dim3(128), 0, st,
+                                         (const float*)pa_o, (const float*)pa_ml, rows.pos, H, plan.mc, 128,
+                                         (__nv_bfloat16*)cx, 0));
+                    check_launch(ctx);
+                }
             }
         } else {
             launch_attention(ctx, m.dtype, dh, strategy, q, e.kc, e.vc, seqs, b.qn, b.off, rows.pos, M, H, kv.cap,

@@ -162,6 +162,8 @@ void tc_release(bass_model& m);
 // built once per forward and reused by every layer.
 struct AttnPlan {
     bool valid = false, fused = false;   // fused: CTA walks all chunks, writes ctx directly
+    bool stream = false;                 // streaming flash-decoding kernel (attn_stream.cu)
+    bool needs_combine = false;          // some row spans more than one 1024-key split
     int NQ = 0, pad_len = 0, strategy = 0, H = 0, cap = 0, n_slots = 0, mc = 0, tmem_cols = 32;
     std::vector<int> first;
     void* work = nullptr;
@@ -173,6 +175,13 @@ void tc_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, int n_
 void tc_attention_run(bass_ctx* ctx, const AttnPlan& plan, const void* kc, const void* vc, const Seqs& seqs_dev,
                       float* part_o, float* part_ml, void* out);
 bool tc_attention_supported(int dtype, int dh);
+// streaming tcgen05 attention (attn_stream.cu): the default bf16 d_head=128 path
+int stream_split_len();
+void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, int n_slots,
+                           const std::vector<int32_t>& qn, const std::vector<int32_t>& off, int H, int cap,
+                           DevBuf& work_buf, AttnPlan& plan);
+void stream_attention_run(bass_ctx* ctx, const AttnPlan& plan, const void* kc, const void* vc, const Seqs& seqs_dev,
+                          float* part_o, float* part_ml, void* out);
 void tc_attention(bass_ctx* ctx, int strategy, const void* q, int M, const void* kc, const void* vc, int n_slots,
                   const Seqs& seqs_dev, const std::vector<int32_t>& qn, const std::vector<int32_t>& off, int H, int cap,
                   DevBuf& work_buf, float* part_o, float* part_ml, int max_chunks, int* nq_out);
