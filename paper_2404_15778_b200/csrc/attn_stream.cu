@@ -109,18 +109,20 @@ struct Work {
 
 template <int NQ>
 struct Cfg {
-    static constexpr int STAGES = NQ <= 32 ? 3 : 2;
-    static constexpr int KV_TILE = CH * 128;   // one 64-wide swizzle sub-tile (bytes)
-    static constexpr int STAGE = 4 * KV_TILE;  // K0 K1 V0 V1
-    static constexpr int Q_TILE = NQ * 128;
-    static constexpr int OFF_Q = STAGES * STAGE, OFF_P = OFF_Q + 2 * Q_TILE;
-    static constexpr int OFF_ST = OFF_P + 2 * Q_TILE;       // floats: m_run, l_run, alpha, m_new, red_max[4], red_sum[4]
-    static constexpr int OFF_BAR = OFF_ST + 12 * NQ * 4;
+    static constexpr int STAGES = 2;
+    static constexpr int KV_TILE = CH * 128;     // one 64-wide swizzle sub-tile (bytes)
+    static constexpr int STAGE = 4 * KV_TILE;    // K0 K1 V0 V1
+    static constexpr int R_TILE = 128 * 128;     // 128 rows x 64 bf16: one sub-tile of Q or P
+    static constexpr int OFF_Q = STAGES * STAGE, OFF_P = OFF_Q + 2 * R_TILE;
+    static constexpr int OFF_BAR = OFF_P + 2 * R_TILE;
     static constexpr int NBAR = 2 * STAGES + 1 + 2 + 1 + 1;   // kv_full, kv_empty, q_full, s_full[2], p_full, o_done
     static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
-    static constexpr int TMEM_COLS = 3 * NQ <= 32 ? 32 : 3 * NQ <= 64 ? 64 : 3 * NQ <= 128 ? 128 : 3 * NQ <= 256 ? 256 : 512;
+    static constexpr int TMEM_COLS = 512;        // S0 [0,128) S1 [128,256) O [256,384)
 };
 
+// Query rows on TMEM lanes: S = Q . K^T (M = 128 query rows, N = 128 keys),
+// so each softmax thread owns one row and the max / sum over keys are
+// register-local; O = P . V (A = P from smem, B = V read MN-major).
 template <int NQ>
 __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
     const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
@@ -137,16 +139,11 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
     const int s0 = wk.split * SPLIT;
     if (wk.t0 >= qn || wk.nch <= 0) return;   // idle CTA (uniform)
     const int nch = wk.nch;
+    const int rows_valid = min(128, qn - wk.t0);
 
     const uint32_t raw = su32(smem_raw);
     const uint32_t base = (raw + 1023) & ~1023u;
     uint8_t* sm = smem_raw + (base - raw);
-    float* m_run = reinterpret_cast<float*>(sm + Cf::OFF_ST);
-    float* l_run = m_run + NQ;
-    float* alpha = l_run + NQ;
-    float* m_new = alpha + NQ;
-    float* red_max = m_new + NQ;   // [4][NQ]
-    float* red_sum = red_max + 4 * NQ;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Cf::OFF_BAR);
     uint64_t* kv_full = bars;
     uint64_t* kv_empty = bars + ST;
@@ -162,10 +159,6 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    if (threadIdx.x >= 128 && threadIdx.x < 128 + NQ) {
-        m_run[threadIdx.x - 128] = -INFINITY;
-        l_run[threadIdx.x - 128] = 0.f;
-    }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
                      "r"(Cf::TMEM_COLS)
@@ -175,16 +168,16 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
     fence_before();
     __syncthreads();
     fence_after();
-    const uint32_t tmem = *tmem_slot;                 // S buffers at cols [0, NQ) and [NQ, 2NQ); O at 2NQ
-    const uint32_t tO = tmem + 2 * NQ;
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tO = tmem + 256;
     const int kv_row0 = (slot * H + h) * cap + s0;
 
     if (warp == 0) {
         if (lane == 0) {   // ---- producer
             asm volatile("griddepcontrol.wait;" ::: "memory");   // Q and this step's K/V rows come from the QKV GEMM
-            mbar_expect_tx(su32(q_full), 2 * Cf::Q_TILE);
+            mbar_expect_tx(su32(q_full), 2 * Cf::R_TILE);
             for (int s = 0; s < 2; ++s)
-                tma_2d(&tq, base + Cf::OFF_Q + s * Cf::Q_TILE, su32(q_full), h * DH + s * 64, q0row + wk.t0);
+                tma_2d(&tq, base + Cf::OFF_Q + s * Cf::R_TILE, su32(q_full), h * DH + s * 64, q0row + wk.t0);
             for (int c = 0; c < nch; ++c) {
                 const int s = c % ST;
                 if (c >= ST) mbar_wait(su32(&kv_empty[s]), ((c / ST) - 1) & 1);
@@ -199,14 +192,15 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
         __syncwarp();
     } else if (warp == 1) {
         if (lane == 0) {   // ---- MMA issuer
-            constexpr uint32_t ID1 = idesc(NQ, 0), ID2 = idesc(NQ, 1);
-            auto mma1 = [&](int c) {   // S^T_c = K_c . Q^T
+            constexpr uint32_t ID1 = idesc(128, 0);                      // S = Q . K^T
+            constexpr uint32_t ID2 = idesc(128, 0) | (1u << 16);          // O = P . V  (B = V, MN-major)
+            auto mma1 = [&](int c) {
                 const uint32_t st = base + (c % ST) * Cf::STAGE;
 #pragma unroll
                 for (int kk = 0; kk < DH / 16; ++kk) {
                     const uint32_t sub = kk >> 2, in = (kk & 3) * 32;
-                    umma(tmem + (c & 1) * NQ, sdesc(st + sub * Cf::KV_TILE + in, 16, 1024),
-                         sdesc(base + Cf::OFF_Q + sub * Cf::Q_TILE + in, 16, 1024), ID1, kk > 0);
+                    umma(tmem + (c & 1) * 128, sdesc(base + Cf::OFF_Q + sub * Cf::R_TILE + in, 16, 1024),
+                         sdesc(st + sub * Cf::KV_TILE + in, 16, 1024), ID1, kk > 0);
                 }
                 commit(su32(&s_full[c & 1]));
             };
@@ -224,10 +218,10 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
                 fence_after();
                 const uint32_t st = base + (c % ST) * Cf::STAGE;
 #pragma unroll
-                for (int kk = 0; kk < CH / 16; ++kk) {   // O^T += V_c^T . P_c^T
+                for (int kk = 0; kk < CH / 16; ++kk) {
                     const uint32_t sub = kk >> 2, in = (kk & 3) * 32;
-                    umma(tO, sdesc(st + 2 * Cf::KV_TILE + kk * 2048, Cf::KV_TILE, 1024),
-                         sdesc(base + Cf::OFF_P + sub * Cf::Q_TILE + in, 16, 1024), ID2, (c > 0 || kk > 0) ? 1u : 0u);
+                    umma(tO, sdesc(base + Cf::OFF_P + sub * Cf::R_TILE + in, 16, 1024),
+                         sdesc(st + 2 * Cf::KV_TILE + kk * 2048, Cf::KV_TILE, 1024), ID2, (c > 0 || kk > 0) ? 1u : 0u);
                 }
                 commit(su32(o_done));
                 commit(su32(&kv_empty[c % ST]));
@@ -235,101 +229,126 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
         }
         __syncwarp();
     } else if (warp >= 4) {
-        // ---- softmax / correction / epilogue: TMEM lane quarter = warp % 4
-        const int sw = warp - 4, key = sw * 32 + lane, tid = threadIdx.x - 128;
-        const uint32_t lane_off = (uint32_t)(sw * 32) << 16;
+        // ---- softmax / correction / epilogue: thread r owns query row t0 + r (TMEM lane r)
+        const int r = threadIdx.x - 128, t = wk.t0 + r;
+        const bool warp_live = (warp - 4) * 32 < rows_valid;   // warp-uniform
+        const bool live = r < rows_valid;
+        const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
         const float scale = sqrtf((float)DH);
-        uint8_t* P = sm + Cf::OFF_P;
-        const int psub = key >> 6, pin = key & 63;
+        uint8_t* Prow = sm + Cf::OFF_P + r * 128;
+        float m_run = -INFINITY, l_run = 0.f;
         for (int c = 0; c < nch; ++c) {
-            const int kpos = s0 + c * CH + key;
-            const uint32_t tS = tmem + lane_off + (c & 1) * NQ;
+            const int kbase = s0 + c * CH;
+            const uint32_t tS = tmem + lane_off + (c & 1) * 128;
             mbar_wait(su32(&s_full[c & 1]), (c >> 1) & 1);
             fence_after();
+            float mn = m_run, alpha = 1.f;
+            if (warp_live) {
+                float mc = -INFINITY;
 #pragma unroll 1
-            for (int j0 = 0; j0 < NQ; j0 += 16) {
-                float v[16];
-                ld16(tS + j0, v);
+                for (int j0 = 0; j0 < 128; j0 += 16) {
+                    float v[16];
+                    ld16(tS + j0, v);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int t = wk.t0 + j0 + j;
-                    const bool ok = t < qn && kpos <= off + t && kpos < L;
-                    const float mx = warp_max(ok ? v[j] / scale : -INFINITY);
-                    if (lane == 0) red_max[sw * NQ + j0 + j] = mx;
+                    for (int j = 0; j < 16; ++j) {
+                        const int kp = kbase + j0 + j;
+                        if (live && kp <= off + t && kp < L) mc = fmaxf(mc, v[j] / scale);
+                    }
                 }
+                mn = fmaxf(m_run, mc);
+                alpha = mn == -INFINITY ? 1.f : expf(m_run - mn);   // m_run = -inf -> 0
             }
-            softmax_bar();
-            if (tid < NQ) {
-                const float mc = fmaxf(fmaxf(red_max[tid], red_max[NQ + tid]),
-                                       fmaxf(red_max[2 * NQ + tid], red_max[3 * NQ + tid]));
-                const float mo = m_run[tid], mn = fmaxf(mo, mc);
-                m_new[tid] = mn;
-                alpha[tid] = mn == -INFINITY ? 1.f : expf(mo - mn);   // mo = -inf -> 0
-            }
-            softmax_bar();
-            if (c > 0) {   // O^T columns *= alpha once the previous PV has landed
+            if (c > 0) {   // previous PV landed: P buffer free, O may be rescaled
                 mbar_wait(su32(o_done), (c - 1) & 1);
                 fence_after();
+                if (warp_live && __any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
-                for (int j0 = 0; j0 < NQ; j0 += 16) {
+                    for (int j0 = 0; j0 < 128; j0 += 16) {
+                        float v[16];
+                        ld16(tO + lane_off + j0, v);
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) v[j] *= alpha;
+                        st16(tO + lane_off + j0, v);
+                    }
+                }
+            }
+            float ls = 0.f;
+            if (warp_live) {
+#pragma unroll 1
+                for (int j0 = 0; j0 < 128; j0 += 16) {
                     float v[16];
-                    ld16(tO + lane_off + j0, v);
+                    ld16(tS + j0, v);
+                    uint32_t pk[8];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] *= alpha[j0 + j];
-                    st16(tO + lane_off + j0, v);
-                }
-            }
-#pragma unroll 1
-            for (int j0 = 0; j0 < NQ; j0 += 16) {
-                float v[16];
-                ld16(tS + j0, v);
+                    for (int j = 0; j < 16; j += 2) {
+                        float p2[2];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int q = j0 + j, t = wk.t0 + q;
-                    const bool ok = t < qn && kpos <= off + t && kpos < L;
-                    const float mn = m_new[q];
-                    const float p = (ok && mn != -INFINITY) ? expf(v[j] / scale - mn) : 0.f;
-                    const float ps = warp_sum(p);
-                    if (lane == 0) red_sum[sw * NQ + q] = ps;
-                    const uint32_t ch16 = (uint32_t)(pin >> 3) ^ (uint32_t)(q & 7);
-                    *(reinterpret_cast<__nv_bfloat16*>(P + psub * Cf::Q_TILE + q * 128 + ch16 * 16) + (pin & 7)) =
-                        __float2bfloat16_rn(p);
+                        for (int u = 0; u < 2; ++u) {
+                            const int kp = kbase + j0 + j + u;
+                            const bool ok = live && kp <= off + t && kp < L && mn != -INFINITY;
+                            p2[u] = ok ? expf(v[j + u] / scale - mn) : 0.f;
+                            ls += p2[u];
+                        }
+                        __nv_bfloat162 b2 = __floats2bfloat162_rn(p2[0], p2[1]);
+                        pk[j >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+                    }
+                    // keys j0..j0+15 = two 16-byte chunks of the 128B-swizzled row
+                    const int kb = j0 >> 6, ch = (j0 & 63) >> 3;
+                    uint8_t* rowp = Prow + kb * Cf::R_TILE;
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const uint32_t pc = (uint32_t)(ch + u) ^ (uint32_t)(r & 7);
+                        *reinterpret_cast<uint4*>(rowp + pc * 16) =
+                            make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+                    }
                 }
+            } else {
+                // rows of an idle warp still hand the tensor core zeros
+#pragma unroll
+                for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+                    for (int ch = 0; ch < 8; ++ch)
+                        *reinterpret_cast<uint4*>(Prow + kb * Cf::R_TILE + ch * 16) = make_uint4(0, 0, 0, 0);
             }
+            l_run = l_run * alpha + ls;
+            m_run = mn;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // P -> tensor core
             fence_before();
             softmax_bar();
-            if (tid < NQ) {
-                const float ls = (red_sum[tid] + red_sum[NQ + tid]) + (red_sum[2 * NQ + tid] + red_sum[3 * NQ + tid]);
-                l_run[tid] = l_run[tid] * alpha[tid] + ls;
-                m_run[tid] = m_new[tid];
-            }
-            if (tid == 0) mbar_arrive(su32(p_full));
+            if (r == 0) mbar_arrive(su32(p_full));
         }
-        // ---- epilogue
+        // ---- epilogue: row t, 128 head dims
         mbar_wait(su32(o_done), (nch - 1) & 1);
         fence_after();
-        softmax_bar();
-        const int d = key;
+        if (warp_live) {
+            const bool sees = live && off + t >= s0;
+            const int row = q0row + t;
+            const bool direct = off + t < SPLIT;   // whole history in split 0
+            const int64_t idx = ((int64_t)row * H + h) * max_splits + wk.split;
 #pragma unroll 1
-        for (int j0 = 0; j0 < NQ; j0 += 16) {
-            float v[16];
-            ld16(tO + lane_off + j0, v);
+            for (int j0 = 0; j0 < 128; j0 += 16) {
+                float v[16];
+                ld16(tO + lane_off + j0, v);
+                if (!sees) continue;
+                if (direct) {
+                    uint32_t pk[8];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int q = j0 + j, t = wk.t0 + q;
-                if (t >= qn || off + t < s0) continue;               // row does not see this split
-                const int row = q0row + t;
-                if (off + t < SPLIT) {                               // whole history in split 0
-                    out[((int64_t)row * H + h) * DH + d] = __float2bfloat16_rn(v[j] / l_run[q]);
-                } else {
-                    const int64_t idx = ((int64_t)row * H + h) * max_splits + wk.split;
-                    part_o[idx * DH + d] = v[j];
-                    if (d == 0) {
-                        part_ml[idx * 2] = m_run[q];
-                        part_ml[idx * 2 + 1] = l_run[q];
+                    for (int j = 0; j < 16; j += 2) {
+                        __nv_bfloat162 b2 = __floats2bfloat162_rn(v[j] / l_run, v[j + 1] / l_run);
+                        pk[j >> 1] = *reinterpret_cast<uint32_t*>(&b2);
                     }
+                    uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)row * H + h) * DH + j0);
+                    dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                    dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                } else {
+                    float4* dst = reinterpret_cast<float4*>(part_o + idx * DH + j0);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) dst[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
                 }
+            }
+            if (sees && !direct) {
+                part_ml[idx * 2] = m_run;
+                part_ml[idx * 2 + 1] = l_run;
             }
         }
     }
@@ -402,7 +421,7 @@ void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, in
         max_qn = std::max(max_qn, qn[i]);
         max_L = std::max(max_L, off[i] + qn[i]);
     }
-    const int NQ = max_qn <= 16 ? 16 : max_qn <= 32 ? 32 : max_qn <= 64 ? 64 : 128;
+    const int NQ = 128;   // query-row tile (TMEM lanes)
     std::vector<int32_t> w;
     std::vector<int> first(n_seq + 1, 0);
     bool multi = false;
