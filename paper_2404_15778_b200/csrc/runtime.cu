@@ -224,10 +224,12 @@ void gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, i
 #undef BASS_GEMM_CASE
 }
 
-// BASS_ATTN_MODE=chunk selects the earlier one-chunk-per-CTA kernel (attn_tc.cu)
+// BASS_ATTN_MODE=stream selects the streaming kernel (attn_stream.cu); the
+// default is the chunk kernel (attn_tc.cu) until the streaming one beats it
+// (profiles/r1_attn_sweep_*.jsonl: stream 0.35-0.45 TB/s vs chunk 0.8-2.4 TB/s)
 static bool attn_stream_mode() {
-    static const bool chunk = getenv("BASS_ATTN_MODE") && std::string(getenv("BASS_ATTN_MODE")) == "chunk";
-    return !chunk;
+    static const bool stream = getenv("BASS_ATTN_MODE") && std::string(getenv("BASS_ATTN_MODE")) == "stream";
+    return stream;
 }
 
 template <typename TA, int DH>
