@@ -1,21 +1,27 @@
-// Streaming flash-decoding attention on tcgen05 (sm_100a), d_head = 128.
+// Persistent warp-specialised flash-decoding attention on tcgen05 (sm_100a),
+// d_head = 128 — the ragged verify / draft / prefill attention of BASS
+// (PAD and SPLIT, ref:attention.py:85-154).
 //
-// One CTA = (sequence, query tile of NQ rows, head, 1024-key split).  Warp
-// roles (256 threads):
-//   warp 0  TMA producer: Q once, then K/V 128-key chunks into a 2-3 stage
-//           ring (64 KB per stage) — the HBM stream;
-//   warp 1  MMA issuer: S^T_c = K_c . Q^T into one of two TMEM buffers, one
-//           chunk ahead of the softmax; O^T += V_c^T . P_c^T into TMEM;
-//   warp 2  TMEM allocator;
-//   warps 4-7 softmax / correction / epilogue (TMEM lane quarter = warp % 4):
-//           online softmax per query column (causal s <= off + t, / sqrt(dh)),
-//           O rescaled in TMEM when the running max moves, P (bf16) to smem.
-// Split boundaries are absolute key positions (multiples of 1024) and every
-// reduction is per column in a fixed order, so a row's bits do not depend on
-// the batch, the tile or the strategy.  Rows whose history fits one split are
-// written normalised (o / l) directly; longer rows leave (m, l, o) per split
-// for attn_combine_kernel (same arithmetic as a one-split merge).
-// ref:attention.py:85-137 (PAD / SPLIT per-sequence causal softmax).
+// Work item = (sequence, query tile of NQ rows, head, 1024-key split).  The
+// grid is persistent (<= one CTA per SM); CTA b walks items b, b + grid, ...
+// and streams every 128-key chunk of each through a TMA ring, so loads of
+// the next item overlap the softmax / epilogue of the current one.
+//
+// Orientation: S^T = K . Q^T (UMMA M = 128 keys on TMEM lanes, N = NQ query
+// columns); O^T = V^T . P^T (M = 128 head dims, N = NQ).  Warp roles (192
+// threads):
+//   warp 0      TMA producer (Q tile per item, K and V chunks into the ring)
+//   warp 1      MMA issuer (S^T one chunk ahead of the softmax, then O^T += V^T P^T)
+//   warps 2-5   softmax / epilogue; thread = key (softmax) = head dim (O).
+// Online softmax with a lazily refreshed per-column reference max: a chunk
+// whose scores stay within 2^TH of the reference reuses it (no rescale of O,
+// no cross-warp max) — decided by one block vote per chunk.  Every rule is
+// column-local and chunk / split boundaries are absolute key positions, so a
+// row's bits depend only on its own keys: PAD, SPLIT and RAGGED launches,
+// prefill, verify and single-token decode agree bitwise (the property behind
+// greedy speculative == regular decoding).
+// Rows whose history fits one split are written normalised; longer rows leave
+// (m, l, o) per split for attn_combine_kernel.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -30,7 +36,8 @@
 namespace bass {
 namespace ast {
 
-constexpr int DH = 128, CH = 128, SPLIT_CH = 8, SPLIT = CH * SPLIT_CH, THREADS = 256;
+constexpr int DH = 128, CH = 128, SPLIT_CH = 8, SPLIT = CH * SPLIT_CH, THREADS = 192;
+constexpr float TH = 8.f;   // reuse the reference max while scores stay below it + TH (log2 units)
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -58,10 +65,12 @@ __device__ __forceinline__ void tma_2d(const CUtensorMap* map, uint32_t dst, uin
         "l"(map), "r"(bar), "r"(c0), "r"(c1)
         : "memory");
 }
+// shared-memory matrix descriptor, 128-byte swizzle, version 1
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
     return (uint64_t)((addr & 0x3FFFF) >> 4) | ((uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16) |
            ((uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
+// kind::f16, bf16 x bf16 -> f32, M = 128, N = n, B K-major; a_mn: A is MN-major
 __host__ __device__ constexpr uint32_t idesc(int n, int a_mn) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)(n >> 3) << 17) |
            ((uint32_t)(128 >> 4) << 24);
@@ -77,17 +86,18 @@ __device__ __forceinline__ void commit(uint32_t bar) {
 }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void ld16(uint32_t taddr, float* v) {
+// 16 consecutive fp32 columns of this thread's TMEM lane (no wait)
+__device__ __forceinline__ void ld16_nowait(uint32_t taddr, float* v) {
     uint32_t r[16];
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void st16(uint32_t taddr, const float* v) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
@@ -99,9 +109,68 @@ __device__ __forceinline__ void st16(uint32_t taddr, const float* v) {
         "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
         "r"(__float_as_uint(v[15]))
         : "memory");
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// named barrier 1 over the four softmax warps
+__device__ __forceinline__ void sm_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ bool sm_vote_any(bool p) {
+    uint32_t r;
+    asm volatile(
+        "{\n .reg .pred a, b;\n setp.ne.u32 a, %1, 0;\n bar.red.or.pred b, 1, 128, a;\n selp.u32 %0, 1, 0, b;\n}"
+        : "=r"(r)
+        : "r"((uint32_t)p)
+        : "memory");
+    return r != 0;
+}
+__device__ __forceinline__ float fast_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Column reduction over the 128 softmax threads (fixed order => deterministic).
+// v[NQ] per thread -> fin[NQ] in shared memory (every thread then reads it).
+// Intra-warp: transpose-reduce (lane L ends holding columns L*NQ/32 + i);
+// then the four warps' partials are combined in warp order by NQ threads.
+template <int NQ, bool MAX>
+__device__ __forceinline__ void col_reduce(float (&v)[NQ], float* red, float* fin, int wq, int lane, int tid) {
+    float w[NQ];
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) w[i] = v[i];
+    int n = NQ;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const bool up = (lane & o) != 0;
+        if (n >= 2) {
+            const int half = n >> 1;
+#pragma unroll
+            for (int i = 0; i < NQ / 2; ++i) {
+                if (i < half) {
+                    const float send = up ? w[i] : w[i + half];
+                    const float keep = up ? w[i + half] : w[i];
+                    const float r = __shfl_xor_sync(0xffffffffu, send, o);
+                    w[i] = MAX ? fmaxf(keep, r) : keep + r;
+                }
+            }
+            n = half;
+        } else {
+            const float r = __shfl_xor_sync(0xffffffffu, w[0], o);
+            w[0] = MAX ? fmaxf(w[0], r) : w[0] + r;
+        }
+    }
+    constexpr int PER = NQ >= 32 ? NQ / 32 : 1;
+    constexpr int REP = NQ >= 32 ? 1 : 32 / NQ;
+    if (lane % REP == 0) {
+#pragma unroll
+        for (int i = 0; i < PER; ++i) red[wq * NQ + (lane * NQ) / 32 + i] = w[i];
+    }
+    sm_bar();
+    if (tid < NQ) {
+        const float a = red[tid], b = red[NQ + tid], c = red[2 * NQ + tid], d = red[3 * NQ + tid];
+        fin[tid] = MAX ? fmaxf(fmaxf(a, b), fmaxf(c, d)) : (a + b) + (c + d);
+    }
+    sm_bar();
+}
 
 struct Work {
     int32_t seq, t0, split, nch;   // nch: 128-key chunks of this split the tile's last row sees
@@ -109,57 +178,67 @@ struct Work {
 
 template <int NQ>
 struct Cfg {
-    static constexpr int STAGES = 2;
-    static constexpr int KV_TILE = CH * 128;     // one 64-wide swizzle sub-tile (bytes)
-    static constexpr int STAGE = 4 * KV_TILE;    // K0 K1 V0 V1
-    static constexpr int R_TILE = 128 * 128;     // 128 rows x 64 bf16: one sub-tile of Q or P
-    static constexpr int OFF_Q = STAGES * STAGE, OFF_P = OFF_Q + 2 * R_TILE;
-    static constexpr int OFF_BAR = OFF_P + 2 * R_TILE;
-    static constexpr int NBAR = 2 * STAGES + 1 + 2 + 1 + 1;   // kv_full, kv_empty, q_full, s_full[2], p_full, o_done
+    static constexpr int STAGES = NQ >= 64 ? 2 : 3;
+    static constexpr int KV_TILE = CH * 128;      // 128 rows x 64 bf16 (one 128B-swizzle sub-tile)
+    static constexpr int STAGE = 4 * KV_TILE;     // K0 K1 V0 V1
+    static constexpr int R_TILE = NQ * 128;       // NQ rows x 64 bf16: one sub-tile of Q or P
+    static constexpr int OFF_Q = STAGES * STAGE;  // 2 buffers x 2 sub-tiles
+    static constexpr int OFF_P = OFF_Q + 4 * R_TILE;
+    static constexpr int OFF_RED = OFF_P + 4 * R_TILE;   // red[4][NQ], fin[NQ], mref[NQ], alph[NQ]
+    static constexpr int OFF_BAR = OFF_RED + 7 * NQ * 4;
+    // q_full[2] q_empty[2] k_full[S] v_full[S] kv_empty[S] s_full[2] s_free[2] p_full[2] p_free[2] o_full[2] o_free[2]
+    static constexpr int NBAR = 16 + 3 * STAGES;
     static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
-    static constexpr int TMEM_COLS = 512;        // S0 [0,128) S1 [128,256) O [256,384)
+    static constexpr int TMEM_COLS = 4 * NQ < 32 ? 32 : 4 * NQ;   // S0 S1 O0 O1
 };
 
-// Query rows on TMEM lanes: S = Q . K^T (M = 128 query rows, N = 128 keys),
-// so each softmax thread owns one row and the max / sum over keys are
-// register-local; O = P . V (A = P from smem, B = V read MN-major).
 template <int NQ>
 __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
     const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
-    const __grid_constant__ CUtensorMap tv, Seqs seqs, const Work* __restrict__ work, int H, int cap, int pad_len,
+    const __grid_constant__ CUtensorMap tv, Seqs seqs, const Work* __restrict__ work, int n_items, int H, int cap,
     float* __restrict__ part_o, float* __restrict__ part_ml, int max_splits, __nv_bfloat16* __restrict__ out) {
     using Cf = Cfg<NQ>;
     constexpr int ST = Cf::STAGES;
     extern __shared__ uint8_t smem_raw[];
     pdl_trigger();
-    const Work wk = work[blockIdx.x];
-    const int h = blockIdx.y;
-    const int slot = seqs.slot[wk.seq], qn = seqs.qn[wk.seq], off = seqs.off[wk.seq], q0row = seqs.q0[wk.seq];
-    const int L = off + qn;
-    const int s0 = wk.split * SPLIT;
-    if (wk.t0 >= qn || wk.nch <= 0) return;   // idle CTA (uniform)
-    const int nch = wk.nch;
-    const int rows_valid = min(128, qn - wk.t0);
 
     const uint32_t raw = su32(smem_raw);
     const uint32_t base = (raw + 1023) & ~1023u;
     uint8_t* sm = smem_raw + (base - raw);
+    float* red = reinterpret_cast<float*>(sm + Cf::OFF_RED);
+    float* fin = red + 4 * NQ;
+    float* mref = fin + NQ;   // per-column reference max (log2 units), shared
+    float* alph = mref + NQ;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Cf::OFF_BAR);
-    uint64_t* kv_full = bars;
-    uint64_t* kv_empty = bars + ST;
-    uint64_t* q_full = bars + 2 * ST;
-    uint64_t* s_full = bars + 2 * ST + 1;   // [2]
-    uint64_t* p_full = bars + 2 * ST + 3;
-    uint64_t* o_done = bars + 2 * ST + 4;
+    uint64_t* q_full = bars;
+    uint64_t* q_empty = bars + 2;
+    uint64_t* k_full = bars + 4;
+    uint64_t* v_full = k_full + ST;
+    uint64_t* kv_empty = v_full + ST;
+    uint64_t* s_full = kv_empty + ST;
+    uint64_t* s_free = s_full + 2;
+    uint64_t* p_full = s_free + 2;
+    uint64_t* p_free = p_full + 2;
+    uint64_t* o_full = p_free + 2;
+    uint64_t* o_free = o_full + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cf::NBAR);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < Cf::NBAR; ++i) mbar_init(su32(&bars[i]), 1);
+        // software arrivals: one per softmax warp
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(su32(&s_free[i]), 4);
+            mbar_init(su32(&p_full[i]), 4);
+            mbar_init(su32(&o_free[i]), 4);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tk) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tv) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tq) : "memory");
     }
-    if (warp == 2) {
+    if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
                      "r"(Cf::TMEM_COLS)
                      : "memory");
@@ -169,192 +248,226 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
     __syncthreads();
     fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tO = tmem + 256;
-    const int kv_row0 = (slot * H + h) * cap + s0;
+    // Q and this layer's K/V rows come from the QKV GEMM; the output buffer
+    // is read by earlier kernels of the stream
+    pdl_wait();
+
+    // items of this CTA: it = blockIdx.x + k * gridDim.x; idle items (no row
+    // of the tile sees the split) are skipped identically by every role
+    auto item_info = [&](int it, Work& wk, int& h) -> bool {
+        wk = work[it / H];
+        h = it % H;
+        return wk.nch > 0 && wk.t0 < seqs.qn[wk.seq];
+    };
 
     if (warp == 0) {
-        if (lane == 0) {   // ---- producer
-            asm volatile("griddepcontrol.wait;" ::: "memory");   // Q and this step's K/V rows come from the QKV GEMM
-            mbar_expect_tx(su32(q_full), 2 * Cf::R_TILE);
-            for (int s = 0; s < 2; ++s)
-                tma_2d(&tq, base + Cf::OFF_Q + s * Cf::R_TILE, su32(q_full), h * DH + s * 64, q0row + wk.t0);
-            for (int c = 0; c < nch; ++c) {
-                const int s = c % ST;
-                if (c >= ST) mbar_wait(su32(&kv_empty[s]), ((c / ST) - 1) & 1);
-                const uint32_t b = su32(&kv_full[s]), st = base + s * Cf::STAGE;
-                mbar_expect_tx(b, Cf::STAGE);
-                for (int sub = 0; sub < 2; ++sub) {
-                    tma_2d(&tk, st + sub * Cf::KV_TILE, b, sub * 64, kv_row0 + c * CH);
-                    tma_2d(&tv, st + (2 + sub) * Cf::KV_TILE, b, sub * 64, kv_row0 + c * CH);
+        if (lane == 0) {   // ---------------- TMA producer
+            int g = 0, n = 0;
+            for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+                Work wk;
+                int h;
+                if (!item_info(it, wk, h)) continue;
+                const int slot = seqs.slot[wk.seq], q0row = seqs.q0[wk.seq];
+                const int qb = n & 1;
+                if (n >= 2) mbar_wait(su32(&q_empty[qb]), ((n >> 1) - 1) & 1);
+                mbar_expect_tx(su32(&q_full[qb]), 2 * Cf::R_TILE);
+                for (int s = 0; s < 2; ++s)
+                    tma_2d(&tq, base + Cf::OFF_Q + (2 * qb + s) * Cf::R_TILE, su32(&q_full[qb]), h * DH + s * 64,
+                           q0row + wk.t0);
+                const int kv_row0 = (slot * H + h) * cap + wk.split * SPLIT;
+                for (int c = 0; c < wk.nch; ++c, ++g) {
+                    const int st = g % ST;
+                    if (g >= ST) mbar_wait(su32(&kv_empty[st]), ((g / ST) - 1) & 1);
+                    const uint32_t sb = base + st * Cf::STAGE;
+                    mbar_expect_tx(su32(&k_full[st]), 2 * Cf::KV_TILE);
+                    for (int s = 0; s < 2; ++s) tma_2d(&tk, sb + s * Cf::KV_TILE, su32(&k_full[st]), s * 64, kv_row0 + c * CH);
+                    mbar_expect_tx(su32(&v_full[st]), 2 * Cf::KV_TILE);
+                    for (int s = 0; s < 2; ++s)
+                        tma_2d(&tv, sb + (2 + s) * Cf::KV_TILE, su32(&v_full[st]), s * 64, kv_row0 + c * CH);
                 }
+                ++n;
             }
         }
         __syncwarp();
     } else if (warp == 1) {
-        if (lane == 0) {   // ---- MMA issuer
-            constexpr uint32_t ID1 = idesc(128, 0);                      // S = Q . K^T
-            constexpr uint32_t ID2 = idesc(128, 0) | (1u << 16);          // O = P . V  (B = V, MN-major)
-            auto mma1 = [&](int c) {
-                const uint32_t st = base + (c % ST) * Cf::STAGE;
-#pragma unroll
-                for (int kk = 0; kk < DH / 16; ++kk) {
-                    const uint32_t sub = kk >> 2, in = (kk & 3) * 32;
-                    umma(tmem + (c & 1) * 128, sdesc(base + Cf::OFF_Q + sub * Cf::R_TILE + in, 16, 1024),
-                         sdesc(st + sub * Cf::KV_TILE + in, 16, 1024), ID1, kk > 0);
-                }
-                commit(su32(&s_full[c & 1]));
-            };
-            mbar_wait(su32(q_full), 0);
-            mbar_wait(su32(&kv_full[0]), 0);
-            fence_after();
-            mma1(0);
-            for (int c = 0; c < nch; ++c) {
-                if (c + 1 < nch) {
-                    mbar_wait(su32(&kv_full[(c + 1) % ST]), ((c + 1) / ST) & 1);
-                    fence_after();
-                    mma1(c + 1);
-                }
-                mbar_wait(su32(p_full), c & 1);
+        if (lane == 0) {   // ---------------- MMA issuer
+            constexpr uint32_t ID1 = idesc(NQ, 0);   // S^T = K . Q^T   (A = K, K-major)
+            constexpr uint32_t ID2 = idesc(NQ, 1);   // O^T = V^T . P^T (A = V, MN-major)
+            struct Pend {
+                int g, st, ob, first, last;
+            } pend{-1, 0, 0, 0, 0};
+            auto pv = [&](const Pend& p) {
+                const int sb = p.g & 1;
+                mbar_wait(su32(&p_full[sb]), (p.g >> 1) & 1);
+                mbar_wait(su32(&v_full[p.st]), (p.g / ST) & 1);
                 fence_after();
-                const uint32_t st = base + (c % ST) * Cf::STAGE;
+                const uint32_t vs = base + p.st * Cf::STAGE + 2 * Cf::KV_TILE;
+                const uint32_t ps = base + Cf::OFF_P + 2 * sb * Cf::R_TILE;
+                const uint32_t d = tmem + 2 * NQ + p.ob * NQ;
 #pragma unroll
                 for (int kk = 0; kk < CH / 16; ++kk) {
                     const uint32_t sub = kk >> 2, in = (kk & 3) * 32;
-                    umma(tO, sdesc(base + Cf::OFF_P + sub * Cf::R_TILE + in, 16, 1024),
-                         sdesc(st + 2 * Cf::KV_TILE + kk * 2048, Cf::KV_TILE, 1024), ID2, (c > 0 || kk > 0) ? 1u : 0u);
+                    umma(d, sdesc(vs + kk * 2048, Cf::KV_TILE, 1024), sdesc(ps + sub * Cf::R_TILE + in, 16, 1024), ID2,
+                         (p.first && kk == 0) ? 0u : 1u);
                 }
-                commit(su32(o_done));
-                commit(su32(&kv_empty[c % ST]));
+                commit(su32(&kv_empty[p.st]));
+                commit(su32(&p_free[sb]));
+                if (p.last) commit(su32(&o_full[p.ob]));
+            };
+            int g = 0, n = 0;
+            for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+                Work wk;
+                int h;
+                if (!item_info(it, wk, h)) continue;
+                const int qb = n & 1, ob = n & 1;
+                mbar_wait(su32(&q_full[qb]), (n >> 1) & 1);
+                for (int c = 0; c < wk.nch; ++c, ++g) {
+                    const int st = g % ST, sb = g & 1;
+                    mbar_wait(su32(&k_full[st]), (g / ST) & 1);
+                    if (g >= 2) mbar_wait(su32(&s_free[sb]), ((g >> 1) - 1) & 1);
+                    fence_after();
+                    const uint32_t ks = base + st * Cf::STAGE;
+                    const uint32_t qs = base + Cf::OFF_Q + 2 * qb * Cf::R_TILE;
+#pragma unroll
+                    for (int kk = 0; kk < DH / 16; ++kk) {
+                        const uint32_t sub = kk >> 2, in = (kk & 3) * 32;
+                        umma(tmem + sb * NQ, sdesc(ks + sub * Cf::KV_TILE + in, 16, 1024),
+                             sdesc(qs + sub * Cf::R_TILE + in, 16, 1024), ID1, kk > 0);
+                    }
+                    commit(su32(&s_full[sb]));
+                    if (c == wk.nch - 1) commit(su32(&q_empty[qb]));
+                    // O^T += V^T P^T of the previous chunk while the softmax works on this one
+                    if (pend.g >= 0) pv(pend);
+                    if (c == 0 && n >= 2) mbar_wait(su32(&o_free[ob]), ((n >> 1) - 1) & 1);
+                    pend = Pend{g, st, ob, c == 0, c == wk.nch - 1};
+                }
+                ++n;
             }
+            if (pend.g >= 0) pv(pend);
         }
         __syncwarp();
-    } else if (warp >= 4) {
-        // ---- softmax / correction / epilogue: thread r owns query row t0 + r (TMEM lane r)
-        const int r = threadIdx.x - 128, t = wk.t0 + r;
-        const bool warp_live = (warp - 4) * 32 < rows_valid;   // warp-uniform
-        const bool live = r < rows_valid;
-        const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
-        const float scale = sqrtf((float)DH);
-        uint8_t* Prow = sm + Cf::OFF_P + r * 128;
-        float m_run = -INFINITY, l_run = 0.f;
-        for (int c = 0; c < nch; ++c) {
-            const int kbase = s0 + c * CH;
-            const uint32_t tS = tmem + lane_off + (c & 1) * 128;
-            mbar_wait(su32(&s_full[c & 1]), (c >> 1) & 1);
-            fence_after();
-            float mn = m_run, alpha = 1.f;
-            if (warp_live) {
-                float mc = -INFINITY;
-#pragma unroll 1
-                for (int j0 = 0; j0 < 128; j0 += 16) {
-                    float v[16];
-                    ld16(tS + j0, v);
+    } else {
+        // ---------------- softmax / epilogue (warps 2-5)
+        const int wq = warp & 3;                 // TMEM lane quarter this warp may access
+        const int key = wq * 32 + lane;          // key within the chunk (S^T lane) = head dim (O^T lane)
+        const int tid = threadIdx.x - 64;        // 0..127
+        const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+        const float C = 1.4426950408889634f / sqrtf((float)DH);   // log2(e) / sqrt(dh)
+        const int psub = key >> 6, pin = key & 63;
+        int g = 0, n = 0;
+        for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+            Work wk;
+            int h;
+            if (!item_info(it, wk, h)) continue;
+            const int qn = seqs.qn[wk.seq], off = seqs.off[wk.seq], q0row = seqs.q0[wk.seq];
+            const int L = off + qn, s0 = wk.split * SPLIT, ob = n & 1;
+            float l_t[NQ];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int kp = kbase + j0 + j;
-                        if (live && kp <= off + t && kp < L) mc = fmaxf(mc, v[j] / scale);
-                    }
-                }
-                mn = fmaxf(m_run, mc);
-                alpha = mn == -INFINITY ? 1.f : expf(m_run - mn);   // m_run = -inf -> 0
-            }
-            if (c > 0) {   // previous PV landed: P buffer free, O may be rescaled
-                mbar_wait(su32(o_done), (c - 1) & 1);
+            for (int j = 0; j < NQ; ++j) l_t[j] = 0.f;
+            for (int c = 0; c < wk.nch; ++c, ++g) {
+                const int sb = g & 1;
+                const bool first = c == 0;
+                mbar_wait(su32(&s_full[sb]), (g >> 1) & 1);
                 fence_after();
-                if (warp_live && __any_sync(0xffffffffu, alpha != 1.f)) {
-#pragma unroll 1
-                    for (int j0 = 0; j0 < 128; j0 += 16) {
-                        float v[16];
-                        ld16(tO + lane_off + j0, v);
+                float x[NQ];
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) v[j] *= alpha;
-                        st16(tO + lane_off + j0, v);
-                    }
+                for (int j0 = 0; j0 < NQ; j0 += 16) ld16_nowait(tmem + lane_off + sb * NQ + j0, x + j0);
+                ld_wait();
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(su32(&s_free[sb]));
+                const int kp = s0 + c * CH + key;
+                bool over = false;
+#pragma unroll
+                for (int j = 0; j < NQ; ++j) {
+                    const int t = wk.t0 + j;
+                    x[j] = (t < qn && kp <= off + t && kp < L) ? x[j] * C : -INFINITY;
+                    over |= first ? x[j] != -INFINITY : x[j] > mref[j] + TH;
                 }
-            }
-            float ls = 0.f;
-            if (warp_live) {
-#pragma unroll 1
-                for (int j0 = 0; j0 < 128; j0 += 16) {
-                    float v[16];
-                    ld16(tS + j0, v);
-                    uint32_t pk[8];
-#pragma unroll
-                    for (int j = 0; j < 16; j += 2) {
-                        float p2[2];
-#pragma unroll
-                        for (int u = 0; u < 2; ++u) {
-                            const int kp = kbase + j0 + j + u;
-                            const bool ok = live && kp <= off + t && kp < L && mn != -INFINITY;
-                            p2[u] = ok ? expf(v[j + u] / scale - mn) : 0.f;
-                            ls += p2[u];
+                if (sm_vote_any(over)) {
+                    // some column's scores left the reference window: exact chunk
+                    // max; the reference moves only where that column overflowed
+                    col_reduce<NQ, true>(x, red, fin, wq, lane, tid);
+                    bool resc = false;
+                    if (tid < NQ) {
+                        const float cm = fin[tid], mo = first ? -INFINITY : mref[tid];
+                        float a = 1.f;
+                        if (cm > mo + TH) {
+                            a = mo == -INFINITY ? 0.f : fast_exp2(mo - cm);
+                            resc = mo != -INFINITY;
+                            mref[tid] = cm;
                         }
-                        __nv_bfloat162 b2 = __floats2bfloat162_rn(p2[0], p2[1]);
-                        pk[j >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+                        alph[tid] = a;
                     }
-                    // keys j0..j0+15 = two 16-byte chunks of the 128B-swizzled row
-                    const int kb = j0 >> 6, ch = (j0 & 63) >> 3;
-                    uint8_t* rowp = Prow + kb * Cf::R_TILE;
+                    const bool any_rescale = sm_vote_any(resc);   // also publishes mref / alph
 #pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const uint32_t pc = (uint32_t)(ch + u) ^ (uint32_t)(r & 7);
-                        *reinterpret_cast<uint4*>(rowp + pc * 16) =
-                            make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+                    for (int j = 0; j < NQ; ++j) l_t[j] *= alph[j];
+                    if (any_rescale) {
+                        // O^T holds chunks < c: wait for the previous PV, rescale its columns
+                        mbar_wait(su32(&p_free[(g - 1) & 1]), ((g - 1) >> 1) & 1);
+                        fence_after();
+                        const uint32_t to = tmem + lane_off + 2 * NQ + ob * NQ;
+#pragma unroll
+                        for (int j0 = 0; j0 < NQ; j0 += 16) {
+                            float o[16];
+                            ld16_nowait(to + j0, o);
+                            ld_wait();
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) o[j] *= alph[j0 + j];
+                            st16(to + j0, o);
+                        }
+                        st_wait();
+                        fence_before();
                     }
                 }
-            } else {
-                // rows of an idle warp still hand the tensor core zeros
+                // P (bf16) for this chunk; the previous user of the buffer (PV g-2) must be done
+                if (g >= 2) mbar_wait(su32(&p_free[sb]), ((g >> 1) - 1) & 1);
+                uint8_t* P = sm + Cf::OFF_P + 2 * sb * Cf::R_TILE + psub * Cf::R_TILE;
 #pragma unroll
-                for (int kb = 0; kb < 2; ++kb)
-#pragma unroll
-                    for (int ch = 0; ch < 8; ++ch)
-                        *reinterpret_cast<uint4*>(Prow + kb * Cf::R_TILE + ch * 16) = make_uint4(0, 0, 0, 0);
+                for (int j = 0; j < NQ; ++j) {
+                    const float p = x[j] == -INFINITY ? 0.f : fast_exp2(x[j] - mref[j]);
+                    l_t[j] += p;
+                    const uint32_t chunk = (uint32_t)(pin >> 3) ^ (uint32_t)(j & 7);
+                    *(reinterpret_cast<__nv_bfloat16*>(P + j * 128 + chunk * 16) + (pin & 7)) = __float2bfloat16_rn(p);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // P -> tensor core
+                __syncwarp();
+                if (lane == 0) mbar_arrive(su32(&p_full[sb]));
             }
-            l_run = l_run * alpha + ls;
-            m_run = mn;
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // P -> tensor core
+            // ---- epilogue: l per column (fixed-order block sum), O^T lane = head dim
+            col_reduce<NQ, false>(l_t, red, fin, wq, lane, tid);
+            mbar_wait(su32(&o_full[ob]), (n >> 1) & 1);
+            fence_after();
+            float o[NQ];
+#pragma unroll
+            for (int j0 = 0; j0 < NQ; j0 += 16) ld16_nowait(tmem + lane_off + 2 * NQ + ob * NQ + j0, o + j0);
+            ld_wait();
             fence_before();
-            softmax_bar();
-            if (r == 0) mbar_arrive(su32(p_full));
-        }
-        // ---- epilogue: row t, 128 head dims
-        mbar_wait(su32(o_done), (nch - 1) & 1);
-        fence_after();
-        if (warp_live) {
-            const bool sees = live && off + t >= s0;
-            const int row = q0row + t;
-            const bool direct = off + t < SPLIT;   // whole history in split 0
-            const int64_t idx = ((int64_t)row * H + h) * max_splits + wk.split;
-#pragma unroll 1
-            for (int j0 = 0; j0 < 128; j0 += 16) {
-                float v[16];
-                ld16(tO + lane_off + j0, v);
-                if (!sees) continue;
-                if (direct) {
-                    uint32_t pk[8];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(su32(&o_free[ob]));
 #pragma unroll
-                    for (int j = 0; j < 16; j += 2) {
-                        __nv_bfloat162 b2 = __floats2bfloat162_rn(v[j] / l_run, v[j + 1] / l_run);
-                        pk[j >> 1] = *reinterpret_cast<uint32_t*>(&b2);
-                    }
-                    uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)row * H + h) * DH + j0);
-                    dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                    dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            for (int j = 0; j < NQ; ++j) {
+                const int t = wk.t0 + j;
+                if (t >= qn || off + t < s0) continue;   // padded row / row does not see this split
+                const int row = q0row + t;
+                const float l = fin[j];
+                if (off + t < SPLIT) {   // whole history in split 0: normalised output
+                    out[((int64_t)row * H + h) * DH + key] = __float2bfloat16_rn(o[j] / l);
                 } else {
-                    float4* dst = reinterpret_cast<float4*>(part_o + idx * DH + j0);
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) dst[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+                    const int64_t idx = ((int64_t)row * H + h) * max_splits + wk.split;
+                    part_o[idx * DH + key] = o[j];
+                    if (key == 0) {
+                        part_ml[idx * 2] = mref[j] * 0.6931471805599453f;   // natural-log units for the combine
+                        part_ml[idx * 2 + 1] = l;
+                    }
                 }
             }
-            if (sees && !direct) {
-                part_ml[idx * 2] = m_run;
-                part_ml[idx * 2 + 1] = l_run;
-            }
+            ++n;
         }
     }
     fence_before();
     __syncthreads();
-    if (warp == 2)
+    if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cf::TMEM_COLS)
                      : "memory");
 }
@@ -401,8 +514,10 @@ static void launch(bass_ctx* ctx, const AttnPlan& p, const CUtensorMap& tk, cons
         BASS_CUDA(cudaFuncSetAttribute(attn_stream_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
         attr = true;
     }
-    BASS_CUDA(launch_pdl(attn_stream_kernel<NQ>, dim3(nw, p.H), dim3(THREADS), (size_t)Cf::SMEM, ctx->stream, p.tq,
-                         tk, tv, seqs, wp, p.H, p.cap, p.pad_len, po, pml, p.mc, out));
+    const int n_items = nw * p.H;
+    const int grid = std::max(1, std::min(n_items, ctx->sm_count));
+    BASS_CUDA(launch_pdl(attn_stream_kernel<NQ>, dim3(grid), dim3(THREADS), (size_t)Cf::SMEM, ctx->stream, p.tq, tk,
+                         tv, seqs, wp, n_items, p.H, p.cap, po, pml, p.mc, out));
 }
 
 }  // namespace ast
@@ -410,7 +525,7 @@ static void launch(bass_ctx* ctx, const AttnPlan& p, const CUtensorMap& tk, cons
 int stream_split_len() { return ast::SPLIT; }
 
 // Plan: work items (seq, q tile, split, chunks seen) — RAGGED/SPLIT exact,
-// PAD over the padded [max q] x [max L] grid (padded keys computed, masked).
+// PAD over the padded [max q] x [max L] grid (padded keys streamed, masked).
 void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, int n_slots,
                            const std::vector<int32_t>& qn, const std::vector<int32_t>& off, int H, int cap,
                            DevBuf& work_buf, AttnPlan& plan) {
@@ -421,7 +536,8 @@ void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, in
         max_qn = std::max(max_qn, qn[i]);
         max_L = std::max(max_L, off[i] + qn[i]);
     }
-    const int NQ = 128;   // query-row tile (TMEM lanes)
+    // query tile: smallest of 16 / 32 / 64 columns covering the longest block
+    const int NQ = max_qn <= 16 ? 16 : max_qn <= 32 ? 32 : 64;
     std::vector<int32_t> w;
     std::vector<int> first(n_seq + 1, 0);
     bool multi = false;
@@ -476,8 +592,7 @@ void stream_attention_run(bass_ctx* ctx, const AttnPlan& p, const void* kc, cons
         switch (p.NQ) {
             case 16: launch<16>(ctx, p, tk, tv, seqs_dev, wp, nw, part_o, part_ml, o); break;
             case 32: launch<32>(ctx, p, tk, tv, seqs_dev, wp, nw, part_o, part_ml, o); break;
-            case 64: launch<64>(ctx, p, tk, tv, seqs_dev, wp, nw, part_o, part_ml, o); break;
-            default: launch<128>(ctx, p, tk, tv, seqs_dev, wp, nw, part_o, part_ml, o); break;
+            default: launch<64>(ctx, p, tk, tv, seqs_dev, wp, nw, part_o, part_ml, o); break;
         }
         ctx->launches++;
         cudaError_t e = cudaGetLastError();

@@ -224,12 +224,11 @@ void gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, i
 #undef BASS_GEMM_CASE
 }
 
-// BASS_ATTN_MODE=stream selects the streaming kernel (attn_stream.cu); the
-// default is the chunk kernel (attn_tc.cu) until the streaming one beats it
-// (profiles/r1_attn_sweep_*.jsonl: stream 0.35-0.45 TB/s vs chunk 0.8-2.4 TB/s)
+// Default: the persistent streaming kernel (attn_stream.cu);
+// BASS_ATTN_MODE=chunk selects the earlier one-CTA-per-tile kernel (attn_tc.cu)
 static bool attn_stream_mode() {
-    static const bool stream = getenv("BASS_ATTN_MODE") && std::string(getenv("BASS_ATTN_MODE")) == "stream";
-    return stream;
+    static const bool chunk = getenv("BASS_ATTN_MODE") && std::string(getenv("BASS_ATTN_MODE")) == "chunk";
+    return !chunk;
 }
 
 template <typename TA, int DH>
@@ -872,6 +871,60 @@ int bass_attention(bass_ctx* c, int strategy, int dtype, int n_seq, int n_head, 
         launch_attention(c, dtype, d_head, strategy, q, k, v, seqs, qn, off, dm + 4 * n_seq, M, n_head, kv_stride,
                          n_seq, work, po, pml, out);
         c->sync();
+    });
+}
+
+int bass_attention_bench(bass_ctx* c, int strategy, int n_seq, int n_head, const int32_t* cu_q, const int32_t* offsets,
+                         const void* q, const void* k, const void* v, int kv_stride, int n_kv, void* out, int reps,
+                         double* ms_per_call) {
+    return guarded(c, [&] {
+        BASS_REQUIRE(n_seq >= 1 && reps >= 1 && n_kv >= 1, "attention bench: bad sizes");
+        std::vector<int32_t> slot(n_seq), q0(n_seq), qn(n_seq), off(n_seq), row_pos;
+        for (int i = 0; i < n_seq; ++i) {
+            slot[i] = i;
+            q0[i] = cu_q[i];
+            qn[i] = cu_q[i + 1] - cu_q[i];
+            off[i] = offsets[i];
+            BASS_REQUIRE(qn[i] >= 1 && off[i] >= 0 && off[i] + qn[i] <= kv_stride, "attention bench: bad lengths");
+            for (int t = 0; t < qn[i]; ++t) row_pos.push_back(off[i] + t);
+        }
+        const int M = cu_q[n_seq], H = n_head;
+        static DevBuf meta, work, po, pml;
+        int32_t* dm = (int32_t*)meta.need((4 * (size_t)n_seq + M) * 4, c->stream);
+        std::vector<int32_t> hm;
+        for (auto* v_ : {&slot, &q0, &qn, &off}) hm.insert(hm.end(), v_->begin(), v_->end());
+        hm.insert(hm.end(), row_pos.begin(), row_pos.end());
+        upload_i32(c, dm, hm.data(), hm.size());
+        Seqs seqs{dm, dm + n_seq, dm + 2 * n_seq, dm + 3 * n_seq};
+        AttnPlan plan;
+        stream_attention_plan(c, strategy, q, M, n_seq, qn, off, H, kv_stride, work, plan);
+        float* so = (float*)po.need((size_t)M * H * plan.mc * 128 * 4, c->stream);
+        float* sml = (float*)pml.need((size_t)M * H * plan.mc * 2 * 4, c->stream);
+        const size_t kv_bytes = (size_t)n_seq * H * kv_stride * 128 * 2;
+        auto call = [&](int i) {
+            const char* kc = (const char*)k + (size_t)(i % n_kv) * kv_bytes;
+            const char* vc = (const char*)v + (size_t)(i % n_kv) * kv_bytes;
+            stream_attention_run(c, plan, kc, vc, seqs, so, sml, out);
+            if (plan.needs_combine) {
+                BASS_CUDA(launch_pdl(attn_combine_kernel<__nv_bfloat16, 128>, dim3(M, H), dim3(128), 0, c->stream,
+                                     (const float*)so, (const float*)sml, (const int32_t*)(dm + 4 * n_seq), H, plan.mc,
+                                     stream_split_len(), (__nv_bfloat16*)out, 1));
+                check_launch(c);
+            }
+        };
+        for (int i = 0; i < n_kv; ++i) call(i);   // warm (tensor maps, first-launch costs)
+        cudaEvent_t a, b;
+        BASS_CUDA(cudaEventCreate(&a));
+        BASS_CUDA(cudaEventCreate(&b));
+        BASS_CUDA(cudaEventRecord(a, c->stream));
+        for (int i = 0; i < reps; ++i) call(i);
+        BASS_CUDA(cudaEventRecord(b, c->stream));
+        c->sync();
+        float ms = 0.f;
+        BASS_CUDA(cudaEventElapsedTime(&ms, a, b));
+        *ms_per_call = ms / reps;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
     });
 }
 
