@@ -184,8 +184,9 @@ struct Cfg {
     static constexpr int R_TILE = NQ * 128;       // NQ rows x 64 bf16: one sub-tile of Q or P
     static constexpr int OFF_Q = STAGES * STAGE;  // 2 buffers x 2 sub-tiles
     static constexpr int OFF_P = OFF_Q + 4 * R_TILE;
-    static constexpr int OFF_RED = OFF_P + 4 * R_TILE;   // red[4][NQ], fin[NQ], mref[NQ], alph[NQ]
-    static constexpr int OFF_BAR = OFF_RED + 7 * NQ * 4;
+    static constexpr int P_BUF = CH * NQ * 2;     // P^T [128 keys][NQ] bf16, MN-major (queries contiguous)
+    static constexpr int OFF_RED = OFF_P + 2 * P_BUF;    // red[4][NQ], fin, mref, thr, alph [NQ]
+    static constexpr int OFF_BAR = OFF_RED + 8 * NQ * 4;
     // q_full[2] q_empty[2] k_full[S] v_full[S] kv_empty[S] s_full[2] s_free[2] p_full[2] p_free[2] o_full[2] o_free[2]
     static constexpr int NBAR = 16 + 3 * STAGES;
     static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
@@ -208,7 +209,8 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
     float* red = reinterpret_cast<float*>(sm + Cf::OFF_RED);
     float* fin = red + 4 * NQ;
     float* mref = fin + NQ;   // per-column reference max (log2 units), shared
-    float* alph = mref + NQ;
+    float* thr = mref + NQ;   // raw-score threshold (mref + TH) / C above which a chunk refreshes it
+    float* alph = thr + NQ;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Cf::OFF_BAR);
     uint64_t* q_full = bars;
     uint64_t* q_empty = bars + 2;
@@ -292,7 +294,9 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
     } else if (warp == 1) {
         if (lane == 0) {   // ---------------- MMA issuer
             constexpr uint32_t ID1 = idesc(NQ, 0);   // S^T = K . Q^T   (A = K, K-major)
-            constexpr uint32_t ID2 = idesc(NQ, 1);   // O^T = V^T . P^T (A = V, MN-major)
+            constexpr uint32_t ID2 = idesc(NQ, 1) | (1u << 16);   // O^T = V^T . P^T (A = V, B = P^T: MN-major)
+            // P^T swizzle: one atom spans the NQ queries (32 / 64 / 128 bytes) x 8 keys
+            constexpr uint64_t PLT = NQ == 16 ? 6ull : NQ == 32 ? 4ull : 2ull;
             struct Pend {
                 int g, st, ob, first, last;
             } pend{-1, 0, 0, 0, 0};
@@ -302,13 +306,12 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
                 mbar_wait(su32(&v_full[p.st]), (p.g / ST) & 1);
                 fence_after();
                 const uint32_t vs = base + p.st * Cf::STAGE + 2 * Cf::KV_TILE;
-                const uint32_t ps = base + Cf::OFF_P + 2 * sb * Cf::R_TILE;
+                const uint32_t ps = base + Cf::OFF_P + sb * Cf::P_BUF;
                 const uint32_t d = tmem + 2 * NQ + p.ob * NQ;
 #pragma unroll
                 for (int kk = 0; kk < CH / 16; ++kk) {
-                    const uint32_t sub = kk >> 2, in = (kk & 3) * 32;
-                    umma(d, sdesc(vs + kk * 2048, Cf::KV_TILE, 1024), sdesc(ps + sub * Cf::R_TILE + in, 16, 1024), ID2,
-                         (p.first && kk == 0) ? 0u : 1u);
+                    const uint64_t bdesc = (sdesc(ps + kk * 32 * NQ, Cf::P_BUF, 16 * NQ) & ~(7ull << 61)) | (PLT << 61);
+                    umma(d, sdesc(vs + kk * 2048, Cf::KV_TILE, 1024), bdesc, ID2, (p.first && kk == 0) ? 0u : 1u);
                 }
                 commit(su32(&kv_empty[p.st]));
                 commit(su32(&p_free[sb]));
@@ -353,7 +356,9 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
         const int tid = threadIdx.x - 64;        // 0..127
         const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
         const float C = 1.4426950408889634f / sqrtf((float)DH);   // log2(e) / sqrt(dh)
-        const int psub = key >> 6, pin = key & 63;
+        // P^T row of this key: NQ bf16 (MN-major B operand), 16-byte chunks swizzled
+        const uint32_t prow = (uint32_t)key * (2 * NQ);
+        const uint32_t pswz = NQ == 16 ? ((key >> 2) & 1) : NQ == 32 ? ((key >> 1) & 3) : (key & 7);
         int g = 0, n = 0;
         for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
             Work wk;
@@ -361,6 +366,8 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
             if (!item_info(it, wk, h)) continue;
             const int qn = seqs.qn[wk.seq], off = seqs.off[wk.seq], q0row = seqs.q0[wk.seq];
             const int L = off + qn, s0 = wk.split * SPLIT, ob = n & 1;
+            const int ncol = min(NQ, qn - wk.t0);   // valid query columns of the tile (uniform)
+            const int dlim = off + wk.t0;           // column j sees keys kp <= dlim + j
             float l_t[NQ];
 #pragma unroll
             for (int j = 0; j < NQ; ++j) l_t[j] = 0.f;
@@ -371,37 +378,47 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
                 fence_after();
                 float x[NQ];
 #pragma unroll
-                for (int j0 = 0; j0 < NQ; j0 += 16) ld16_nowait(tmem + lane_off + sb * NQ + j0, x + j0);
+                for (int j0 = 0; j0 < NQ; j0 += 16)
+                    if (j0 < ncol) ld16_nowait(tmem + lane_off + sb * NQ + j0, x + j0);
                 ld_wait();
                 fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(su32(&s_free[sb]));
-                const int kp = s0 + c * CH + key;
-                bool over = false;
+                const int cbase = s0 + c * CH, kp = cbase + key;
+                if (cbase + CH - 1 > dlim) {   // chunk crosses the causal diagonal / the end (uniform)
 #pragma unroll
-                for (int j = 0; j < NQ; ++j) {
-                    const int t = wk.t0 + j;
-                    x[j] = (t < qn && kp <= off + t && kp < L) ? x[j] * C : -INFINITY;
-                    over |= first ? x[j] != -INFINITY : x[j] > mref[j] + TH;
+                    for (int j = 0; j < NQ; ++j)
+                        if (!(kp <= dlim + j && kp < L)) x[j] = -INFINITY;
                 }
-                if (sm_vote_any(over)) {
-                    // some column's scores left the reference window: exact chunk
-                    // max; the reference moves only where that column overflowed
+                bool reduce = first;
+                if (!first) {
+                    bool over = false;
+#pragma unroll
+                    for (int j = 0; j < NQ; ++j)
+                        if (j < ncol) over |= x[j] > thr[j];
+                    reduce = sm_vote_any(over);
+                }
+                if (reduce) {
+                    // exact chunk max; a column's reference moves only when its own
+                    // scores leave the window (first chunk: set unconditionally)
                     col_reduce<NQ, true>(x, red, fin, wq, lane, tid);
                     bool resc = false;
                     if (tid < NQ) {
-                        const float cm = fin[tid], mo = first ? -INFINITY : mref[tid];
+                        const float cm = fin[tid] * C, mo = first ? -INFINITY : mref[tid];
                         float a = 1.f;
-                        if (cm > mo + TH) {
+                        if (first || cm > mo + TH) {
                             a = mo == -INFINITY ? 0.f : fast_exp2(mo - cm);
-                            resc = mo != -INFINITY;
+                            resc = !first;
                             mref[tid] = cm;
+                            thr[tid] = (cm + TH) / C;
                         }
                         alph[tid] = a;
                     }
-                    const bool any_rescale = sm_vote_any(resc);   // also publishes mref / alph
+                    const bool any_rescale = sm_vote_any(resc);   // also publishes mref / thr / alph
+                    if (!first) {
 #pragma unroll
-                    for (int j = 0; j < NQ; ++j) l_t[j] *= alph[j];
+                        for (int j = 0; j < NQ; ++j) l_t[j] *= alph[j];
+                    }
                     if (any_rescale) {
                         // O^T holds chunks < c: wait for the previous PV, rescale its columns
                         mbar_wait(su32(&p_free[(g - 1) & 1]), ((g - 1) >> 1) & 1);
@@ -422,13 +439,26 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
                 }
                 // P (bf16) for this chunk; the previous user of the buffer (PV g-2) must be done
                 if (g >= 2) mbar_wait(su32(&p_free[sb]), ((g >> 1) - 1) & 1);
-                uint8_t* P = sm + Cf::OFF_P + 2 * sb * Cf::R_TILE + psub * Cf::R_TILE;
+                const uint32_t pb = base + Cf::OFF_P + sb * Cf::P_BUF + prow;
 #pragma unroll
-                for (int j = 0; j < NQ; ++j) {
-                    const float p = x[j] == -INFINITY ? 0.f : fast_exp2(x[j] - mref[j]);
-                    l_t[j] += p;
-                    const uint32_t chunk = (uint32_t)(pin >> 3) ^ (uint32_t)(j & 7);
-                    *(reinterpret_cast<__nv_bfloat16*>(P + j * 128 + chunk * 16) + (pin & 7)) = __float2bfloat16_rn(p);
+                for (int j0 = 0; j0 < NQ; j0 += 8) {
+                    if (j0 >= ncol) break;   // columns past the tile's rows: never read back
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int u = 0; u < 8; u += 2) {
+                        const float4 m4 = *reinterpret_cast<const float4*>(mref + j0 + (u & 4));
+                        const float ma = (u & 2) ? m4.z : m4.x, mb = (u & 2) ? m4.w : m4.y;
+                        const float p0 = fast_exp2(fmaf(x[j0 + u], C, -ma));
+                        const float p1 = fast_exp2(fmaf(x[j0 + u + 1], C, -mb));
+                        l_t[j0 + u] += p0;
+                        l_t[j0 + u + 1] += p1;
+                        __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+                        pk[u >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+                    }
+                    const uint32_t dst = pb + ((((uint32_t)j0 >> 3) ^ pswz) << 4);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(pk[0]), "r"(pk[1]),
+                                 "r"(pk[2]), "r"(pk[3])
+                                 : "memory");
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // P -> tensor core
                 __syncwarp();
