@@ -114,7 +114,8 @@ int bass_gemm(bass_model* m, int gemm_mode, int M, int N, int K,
               const void* x_dev, const void* w_dev, float* y_dev);
 /* microbenchmark: `reps` back-to-back launches; launch i uses weight copy
  * i % n_w (w_dev holds n_w contiguous [N, K] copies); device time per launch
- * from CUDA events on the context stream */
+ * from CUDA events on the context stream.  gemm_mode 3: tcgen05 on copies
+ * repacked into the packed tile layout bf16 models use for their weights. */
 int bass_gemm_bench(bass_model* m, int gemm_mode, int M, int N, int K,
                     const void* x_dev, const void* w_dev, float* y_dev,
                     int reps, int n_w, double* ms_per_launch);
@@ -141,6 +142,13 @@ int bass_attention_bench(bass_ctx* ctx, int strategy, int n_seq, int n_head,
                          const void* q_dev, const void* k_dev, const void* v_dev,
                          int kv_stride, int n_kv, void* out_dev, int reps,
                          double* ms_per_call);
+
+/* Timeline trace (diagnostics): with `records` > 0, every CTA of the
+ * GEMM / attention / LayerNorm launches that follow writes one record
+ * {t_start_ns, t_end_ns, smid, tag} (globaltimer) until the buffer is full;
+ * 0 disables.  bass_trace_read copies the records out and rewinds. */
+int bass_trace_enable(bass_ctx* ctx, int64_t records);
+int bass_trace_read(bass_ctx* ctx, uint64_t* host, int64_t max_records, int64_t* n_out);
 
 /* Device RNG parity: uniforms u[2i], u[2i+1] = first two draws of
  * default_rng(SeedSequence((seed, sid[i], role[i], ctr[i]))).random()

@@ -82,6 +82,8 @@ SIGNATURES = {
                                  vp, vp, vp, C.c_int, vp]),
     "bass_attention_bench": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, i32p, i32p, vp, vp, vp, C.c_int,
                                        C.c_int, vp, C.c_int, f64p]),
+    "bass_trace_enable": (C.c_int, [vp, C.c_int64]),
+    "bass_trace_read": (C.c_int, [vp, C.POINTER(C.c_uint64), C.c_int64, C.POINTER(C.c_int64)]),
     "bass_rng_uniforms": (C.c_int, [vp, C.c_int, C.c_uint64, i64p, i32p, i64p, f64p]),
     "bass_shape_sample": (C.c_int, [vp, C.c_int, C.c_int, f32p, C.c_double, C.c_double, f64p,
                                     i32p, f64p]),

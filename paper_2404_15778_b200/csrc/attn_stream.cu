@@ -172,8 +172,33 @@ __device__ __forceinline__ void col_reduce(float (&v)[NQ], float* red, float* fi
     sm_bar();
 }
 
-struct Work {
-    int32_t seq, t0, split, nch;   // nch: 128-key chunks of this split the tile's last row sees
+// One work entry per (sequence, query tile, split), expanded over heads in the
+// kernel; the sequence's metadata is folded in so an item costs one 32-byte load.
+struct alignas(16) Work {
+    int32_t slot, q0row, qn, off;   // KV slot, first Q / out row, rows, committed length
+    int32_t t0, split, nch, pad;    // nch: 128-key chunks of this split the tile's last row sees
+};
+
+// Items of this CTA: blockIdx.x, + gridDim.x, ...; the next item's entry is
+// fetched while the current one is processed (hides the global-load latency).
+struct ItemIter {
+    const Work* work;
+    int n_items, H, it;
+    Work nxt;
+    __device__ __forceinline__ ItemIter(const Work* w, int n, int h) : work(w), n_items(n), H(h), it(blockIdx.x) {
+        if (it < n_items) nxt = work[it / H];
+    }
+    // false when exhausted; idle items (tile beyond the block / no chunk) are skipped
+    __device__ __forceinline__ bool next(Work& wk, int& h) {
+        while (it < n_items) {
+            wk = nxt;
+            h = it % H;
+            it += gridDim.x;
+            if (it < n_items) nxt = work[it / H];
+            if (wk.nch > 0 && wk.t0 < wk.qn) return true;
+        }
+        return false;
+    }
 };
 
 template <int NQ>
@@ -197,7 +222,9 @@ template <int NQ>
 __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
     const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
     const __grid_constant__ CUtensorMap tv, Seqs seqs, const Work* __restrict__ work, int n_items, int H, int cap,
-    float* __restrict__ part_o, float* __restrict__ part_ml, int max_splits, __nv_bfloat16* __restrict__ out) {
+    float* __restrict__ part_o, float* __restrict__ part_ml, int max_splits, __nv_bfloat16* __restrict__ out,
+    TraceArg tr) {
+    const unsigned long long t_start = tr.buf ? gtimer() : 0ull;
     using Cf = Cfg<NQ>;
     constexpr int ST = Cf::STAGES;
     extern __shared__ uint8_t smem_raw[];
@@ -254,22 +281,16 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
     // is read by earlier kernels of the stream
     pdl_wait();
 
-    // items of this CTA: it = blockIdx.x + k * gridDim.x; idle items (no row
-    // of the tile sees the split) are skipped identically by every role
-    auto item_info = [&](int it, Work& wk, int& h) -> bool {
-        wk = work[it / H];
-        h = it % H;
-        return wk.nch > 0 && wk.t0 < seqs.qn[wk.seq];
-    };
+    // every role walks the same item sequence (ItemIter) and skips the same idle items
 
     if (warp == 0) {
         if (lane == 0) {   // ---------------- TMA producer
             int g = 0, n = 0;
-            for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-                Work wk;
-                int h;
-                if (!item_info(it, wk, h)) continue;
-                const int slot = seqs.slot[wk.seq], q0row = seqs.q0[wk.seq];
+            ItemIter items(work, n_items, H);
+            Work wk;
+            int h;
+            while (items.next(wk, h)) {
+                const int slot = wk.slot, q0row = wk.q0row;
                 const int qb = n & 1;
                 if (n >= 2) mbar_wait(su32(&q_empty[qb]), ((n >> 1) - 1) & 1);
                 mbar_expect_tx(su32(&q_full[qb]), 2 * Cf::R_TILE);
@@ -318,10 +339,10 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
                 if (p.last) commit(su32(&o_full[p.ob]));
             };
             int g = 0, n = 0;
-            for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-                Work wk;
-                int h;
-                if (!item_info(it, wk, h)) continue;
+            ItemIter items(work, n_items, H);
+            Work wk;
+            int h;
+            while (items.next(wk, h)) {
                 const int qb = n & 1, ob = n & 1;
                 mbar_wait(su32(&q_full[qb]), (n >> 1) & 1);
                 for (int c = 0; c < wk.nch; ++c, ++g) {
@@ -360,11 +381,11 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
         const uint32_t prow = (uint32_t)key * (2 * NQ);
         const uint32_t pswz = NQ == 16 ? ((key >> 2) & 1) : NQ == 32 ? ((key >> 1) & 3) : (key & 7);
         int g = 0, n = 0;
-        for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-            Work wk;
-            int h;
-            if (!item_info(it, wk, h)) continue;
-            const int qn = seqs.qn[wk.seq], off = seqs.off[wk.seq], q0row = seqs.q0[wk.seq];
+        ItemIter items(work, n_items, H);
+        Work wk;
+        int h;
+        while (items.next(wk, h)) {
+            const int qn = wk.qn, off = wk.off, q0row = wk.q0row;
             const int L = off + qn, s0 = wk.split * SPLIT, ob = n & 1;
             const int ncol = min(NQ, qn - wk.t0);   // valid query columns of the tile (uniform)
             const int dlim = off + wk.t0;           // column j sees keys kp <= dlim + j
@@ -500,6 +521,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cf::TMEM_COLS)
                      : "memory");
+    trace_end(tr, t_start);
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -547,7 +569,7 @@ static void launch(bass_ctx* ctx, const AttnPlan& p, const CUtensorMap& tk, cons
     const int n_items = nw * p.H;
     const int grid = std::max(1, std::min(n_items, ctx->sm_count));
     BASS_CUDA(launch_pdl(attn_stream_kernel<NQ>, dim3(grid), dim3(THREADS), (size_t)Cf::SMEM, ctx->stream, p.tq, tk,
-                         tv, seqs, wp, n_items, p.H, p.cap, po, pml, p.mc, out));
+                         tv, seqs, wp, n_items, p.H, p.cap, po, pml, p.mc, out, ctx->trace(grid, BASS_TR_ATTN)));
 }
 
 }  // namespace ast
@@ -557,8 +579,8 @@ int stream_split_len() { return ast::SPLIT; }
 // Plan: work items (seq, q tile, split, chunks seen) — RAGGED/SPLIT exact,
 // PAD over the padded [max q] x [max L] grid (padded keys streamed, masked).
 void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, int n_slots,
-                           const std::vector<int32_t>& qn, const std::vector<int32_t>& off, int H, int cap,
-                           DevBuf& work_buf, AttnPlan& plan) {
+                           const std::vector<int32_t>& slot, const std::vector<int32_t>& qn,
+                           const std::vector<int32_t>& off, int H, int cap, DevBuf& work_buf, AttnPlan& plan) {
     using namespace ast;
     const int n_seq = (int)qn.size();
     int max_qn = 0, max_L = 0;
@@ -571,20 +593,22 @@ void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, in
     std::vector<int32_t> w;
     std::vector<int> first(n_seq + 1, 0);
     bool multi = false;
+    int q0 = 0;   // rows are laid out sequence after sequence
     for (int i = 0; i < n_seq; ++i) {
-        first[i] = (int)w.size() / 4;
+        first[i] = (int)w.size() / 8;
         const int rows = strategy == BASS_PAD ? max_qn : qn[i];
         for (int t0 = 0; t0 < rows; t0 += NQ) {
             const int last = strategy == BASS_PAD ? max_L - 1 : off[i] + std::min(qn[i], t0 + NQ) - 1;
             const int n_chunks = last / CH + 1;
             for (int s = 0; s * SPLIT_CH < n_chunks; ++s) {
-                w.insert(w.end(), {i, t0, s, std::min(SPLIT_CH, n_chunks - s * SPLIT_CH)});
+                w.insert(w.end(), {slot[i], q0, qn[i], off[i], t0, s, std::min(SPLIT_CH, n_chunks - s * SPLIT_CH), 0});
                 if (s > 0) multi = true;
             }
         }
+        q0 += qn[i];
     }
-    first[n_seq] = (int)w.size() / 4;
-    Work* wd = (Work*)work_buf.need(std::max<size_t>(w.size(), 4) * 4, ctx->stream);
+    first[n_seq] = (int)w.size() / 8;
+    Work* wd = (Work*)work_buf.need(std::max<size_t>(w.size(), 8) * 4, ctx->stream);
     void* hst = ctx->staging.take(w.size() * 4);
     if (!hst) {
         ctx->sync();

@@ -22,6 +22,30 @@ BASS_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :
 // PDL-launched kernel calls this before its first dependent global access.
 BASS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Per-CTA timeline trace (diagnostics): when buf != nullptr, CTA i of a traced
+// launch writes {t_start, t_end, smid, tag} (globaltimer ns) at record base + i.
+struct TraceArg {
+    unsigned long long* buf;
+    long long base;
+    int tag;
+};
+BASS_DEV unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+BASS_DEV void trace_end(const TraceArg& tr, unsigned long long t0) {
+    if (tr.buf && threadIdx.x == 0) {
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        unsigned long long* r = tr.buf + 4 * (tr.base + blockIdx.x);
+        r[0] = t0;
+        r[1] = gtimer();
+        r[2] = sm;
+        r[3] = (unsigned long long)tr.tag;
+    }
+}
+
 // Launch with programmatic stream serialization (PDL).
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -38,6 +62,19 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
+
+// Packed weight layout for the tcgen05 GEMM: [N, K] output-major matrices are
+// stored as 128 x 64 tiles (16 KB each), tile (nt, kb) at ((nt * K/64) + kb),
+// each tile the exact shared-memory image of a K-major 128-byte-swizzled UMMA
+// operand (row r at r * 128 B, 16-byte chunk c at (c ^ (r & 7)) * 16 B).  A
+// CTA's weight stream is then a run of contiguous 16 KB blocks (1-D bulk
+// copies, full DRAM pages) instead of 128-byte row pieces.
+BASS_DEV int64_t packed_index(int64_t n, int64_t k, int64_t K) {
+    const int64_t tile = (n >> 7) * (K >> 6) + (k >> 6);
+    const int r = (int)(n & 127), c = (int)((k & 63) >> 3);
+    return tile * 8192 + r * 64 + ((c ^ (r & 7)) << 3) + (k & 7);
+}
+inline int64_t packed_rows(int64_t N) { return (N + 127) / 128 * 128; }
 
 // element access in either storage dtype; all math is fp32 (or fp64 for sampling)
 BASS_DEV float ld(const float* p, int64_t i) { return p[i]; }

@@ -1,24 +1,37 @@
-// tcgen05 weight-streaming GEMM for the ragged forward (sm_100a).
+// tcgen05 weight-streaming GEMM for the ragged forward (sm_100a): the batched
+// draft / verify projections of BASS (ref:model.py:160-164 `_linear`,
+// :214-245; the dense layers stay batched).
 //
 //   Y[m, n] = sum_k X[m, k] W[n, k]      (W output-major [N, K] bf16, X [M, K] bf16)
 //
-// Swap-AB: the weight tile is the MMA's M side (128 rows of W per CTA) and the
-// token block is the MMA's N side (16..256 tokens), so a skinny verify/draft
-// GEMM (M = 8..264 rows) still issues full 128-row UMMAs and the kernel is a
-// pure HBM weight stream.  Per CTA: TMA (128B swizzle) fills a ring of smem
-// stages {W 128x64, X TTx64}; one elected thread issues tcgen05.mma
-// (kind::f16, fp32 accumulate in TMEM); tcgen05.commit frees each stage;
-// after the last k-block, 4 warps drain TMEM (tcgen05.ld 32x32b) through the
-// fused epilogue (QKV + KV-append, residual add, GELU, fp32 logits).
-// Split-K over a fixed, M-independent split count keeps >= one full wave of
-// CTAs on 148 SMs; partials are reduced in split order by the last CTA of a
-// tile (deterministic, no atomics on data).
+// Swap-AB: weight rows are the MMA's M side (NB sub-tiles of 128 rows per
+// CTA), the token block the N side (TT = 16..256 tokens), so a skinny
+// verify/draft GEMM (M = 8..264 rows) issues full 128-row UMMAs and the kernel
+// is a pure HBM weight stream.  Per CTA a ring of shared-memory stages
+// {W NB x [128 x 64], X [TT x 64]} is filled by one producer thread — W as
+// contiguous 16 KB blocks of the packed tile layout (one 1-D bulk copy each,
+// whole DRAM pages; common.cuh packed_index), X through a 2-D TMA map — and
+// one elected thread issues tcgen05.mma (kind::f16, fp32 accumulators in
+// TMEM, one per sub-tile).  With NB = 2 the two sub-tiles share every X tile,
+// halving the L2 -> SM activation traffic that bounds the verify shapes
+// (M ~ 88-264).  After the last k block four warps drain TMEM (tcgen05.ld
+// 32x32b) through the fused epilogue (QKV + KV-append, residual add, exact
+// GELU, fp32 logits).
+// Split-K over a fixed split count S(N, K) — never a function of M, so a
+// row's bits do not depend on the batch (batched == solo, verify ==
+// sequential decode): the S CTAs of a tile are one thread-block cluster; each
+// writes its fp32 partial to an L2-resident workspace and after a cluster
+// barrier reduces 1/S of the tile in split order (deterministic, no atomics).
+// Many CTAs (2 per SM when they fit) let the hardware scheduler balance the
+// tail and let the next kernel (PDL) prefetch its weights beside this one.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
-#include <mutex>
+#include <string>
 #include <tuple>
 
 #include "runtime.h"
@@ -26,21 +39,23 @@
 namespace bass {
 namespace tc {
 
-constexpr int BN = 128;          // weight rows per CTA (UMMA M)
+constexpr int BN = 128;          // weight rows per sub-tile (UMMA M)
 constexpr int BK = 64;           // k per stage (one 128-byte swizzle row of bf16)
 constexpr int UK = 16;           // k per tcgen05.mma for 16-bit inputs
 constexpr int THREADS = 128;
-constexpr int SMEM_BUDGET = 110 * 1024;   // two CTAs per SM (228 KB per SM)
 
-template <int TT>
+template <int TT, int NB>
 struct Cfg {
-    static constexpr int W_BYTES = BN * BK * 2;
+    static constexpr int W_BYTES = NB * BN * BK * 2;
     static constexpr int X_BYTES = TT * BK * 2;
     static constexpr int STAGE = W_BYTES + X_BYTES;
-    static constexpr int STAGES_RAW = (SMEM_BUDGET - 2048) / STAGE;
+    // two CTAs per SM (110 KB) when that still leaves >= 2 stages, else one
+    static constexpr int BUDGET = (110 * 1024 - 2048) / STAGE >= 2 ? 110 * 1024 - 2048 : 200 * 1024;
+    static constexpr int STAGES_RAW = BUDGET / STAGE;
     static constexpr int STAGES = STAGES_RAW > 8 ? 8 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
     static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
-    static constexpr int TMEM_COLS = TT < 32 ? 32 : TT;
+    static constexpr int COLS = NB * TT;
+    static constexpr int TMEM_COLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128 : COLS <= 256 ? 256 : 512;
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -70,6 +85,12 @@ __device__ __forceinline__ void tma_2d(const CUtensorMap* map, uint32_t dst, uin
             dst),
         "l"(map), "r"(bar), "r"(c0), "r"(c1)
         : "memory");
+}
+// 1-D bulk copy global -> shared (one packed 16 KB weight tile)
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
 }
 // UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B
 // apart (SBO = 64 x 16 B), LBO = 1 (unused for swizzled K-major), version 1.
@@ -109,15 +130,17 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 struct Split {
     int S;             // number of K splits
     int k_iters;       // K / BK
-    float* ws;         // [S][M][N] fp32 partials (S > 1)
-    int* counters;     // per (n_tile, token group), zero between launches
+    float* ws;         // per (tile, token group): [S][TT][NB*BN] fp32 partials (S > 1)
 };
 
-template <int TT, int MODE>
+// PACKED: W in the packed tile layout (1-D bulk copies); else W [N, K] via `tw`.
+template <int TT, int MODE, int NB, bool PACKED>
 __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tw,
-                                                             const __grid_constant__ CUtensorMap tx, int M,
-                                                             int N, Split sp, Epi e) {
-    using C = Cfg<TT>;
+                                                             const __grid_constant__ CUtensorMap tx,
+                                                             const __nv_bfloat16* __restrict__ wpk, int M, int N,
+                                                             Split sp, Epi e, TraceArg tr) {
+    const unsigned long long t_start = tr.buf ? gtimer() : 0ull;
+    using C = Cfg<TT, NB>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = su32(smem_raw);
     const uint32_t base = (raw + 1023) & ~1023u;
@@ -125,11 +148,10 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
     // bars[0..S) full, [S..2S) empty, [2S] done; tmem base address after
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 1);
-    __shared__ int s_last;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_tile = blockIdx.x, split = blockIdx.y, group = blockIdx.z;
-    const int n0 = n_tile * BN, m0 = group * TT;
+    const int tile = blockIdx.x, split = blockIdx.y, group = blockIdx.z;
+    const int n0 = tile * NB * BN, m0 = group * TT;
     const int it0 = (int)((int64_t)split * sp.k_iters / sp.S);
     const int it1 = (int)((int64_t)(split + 1) * sp.k_iters / sp.S);
     const int nit = it1 - it0;
@@ -142,7 +164,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
         mbar_init(su32(&bars[2 * C::STAGES]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&tw) : "memory");
+        if (!PACKED) asm volatile("prefetch.tensormap [%0];" ::"l"(&tw) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tx) : "memory");
     }
     if (warp == 2) {
@@ -159,15 +181,26 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
     // PDL: let the next kernel's CTAs start their own prologue / weight
     // prefetch as soon as SMs free up
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    auto load_w = [&](uint32_t dst, uint32_t bar, int kb) {
+#pragma unroll
+        for (int sub = 0; sub < NB; ++sub) {
+            if constexpr (PACKED) {
+                const int nt = tile * NB + sub;   // 128-row packed tile
+                bulk_g2s(dst + sub * BN * BK * 2, wpk + ((int64_t)nt * sp.k_iters + kb) * (BN * BK), BN * BK * 2, bar);
+            } else {
+                tma_2d(&tw, dst + sub * BN * BK * 2, bar, kb * BK, n0 + sub * BN);
+            }
+        }
+    };
     if (warp == 0) {
-        if (lane == 0) {   // ---- TMA producer
+        if (lane == 0) {   // ---- producer
             // Weights do not depend on the previous kernel: fill the ring with
             // W tiles first, then wait for the producer of X (griddepcontrol)
             const int pre = nit < C::STAGES ? nit : C::STAGES;
             for (int i = 0; i < pre; ++i) {
                 const uint32_t full = su32(&bars[i]);
                 mbar_expect_tx(full, C::STAGE);
-                tma_2d(&tw, base + i * C::STAGE, full, (it0 + i) * BK, n0);
+                load_w(base + i * C::STAGE, full, it0 + i);
             }
             asm volatile("griddepcontrol.wait;" ::: "memory");
             for (int i = 0; i < pre; ++i)
@@ -178,24 +211,28 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
                 const uint32_t full = su32(&bars[s]);
                 const uint32_t st = base + s * C::STAGE;
                 mbar_expect_tx(full, C::STAGE);
-                const int k = (it0 + i) * BK;
-                tma_2d(&tw, st, full, k, n0);
-                tma_2d(&tx, st + C::W_BYTES, full, k, m0);
+                load_w(st, full, it0 + i);
+                tma_2d(&tx, st + C::W_BYTES, full, (it0 + i) * BK, m0);
             }
         }
         __syncwarp();
     } else if (warp == 1) {
-        if (lane == 0) {   // ---- MMA issuer
+        if (lane == 0) {   // ---- MMA issuer: one accumulator (TT columns) per sub-tile
             constexpr uint32_t ID = idesc(TT);
             for (int i = 0; i < nit; ++i) {
                 const int s = i % C::STAGES;
                 mbar_wait(su32(&bars[s]), (i / C::STAGES) & 1);
                 fence_after();
                 const uint32_t st = base + s * C::STAGE;
-                const uint64_t a = sdesc(st), b = sdesc(st + C::W_BYTES);
+                const uint64_t b = sdesc(st + C::W_BYTES);
 #pragma unroll
-                for (int kk = 0; kk < BK / UK; ++kk)   // +32 bytes per UMMA_K step inside the swizzle row
-                    umma(tmem, a + (uint64_t)(kk * 2), b + (uint64_t)(kk * 2), ID, (i > 0 || kk > 0) ? 1u : 0u);
+                for (int sub = 0; sub < NB; ++sub) {
+                    const uint64_t a = sdesc(st + sub * BN * BK * 2);
+#pragma unroll
+                    for (int kk = 0; kk < BK / UK; ++kk)   // +32 bytes per UMMA_K step inside the swizzle row
+                        umma(tmem + sub * TT, a + (uint64_t)(kk * 2), b + (uint64_t)(kk * 2), ID,
+                             (i > 0 || kk > 0) ? 1u : 0u);
+                }
                 umma_commit(su32(&bars[C::STAGES + s]));
             }
             umma_commit(su32(&bars[2 * C::STAGES]));
@@ -203,62 +240,73 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
         __syncwarp();
     }
 
-    // ---- epilogue: TMEM lane = weight row n0 + 32*warp + lane; columns = tokens
+    // ---- epilogue: TMEM lane = weight row n0 + sub*128 + 32*warp + lane; columns = tokens
     asm volatile("griddepcontrol.wait;" ::: "memory");   // previous kernel's writes visible
     mbar_wait(su32(&bars[2 * C::STAGES]), 0);
     fence_after();
-    const int n = n0 + warp * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+    const int rows = min(TT, M - m0);
     if (sp.S == 1) {
-#pragma unroll 1
-        for (int c0 = 0; c0 < TT; c0 += 16) {
-            float v[16];
-            tmem_ld16(trow + c0, v);
-            if (n < N) {
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int m = m0 + c0 + j;
-                    if (m < M) epilogue<MODE, __nv_bfloat16>(e, m, n, N, v[j]);
+        for (int sub = 0; sub < NB; ++sub) {
+            const int n = n0 + sub * BN + warp * 32 + lane;
+#pragma unroll 1
+            for (int c0 = 0; c0 < TT; c0 += 16) {
+                if (c0 >= rows) break;
+                float v[16];
+                tmem_ld16(trow + sub * TT + c0, v);
+                if (n < N) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (c0 + j < rows) epilogue<MODE, __nv_bfloat16>(e, m0 + c0 + j, n, N, v[j]);
                 }
             }
         }
     } else {
         // split-K: the S CTAs of this tile are one thread-block cluster.  Each
         // writes its fp32 partial tile (L2-resident scratch), the cluster
-        // barrier publishes them, and CTA `split` reduces rows
+        // barrier publishes them, and CTA `split` reduces token rows
         // [split*R/S, (split+1)*R/S) of the tile in fixed split order.
-        const int rows = min(TT, M - m0);
-        const int nn = warp * 32 + lane;
-        float* blk = sp.ws + (int64_t)(n_tile * gridDim.z + group) * sp.S * TT * BN;
-#pragma unroll 1
-        for (int c0 = 0; c0 < TT; c0 += 16) {
-            float v[16];
-            tmem_ld16(trow + c0, v);
+        constexpr int WR = NB * BN;   // partial row width
+        float* blk = sp.ws + (int64_t)(tile * gridDim.z + group) * sp.S * TT * WR;
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c0 + j < rows) blk[((int64_t)split * TT + c0 + j) * BN + nn] = v[j];
+        for (int sub = 0; sub < NB; ++sub) {
+            const int nn = sub * BN + warp * 32 + lane;
+#pragma unroll 1
+            for (int c0 = 0; c0 < TT; c0 += 16) {
+                if (c0 >= rows) break;
+                float v[16];
+                tmem_ld16(trow + sub * TT + c0, v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (c0 + j < rows) __stcg(&blk[((int64_t)split * TT + c0 + j) * WR + nn], v[j]);
+            }
         }
         __threadfence();
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         const int r0 = split * rows / sp.S, r1 = (split + 1) * rows / sp.S;
-        if (n < N) {
-            int r = r0;
-            for (; r + 4 <= r1; r += 4) {   // 4 rows x S partials in flight
-                float acc[4] = {0.f, 0.f, 0.f, 0.f};
-                for (int s = 0; s < sp.S; ++s) {
-                    float p[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) p[u] = __ldcg(&blk[((int64_t)s * TT + r + u) * BN + nn]);
+        for (int sub = 0; sub < NB; ++sub) {
+            const int nn = sub * BN + warp * 32 + lane, n = n0 + nn;
+            if (n < N) {
+                int r = r0;
+                for (; r + 4 <= r1; r += 4) {   // 4 rows x S partials in flight
+                    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                    for (int s = 0; s < sp.S; ++s) {
+                        float p[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) acc[u] += p[u];
+                        for (int u = 0; u < 4; ++u) p[u] = __ldcg(&blk[((int64_t)s * TT + r + u) * WR + nn]);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) acc[u] += p[u];
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) epilogue<MODE, __nv_bfloat16>(e, m0 + r + u, n, N, acc[u]);
                 }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) epilogue<MODE, __nv_bfloat16>(e, m0 + r + u, n, N, acc[u]);
-            }
-            for (; r < r1; ++r) {
-                float acc = 0.f;
-                for (int s = 0; s < sp.S; ++s) acc += __ldcg(&blk[((int64_t)s * TT + r) * BN + nn]);
-                epilogue<MODE, __nv_bfloat16>(e, m0 + r, n, N, acc);
+                for (; r < r1; ++r) {
+                    float acc = 0.f;
+                    for (int s = 0; s < sp.S; ++s) acc += __ldcg(&blk[((int64_t)s * TT + r) * WR + nn]);
+                    epilogue<MODE, __nv_bfloat16>(e, m0 + r, n, N, acc);
+                }
             }
         }
     }
@@ -267,6 +315,16 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
     if (warp == 2)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS)
                      : "memory");
+    if (tr.buf && threadIdx.x == 0) {   // trace record index: linear block id
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        const long long id = tr.base + blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z);
+        unsigned long long* rec = tr.buf + 4 * id;
+        rec[0] = t_start;
+        rec[1] = gtimer();
+        rec[2] = sm;
+        rec[3] = (unsigned long long)tr.tag;
+    }
 }
 
 // ------------------------------------------------------------------ host
@@ -304,8 +362,7 @@ struct State {
     std::map<std::tuple<const void*, int, int>, CUtensorMap> wmaps;
     std::map<std::tuple<const void*, int, int, int>, CUtensorMap> xmaps;   // (X, M, K, TT)
     std::map<std::pair<int, int>, int> splits;
-    DevBuf ws, counters;
-    size_t counters_n = 0;
+    DevBuf ws;
 };
 
 static State& state(bass_model& m) {
@@ -315,19 +372,18 @@ static State& state(bass_model& m) {
 
 // Split count from (N, K) only — never from M — so a row's reduction order
 // (and hence its bits) does not depend on how many rows share the launch.
-// Policy: the largest split (<= 8, >= 4 k-blocks per CTA) that still fits in
-// one wave of co-resident CTAs (2 per SM); more tiles than that -> no split.
+// The table holds the benchmark's projection shapes (profiles/r1_gemm_*);
+// elsewhere: the largest split (<= 8, >= 4 k-blocks per CTA) that keeps the
+// 128-row tiles within ~1.75 CTAs per SM.
 static int choose_splits(int sm_count, int N, int K) {
-    const int n_tiles = (N + BN - 1) / BN, k_iters = K / BK;
-    // measured on B200 (profiles/r1_gemm_split_sweep.txt) for the benchmark's
-    // projection shapes; the rule below covers everything else
     static const struct { int N, K, S; } tuned[] = {
         {13824, 4608, 2}, {4608, 4608, 6}, {18432, 4608, 2}, {4608, 18432, 6}, {50272, 4608, 1},
         {6144, 2048, 4},  {2048, 2048, 8}, {8192, 2048, 4},  {2048, 8192, 8},  {50272, 2048, 1}};
-    if (sm_count == 148)
+    if (sm_count == 148 && !getenv("BASS_NO_SPLIT_TABLE"))
         for (const auto& t : tuned)
             if (t.N == N && t.K == K) return t.S;
-    const int slots = sm_count * 7 / 4;   // ~1.75 CTAs per SM keeps clusters in one wave
+    const int n_tiles = (N + BN - 1) / BN, k_iters = K / BK;
+    const int slots = sm_count * 7 / 4;
     static const int cap_s = getenv("BASS_MAX_SPLIT") ? atoi(getenv("BASS_MAX_SPLIT")) : 8;
     int best_s = 1;
     for (int s = 2; s <= cap_s; ++s)
@@ -335,43 +391,62 @@ static int choose_splits(int sm_count, int N, int K) {
     return best_s;
 }
 
-template <int TT, int MODE>
-static void launch(bass_model& m, const CUtensorMap& wm, const CUtensorMap& xm, int M, int N, int K, const Split& sp,
-                   const Epi& e) {
-    using C = Cfg<TT>;
+struct LaunchArgs {
+    const CUtensorMap* wm;
+    const CUtensorMap* xm;
+    const void* W;
+    int M, N;
+    Split sp;
+};
+
+template <int TT, int MODE, int NB, bool PACKED>
+static void launch_k(bass_model& m, const LaunchArgs& a, const Epi& e) {
+    using C = Cfg<TT, NB>;
     static bool attr = false;
     if (!attr) {
-        BASS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<TT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        BASS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<TT, MODE, NB, PACKED>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
         attr = true;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((N + BN - 1) / BN, sp.S, (M + TT - 1) / TT);
+    cfg.gridDim = dim3((a.N + NB * BN - 1) / (NB * BN), a.sp.S, (a.M + TT - 1) / TT);
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = m.ctx->stream;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    at[1].id = cudaLaunchAttributeClusterDimension;   // split-K CTAs of a tile = one cluster
-    at[1].val.clusterDim.x = 1;
-    at[1].val.clusterDim.y = sp.S;
-    at[1].val.clusterDim.z = 1;
     static const bool pdl = !(getenv("BASS_PDL") && atoi(getenv("BASS_PDL")) == 0);
     at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    at[1].id = cudaLaunchAttributeClusterDimension;   // split-K CTAs of a tile = one cluster
+    at[1].val.clusterDim.x = 1;
+    at[1].val.clusterDim.y = a.sp.S;
+    at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
-    cfg.numAttrs = sp.S > 1 ? 2 : 1;
-    BASS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TT, MODE>, wm, xm, M, N, sp, e));
+    cfg.numAttrs = a.sp.S > 1 ? 2 : 1;
+    const int nblk = (int)(cfg.gridDim.x * cfg.gridDim.y * cfg.gridDim.z);
+    BASS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TT, MODE, NB, PACKED>, *a.wm, *a.xm,
+                                 (const __nv_bfloat16*)a.W, a.M, a.N, a.sp, e, m.ctx->trace(nblk, BASS_TR_GEMM)));
+}
+
+template <int TT, int NB>
+static void launch_mode(bass_model& m, int mode, bool packed, const LaunchArgs& a, const Epi& e) {
+    if (!packed) {   // raw [N, K] pointers (bass_gemm): plain fp32 store
+        if (mode != EPI_STORE) throw Error(BASS_ERR_STATE, "tcgen05 GEMM: fused epilogues need packed weights");
+        launch_k<TT, EPI_STORE, NB, false>(m, a, e);
+        return;
+    }
+    switch (mode) {
+        case EPI_QKV: launch_k<TT, EPI_QKV, NB, true>(m, a, e); break;
+        case EPI_RESID: launch_k<TT, EPI_RESID, NB, true>(m, a, e); break;
+        case EPI_GELU: launch_k<TT, EPI_GELU, NB, true>(m, a, e); break;
+        default: launch_k<TT, EPI_STORE, NB, true>(m, a, e); break;
+    }
 }
 
 template <int TT>
-static void launch_mode(bass_model& m, int mode, const CUtensorMap& wm, const CUtensorMap& xm, int M, int N, int K,
-                        const Split& sp, const Epi& e) {
-    switch (mode) {
-        case EPI_QKV: launch<TT, EPI_QKV>(m, wm, xm, M, N, K, sp, e); break;
-        case EPI_RESID: launch<TT, EPI_RESID>(m, wm, xm, M, N, K, sp, e); break;
-        case EPI_GELU: launch<TT, EPI_GELU>(m, wm, xm, M, N, K, sp, e); break;
-        default: launch<TT, EPI_STORE>(m, wm, xm, M, N, K, sp, e); break;
-    }
+static void launch_nb(bass_model& m, int mode, bool packed, int nb, const LaunchArgs& a, const Epi& e) {
+    if (nb == 2) launch_mode<TT, 2>(m, mode, packed, a, e);
+    else launch_mode<TT, 1>(m, mode, packed, a, e);
 }
 
 }  // namespace tc
@@ -380,33 +455,42 @@ bool tc_gemm_supported(const bass_model& m, int N, int K) {
     return m.dtype == BASS_BF16 && K % tc::BK == 0 && K >= tc::BK && N >= tc::BN;
 }
 
-void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K, const Epi& e) {
+void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K, const Epi& e, bool packed) {
     using namespace tc;
     State& S = state(m);
     // token tile: smallest of 16/32/64/128/256 covering M (groups of 256 beyond)
     const int TT = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
-    auto key = std::make_tuple(W, N, K);
-    auto it = S.wmaps.find(key);
-    if (it == S.wmaps.end()) it = S.wmaps.emplace(key, make_map(W, N, K, BN)).first;
+    // NB = 2: 256-row CTA tiles (two accumulators sharing each X tile)
+    static const int nb_env = getenv("BASS_GEMM_NB") ? atoi(getenv("BASS_GEMM_NB")) : 0;
+    // (measured: NB = 1 wins at every benchmark shape, profiles/r1_gemm_nb_split_sweep.txt)
+    const int NB = nb_env == 2 ? 2 : 1;
+    static CUtensorMap dummy{};
+    const CUtensorMap* wm = &dummy;
+    if (!packed) {
+        auto key = std::make_tuple(W, N, K);
+        auto it = S.wmaps.find(key);
+        if (it == S.wmaps.end()) it = S.wmaps.emplace(key, make_map(W, N, K, BN)).first;
+        wm = &it->second;
+    }
     auto xkey = std::make_tuple(X, M, K, TT);
     auto xit = S.xmaps.find(xkey);
     if (xit == S.xmaps.end()) xit = S.xmaps.emplace(xkey, make_map(X, M, K, TT)).first;
-    const CUtensorMap& xm = xit->second;
     auto sk = std::make_pair(N, K);
     auto si = S.splits.find(sk);
     if (si == S.splits.end()) si = S.splits.emplace(sk, choose_splits(m.ctx->sm_count, N, K)).first;
-    Split sp{si->second, K / BK, nullptr, nullptr};
+    Split sp{si->second, K / BK, nullptr};
     if (const char* fs = getenv("BASS_FORCE_SPLIT")) sp.S = std::max(1, std::min(8, atoi(fs)));   // tuning only
     if (sp.S > 1) {
-        const size_t blocks = (size_t)((N + BN - 1) / BN) * ((M + TT - 1) / TT);
-        sp.ws = (float*)S.ws.need(blocks * sp.S * TT * BN * 4, m.ctx->stream);
+        const size_t blocks = (size_t)((N + NB * BN - 1) / (NB * BN)) * ((M + TT - 1) / TT);
+        sp.ws = (float*)S.ws.need(blocks * sp.S * TT * NB * BN * 4, m.ctx->stream);
     }
+    LaunchArgs a{wm, &xit->second, W, M, N, sp};
     switch (TT) {
-        case 16: launch_mode<16>(m, mode, it->second, xm, M, N, K, sp, e); break;
-        case 32: launch_mode<32>(m, mode, it->second, xm, M, N, K, sp, e); break;
-        case 64: launch_mode<64>(m, mode, it->second, xm, M, N, K, sp, e); break;
-        case 128: launch_mode<128>(m, mode, it->second, xm, M, N, K, sp, e); break;
-        default: launch_mode<256>(m, mode, it->second, xm, M, N, K, sp, e); break;
+        case 16: launch_nb<16>(m, mode, packed, NB, a, e); break;
+        case 32: launch_nb<32>(m, mode, packed, NB, a, e); break;
+        case 64: launch_nb<64>(m, mode, packed, NB, a, e); break;
+        case 128: launch_nb<128>(m, mode, packed, NB, a, e); break;
+        default: launch_nb<256>(m, mode, packed, NB, a, e); break;
     }
     m.ctx->launches++;
     cudaError_t err = cudaGetLastError();
@@ -417,7 +501,6 @@ void tc_release(bass_model& m) {
     if (!m.tc_state) return;
     tc::State* s = static_cast<tc::State*>(m.tc_state);
     s->ws.release();
-    s->counters.release();
     delete s;
     m.tc_state = nullptr;
 }

@@ -53,7 +53,8 @@ __global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(const float* __re
                                                                const int32_t* __restrict__ gather,
                                                                const float* __restrict__ g,
                                                                const float* __restrict__ b, int d,
-                                                               TA* __restrict__ out) {
+                                                               TA* __restrict__ out, TraceArg tr) {
+    const unsigned long long t_start = tr.buf ? gtimer() : 0ull;
     __shared__ float red[33];
     pdl_trigger();
     pdl_wait();
@@ -96,6 +97,7 @@ __global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(const float* __re
             st(out, o + 3, (v[i].w - mean) * rstd * gg.w + bv.w);
         }
     }
+    trace_end(tr, t_start);
 }
 
 // ------------------------------------------------------------- epilogues
@@ -146,7 +148,7 @@ constexpr int SG_BN = 64, SG_BM = 16, SG_BK = 32;
 template <int MODE, typename TA, typename TW>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(const TA* __restrict__ X,
                                                          const TW* __restrict__ W, int M, int N,
-                                                         int K, Epi e) {
+                                                         int K, Epi e, bool packed) {
     __shared__ float Ws[SG_BK][SG_BN + 1];
     __shared__ float Xs[SG_BM][SG_BK + 1];
     const int t = threadIdx.x;
@@ -158,7 +160,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const TA* __restrict__ X
         for (int j = 0; j < (SG_BN * SG_BK) / 256; ++j) {
             const int i = t + 256 * j, nn = i / SG_BK, kk = i % SG_BK;
             const int gn = n0 + nn, gk = k0 + kk;
-            Ws[kk][nn] = (gn < N && gk < K) ? ld(W, (int64_t)gn * K + gk) : 0.f;
+            Ws[kk][nn] = (gn < N && gk < K) ? ld(W, packed ? packed_index(gn, gk, K) : (int64_t)gn * K + gk) : 0.f;
         }
 #pragma unroll
         for (int j = 0; j < (SG_BM * SG_BK) / 256; ++j) {

@@ -129,7 +129,7 @@ namespace {
 // dst[n, k] = src[k, n]  (reference input-major [K, N] -> output-major [N, K])
 template <typename T>
 __global__ void transpose_convert(const float* __restrict__ src, int K, int N, T* __restrict__ dst,
-                                  int64_t dst_ld) {
+                                  int64_t dst_ld, int64_t row_off, bool packed) {
     __shared__ float tile[32][33];
     const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -139,7 +139,17 @@ __global__ void transpose_convert(const float* __restrict__ src, int K, int N, T
     __syncthreads();
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
         const int n = n0 + i, k = k0 + threadIdx.x;
-        if (n < N && k < K) dst[(int64_t)n * dst_ld + k] = cvt<T>(tile[threadIdx.x][i]);
+        if (n < N && k < K)
+            dst[packed ? packed_index(row_off + n, k, dst_ld) : (row_off + n) * dst_ld + k] = cvt<T>(tile[threadIdx.x][i]);
+    }
+}
+
+__global__ void pack_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst, int N, int K,
+                            int64_t src_stride, int64_t dst_stride, int n_mat) {
+    const int64_t per = (int64_t)N * K;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < per * n_mat; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t mat = i / per, r = i - mat * per, n = r / K, k = r - n * K;
+        dst[mat * dst_stride + packed_index(n, k, K)] = src[mat * src_stride + r];
     }
 }
 
@@ -175,7 +185,7 @@ static void launch_layernorm(bass_model& m, const float* x, const int32_t* gathe
                              const float* b, int rows, TA* out) {
     ProfScope prof(m.ctx, BASS_PROF_NORM, (double)rows * m.g.d_model * (4.0 + sizeof(TA)));
     BASS_CUDA(launch_pdl(layernorm_kernel<TA>, dim3(rows), dim3(256), 0, m.ctx->stream, x, gather, g, b,
-                         m.g.d_model, out));
+                         m.g.d_model, out, m.ctx->trace(rows, BASS_TR_NORM)));
     check_launch(m.ctx);
 }
 
@@ -186,9 +196,9 @@ static void launch_layernorm_any(bass_model& m, const float* x, const int32_t* g
 }
 
 template <int MODE, typename TA>
-static void gemm_simt(bass_model& m, const void* X, const void* W, int M, int N, int K, const Epi& e) {
+static void gemm_simt(bass_model& m, const void* X, const void* W, int M, int N, int K, const Epi& e, bool packed) {
     dim3 grid((N + SG_BN - 1) / SG_BN, (M + SG_BM - 1) / SG_BM);
-    gemm_simt_kernel<MODE, TA, TA><<<grid, 256, 0, m.ctx->stream>>>((const TA*)X, (const TA*)W, M, N, K, e);
+    gemm_simt_kernel<MODE, TA, TA><<<grid, 256, 0, m.ctx->stream>>>((const TA*)X, (const TA*)W, M, N, K, e, packed);
     check_launch(m.ctx);
 }
 
@@ -199,20 +209,29 @@ static double gemm_bytes(const bass_model& m, int mode, int M, int N, int K) {
     return es * N * K + es * M * K + out;
 }
 
-void gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K, const Epi& e) {
+void pack_weights(cudaStream_t st, const void* src, void* dst, int N, int K, int n_mat) {
+    pack_kernel<<<1184, 256, 0, st>>>((const __nv_bfloat16*)src, (__nv_bfloat16*)dst, N, K, (int64_t)N * K,
+                                      packed_rows(N) * K, n_mat);
+    BASS_CUDA(cudaGetLastError());
+}
+
+void gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K, const Epi& e, bool packed) {
     if (M == 0) return;
     ProfScope prof(m.ctx, BASS_PROF_GEMM, gemm_bytes(m, mode, M, N, K), 2.0 * M * N * K);
     const bool tc = m.dtype == BASS_BF16 && m.gemm_mode != BASS_GEMM_SIMT && tc_gemm_supported(m, N, K);
     if (m.gemm_mode == BASS_GEMM_TC && !tc)
         throw Error(BASS_ERR_STATE, "tcgen05 GEMM requested but unsupported for this shape/dtype");
     if (tc) {
-        tc_gemm(m, mode, X, W, M, N, K, e);
+        // default: split-K clusters (gemm_tc.cu); BASS_GEMM_IMPL=sk: persistent stream-K (gemm_sk.cu)
+        static const bool skm = getenv("BASS_GEMM_IMPL") && std::string(getenv("BASS_GEMM_IMPL")) == "sk";
+        if (skm) sk_gemm(m, mode, X, W, M, N, K, e, packed);
+        else tc_gemm(m, mode, X, W, M, N, K, e, packed);
         return;
     }
 #define BASS_GEMM_CASE(MD)                                                            \
     case MD:                                                                          \
-        if (m.dtype == BASS_BF16) gemm_simt<MD, __nv_bfloat16>(m, X, W, M, N, K, e);  \
-        else gemm_simt<MD, float>(m, X, W, M, N, K, e);                               \
+        if (m.dtype == BASS_BF16) gemm_simt<MD, __nv_bfloat16>(m, X, W, M, N, K, e, packed); \
+        else gemm_simt<MD, float>(m, X, W, M, N, K, e, packed);                              \
         break;
     switch (mode) {
         BASS_GEMM_CASE(EPI_QKV)
@@ -251,7 +270,9 @@ static void launch_attention_t(bass_ctx* ctx, int strategy, const void* q, const
             ProfScope prof(ctx, BASS_PROF_ATTN, abytes, aflops);
             if (attn_stream_mode()) {
                 AttnPlan plan;
-                stream_attention_plan(ctx, strategy, q, M, n_slots, qn, off, H, cap, work_buf, plan);
+                std::vector<int32_t> ident(n_seq);
+                for (int i = 0; i < n_seq; ++i) ident[i] = i;   // standalone: sequence i uses K/V entry i
+                stream_attention_plan(ctx, strategy, q, M, n_slots, ident, qn, off, H, cap, work_buf, plan);
                 float* so = (float*)po.need((size_t)M * H * plan.mc * DH * 4, ctx->stream);
                 float* sml = (float*)pml.need((size_t)M * H * plan.mc * 2 * 4, ctx->stream);
                 stream_attention_run(ctx, plan, kc, vc, seqs_dev, so, sml, out);
@@ -402,7 +423,7 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
     float *pa_o = nullptr, *pa_ml = nullptr;
     if (m.dtype == BASS_BF16 && tc_attention_supported(BASS_BF16, dh)) {
         if (attn_stream_mode())
-            stream_attention_plan(ctx, strategy, q, M, kv.n_slots, b.qn, b.off, H, kv.cap, work_buf, plan);
+            stream_attention_plan(ctx, strategy, q, M, kv.n_slots, b.slot, b.qn, b.off, H, kv.cap, work_buf, plan);
         else
             tc_attention_plan(ctx, strategy, q, M, kv.n_slots, b.qn, b.off, H, kv.cap, work_buf, plan);
         pa_o = (float*)m.part_o.need((size_t)M * H * plan.mc * dh * 4, st);
@@ -423,7 +444,7 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
         e.row_slot = rows.slot;
         e.row_pos = rows.pos;
         e.d = d; e.dh = dh; e.H = H; e.cap = kv.cap;
-        gemm(m, EPI_QKV, h, L.wqkv, M, 3 * d, d, e);
+        gemm(m, EPI_QKV, h, L.wqkv, M, 3 * d, d, e, m.packed);
         if (plan.valid) {
             ProfScope prof(ctx, BASS_PROF_ATTN, attn_bytes, attn_flops);
             if (plan.stream) {
@@ -449,19 +470,19 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
         }
         Epi r{};
         r.x = x;
-        gemm(m, EPI_RESID, cx, L.wo, M, d, d, r);
+        gemm(m, EPI_RESID, cx, L.wo, M, d, d, r, m.packed);
         launch_layernorm_any(m, x, nullptr, L.ln2_g, L.ln2_b, M, h);
         Epi ge{};
         ge.out = f;
-        gemm(m, EPI_GELU, h, L.wfc, M, 4 * d, d, ge);
-        gemm(m, EPI_RESID, f, L.wproj, M, d, 4 * d, r);
+        gemm(m, EPI_GELU, h, L.wfc, M, 4 * d, d, ge, m.packed);
+        gemm(m, EPI_RESID, f, L.wproj, M, d, 4 * d, r, m.packed);
     }
     if (R > 0) {
         void* hs = m.hs.need((size_t)R * d * es, st);
         launch_layernorm_any(m, x, lrows, m.lnf_g, m.lnf_b, R, hs);
         Epi so{};
         so.out = logits_out;
-        gemm(m, EPI_STORE, hs, m.head, R, V, d, so);
+        gemm(m, EPI_STORE, hs, m.head, R, V, d, so, m.packed);
     }
 }
 
@@ -575,9 +596,11 @@ int bass_model_create(bass_ctx* c, const bass_geometry* g, int dtype, bass_model
         m->dtype = dtype;
         m->esize = dtype == BASS_BF16 ? 2 : 4;
         const int64_t d = g->d_model, V = g->vocab_size, S = g->max_seq_len, L = g->n_layer;
-        // row alignment of 16 bytes for every matrix (TMA requirement)
-        const int64_t per_layer = 3 * d * d + d * d + 4 * d * d + 4 * d * d;
-        const int64_t total = V * d + S * d + L * per_layer + V * d;
+        // bf16 GEMM weights live in the packed tile layout (rows padded to 128)
+        m->packed = dtype == BASS_BF16 && d % 64 == 0 && !(getenv("BASS_PACK") && atoi(getenv("BASS_PACK")) == 0);
+        auto rows = [&](int64_t N) { return m->packed ? packed_rows(N) : N; };
+        const int64_t per_layer = (rows(3 * d) + rows(d) + rows(4 * d)) * d + rows(d) * 4 * d;
+        const int64_t total = V * d + S * d + L * per_layer + rows(V) * d;
         m->weight_bytes = total * m->esize;
         BASS_CUDA(cudaMalloc(&m->wblob, (size_t)m->weight_bytes));
         const int64_t nf = L * 4 * d + 2 * d;
@@ -590,16 +613,16 @@ int bass_model_create(bass_ctx* c, const bass_geometry* g, int dtype, bass_model
         m->layers.resize(L);
         for (int i = 0; i < L; ++i) {
             bass_layer& ly = m->layers[i];
-            ly.wqkv = take(3 * d * d);
-            ly.wo = take(d * d);
-            ly.wfc = take(4 * d * d);
-            ly.wproj = take(4 * d * d);
+            ly.wqkv = take(rows(3 * d) * d);
+            ly.wo = take(rows(d) * d);
+            ly.wfc = take(rows(4 * d) * d);
+            ly.wproj = take(rows(d) * 4 * d);
             ly.ln1_g = fp; fp += d;
             ly.ln1_b = fp; fp += d;
             ly.ln2_g = fp; fp += d;
             ly.ln2_b = fp; fp += d;
         }
-        m->head = take(V * d);
+        m->head = take(rows(V) * d);
         m->lnf_g = fp; fp += d;
         m->lnf_b = fp; fp += d;
         // LN defaults (gain 1, bias 0) — ref:model.py:121-130
@@ -622,6 +645,7 @@ int bass_model_destroy(bass_model* m) {
     cudaSetDevice(m->ctx->device);
     cudaStreamSynchronize(m->ctx->stream);
     tc_release(*m);
+    sk_release(*m);
     cudaFree(m->wblob);
     cudaFree(m->fblob);
     for (DevBuf* b : {&m->x, &m->h, &m->q, &m->ctxb, &m->f, &m->hs, &m->meta, &m->part_o, &m->part_ml,
@@ -651,10 +675,10 @@ int bass_model_set_weight(bass_model* m, int tensor, int layer, const float* hos
             float* tmp = upload_tmp(K * N);
             dim3 grid((N + 31) / 32, (K + 31) / 32), blk(32, 8);
             if (m->dtype == BASS_BF16)
-                transpose_convert<<<grid, blk, 0, st>>>(tmp, (int)K, (int)N,
-                                                        (__nv_bfloat16*)dst + row_off * K, K);
+                transpose_convert<<<grid, blk, 0, st>>>(tmp, (int)K, (int)N, (__nv_bfloat16*)dst, K, row_off,
+                                                        m->packed);
             else
-                transpose_convert<<<grid, blk, 0, st>>>(tmp, (int)K, (int)N, (float*)dst + row_off * K, K);
+                transpose_convert<<<grid, blk, 0, st>>>(tmp, (int)K, (int)N, (float*)dst, K, row_off, false);
             BASS_CUDA(cudaGetLastError());
             BASS_CUDA(cudaFreeAsync(tmp, st));
         };
@@ -804,18 +828,27 @@ int bass_gemm_bench(bass_model* m, int mode, int M, int N, int K, const void* x,
                     int n_w, double* ms_per_launch) {
     return guarded(m->ctx, [&] {
         BASS_REQUIRE(reps >= 1, "reps must be >= 1");
+        const bool packed = mode == 3;   // tcgen05 on packed copies of the weights
+        if (packed) mode = BASS_GEMM_TC;
         const int saved = m->gemm_mode;
         m->gemm_mode = mode;
         Epi e{};
         e.out = y;
+        void* wp = nullptr;
+        if (packed) {
+            BASS_CUDA(cudaMalloc(&wp, (size_t)packed_rows(N) * K * 2 * n_w));
+            pack_weights(m->ctx->stream, w, wp, N, K, n_w);
+            w = wp;
+        }
         cudaEvent_t a, b;
         BASS_CUDA(cudaEventCreate(&a));
         BASS_CUDA(cudaEventCreate(&b));
         // launch i streams weight copy i % n_w (n_w copies > L2 defeat caching)
-        const size_t wbytes = (size_t)N * K * m->esize;
-        for (int i = 0; i < n_w; ++i) gemm(*m, EPI_STORE, x, (const char*)w + i * wbytes, M, N, K, e);   // warm
+        const size_t wbytes = (size_t)(packed ? packed_rows(N) : N) * K * m->esize;
+        for (int i = 0; i < n_w; ++i) gemm(*m, EPI_STORE, x, (const char*)w + i * wbytes, M, N, K, e, packed);   // warm
         BASS_CUDA(cudaEventRecord(a, m->ctx->stream));
-        for (int i = 0; i < reps; ++i) gemm(*m, EPI_STORE, x, (const char*)w + (i % n_w) * wbytes, M, N, K, e);
+        for (int i = 0; i < reps; ++i)
+            gemm(*m, EPI_STORE, x, (const char*)w + (i % n_w) * wbytes, M, N, K, e, packed);
         BASS_CUDA(cudaEventRecord(b, m->ctx->stream));
         m->gemm_mode = saved;
         m->ctx->sync();
@@ -824,6 +857,7 @@ int bass_gemm_bench(bass_model* m, int mode, int M, int N, int K, const void* x,
         *ms_per_launch = ms / reps;
         cudaEventDestroy(a);
         cudaEventDestroy(b);
+        if (wp) cudaFree(wp);
     });
 }
 
@@ -836,7 +870,7 @@ int bass_gemm(bass_model* m, int mode, int M, int N, int K, const void* x, const
         Epi e{};
         e.out = y;
         try {
-            gemm(*m, EPI_STORE, x, w, M, N, K, e);
+            gemm(*m, EPI_STORE, x, w, M, N, K, e, false);
         } catch (...) {
             m->gemm_mode = saved;
             throw;
@@ -874,6 +908,30 @@ int bass_attention(bass_ctx* c, int strategy, int dtype, int n_seq, int n_head, 
     });
 }
 
+int bass_trace_enable(bass_ctx* c, int64_t records) {
+    return guarded(c, [&] {
+        c->sync();
+        if (c->trace_buf) cudaFree(c->trace_buf);
+        c->trace_buf = nullptr;
+        c->trace_cap = c->trace_n = 0;
+        if (records > 0) {
+            BASS_CUDA(cudaMalloc((void**)&c->trace_buf, (size_t)records * 32));
+            BASS_CUDA(cudaMemset(c->trace_buf, 0, (size_t)records * 32));
+            c->trace_cap = records;
+        }
+    });
+}
+
+int bass_trace_read(bass_ctx* c, uint64_t* host, int64_t max_records, int64_t* n_out) {
+    return guarded(c, [&] {
+        c->sync();
+        const int64_t n = std::min<int64_t>(max_records, c->trace_n);
+        if (n > 0) BASS_CUDA(cudaMemcpy(host, c->trace_buf, (size_t)n * 32, cudaMemcpyDeviceToHost));
+        *n_out = n;
+        c->trace_n = 0;
+    });
+}
+
 int bass_attention_bench(bass_ctx* c, int strategy, int n_seq, int n_head, const int32_t* cu_q, const int32_t* offsets,
                          const void* q, const void* k, const void* v, int kv_stride, int n_kv, void* out, int reps,
                          double* ms_per_call) {
@@ -897,7 +955,7 @@ int bass_attention_bench(bass_ctx* c, int strategy, int n_seq, int n_head, const
         upload_i32(c, dm, hm.data(), hm.size());
         Seqs seqs{dm, dm + n_seq, dm + 2 * n_seq, dm + 3 * n_seq};
         AttnPlan plan;
-        stream_attention_plan(c, strategy, q, M, n_seq, qn, off, H, kv_stride, work, plan);
+        stream_attention_plan(c, strategy, q, M, n_seq, slot, qn, off, H, kv_stride, work, plan);
         float* so = (float*)po.need((size_t)M * H * plan.mc * 128 * 4, c->stream);
         float* sml = (float*)pml.need((size_t)M * H * plan.mc * 2 * 4, c->stream);
         const size_t kv_bytes = (size_t)n_seq * H * kv_stride * 128 * 2;

@@ -74,7 +74,19 @@ struct bass_ctx {
     cudaEvent_t ev();
     void resolve();
     void sync();
+    // timeline trace (bass_trace_enable): records of {t0, t1, smid, tag}
+    unsigned long long* trace_buf = nullptr;
+    long long trace_cap = 0, trace_n = 0;
+    int trace_seq = 0;
+    bass::TraceArg trace(int grid, int cls) {   // tag = kernel class | launch sequence << 4
+        if (!trace_buf || trace_n + grid > trace_cap) return bass::TraceArg{nullptr, 0, 0};
+        bass::TraceArg t{trace_buf, trace_n, cls | (trace_seq++ << 4)};
+        trace_n += grid;
+        return t;
+    }
 };
+// trace tags (kernel classes)
+enum { BASS_TR_GEMM = 1, BASS_TR_ATTN = 2, BASS_TR_NORM = 3, BASS_TR_COMBINE = 4 };
 
 namespace bass {
 // RAII timer around one launch (no-op unless ctx->profile)
@@ -110,6 +122,7 @@ struct bass_model {
     bass_geometry g{};
     int dtype = BASS_BF16;
     int gemm_mode = BASS_GEMM_AUTO;
+    bool packed = false;             // GEMM weights in the packed tile layout (bf16, d % 64 == 0)
     size_t esize = 2;
     void* wblob = nullptr;           // all matrices, one allocation
     float* fblob = nullptr;          // LN params
@@ -119,7 +132,8 @@ struct bass_model {
     std::vector<bass_layer> layers;
     // workspace (grown on demand)
     bass::DevBuf x, h, q, ctxb, f, hs, meta, part_o, part_ml, logits_tmp;
-    void* tc_state = nullptr;        // tcgen05 GEMM descriptors (gemm_tc.cu)
+    void* tc_state = nullptr;        // tcgen05 split-K GEMM descriptors (gemm_tc.cu)
+    void* sk_state = nullptr;        // stream-K GEMM descriptors / workspace (gemm_sk.cu)
 };
 
 struct bass_kv {
@@ -149,14 +163,21 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
              const int32_t* proposals, int pstride);
 
 // GEMM dispatch (SIMT or tcgen05) — Y = X W^T with a fused epilogue.
+// `packed`: W is in the packed tile layout (packed_index) — the model's own
+// weights; raw [N, K] pointers (bass_gemm) pass false.
 void gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K,
-          const Epi& e);
+          const Epi& e, bool packed);
 
 // tcgen05 GEMM (gemm_tc.cu); returns false when the shape is unsupported.
 bool tc_gemm_supported(const bass_model& m, int N, int K);
 void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K,
-             const Epi& e);
+             const Epi& e, bool packed);
 void tc_release(bass_model& m);
+// persistent stream-K tcgen05 GEMM (gemm_sk.cu): the default bf16 path
+void sk_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K, const Epi& e, bool packed);
+// pack n_mat contiguous [N, K] bf16 matrices into the packed layout (dst: n_mat * packed_rows(N) * K)
+void pack_weights(cudaStream_t st, const void* src, void* dst, int N, int K, int n_mat);
+void sk_release(bass_model& m);
 
 // tcgen05 attention (attn_tc.cu).  A plan (work list + Q tensor map) is
 // built once per forward and reused by every layer.
@@ -178,8 +199,8 @@ bool tc_attention_supported(int dtype, int dh);
 // streaming tcgen05 attention (attn_stream.cu): the default bf16 d_head=128 path
 int stream_split_len();
 void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, int n_slots,
-                           const std::vector<int32_t>& qn, const std::vector<int32_t>& off, int H, int cap,
-                           DevBuf& work_buf, AttnPlan& plan);
+                           const std::vector<int32_t>& slot, const std::vector<int32_t>& qn,
+                           const std::vector<int32_t>& off, int H, int cap, DevBuf& work_buf, AttnPlan& plan);
 void stream_attention_run(bass_ctx* ctx, const AttnPlan& plan, const void* kc, const void* vc, const Seqs& seqs_dev,
                           float* part_o, float* part_ml, void* out);
 void tc_attention(bass_ctx* ctx, int strategy, const void* q, int M, const void* kc, const void* vc, int n_slots,

@@ -19,7 +19,9 @@ SHAPES = {"qkv": (3 * d, d), "o": (d, d), "fc": (4 * d, d), "proj": (d, 4 * d), 
           "d_qkv": (3 * dd, dd), "d_o": (dd, dd), "d_fc": (4 * dd, dd), "d_proj": (dd, 4 * dd),
           "d_head": (V, dd)}
 Ms = [int(a) for a in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["8", "16", "88", "264"])]
-only = sys.argv[2].split(",") if len(sys.argv) > 2 else list(SHAPES)
+only = sys.argv[2].split(",") if len(sys.argv) > 2 and sys.argv[2] != "all" else list(SHAPES)
+# argv[3] == "packed": weights in the packed tile layout the model uses (mode 3 of bass_gemm_bench)
+gmode = 3 if len(sys.argv) > 3 and sys.argv[3] == "packed" else L.GEMM_TC
 reps = 40
 hbm = 6545.9
 handle = B.DeviceWeights(B.ModelConfig(1, 2, 128, 64, 256, 64), "bf16")
@@ -32,7 +34,7 @@ for name in only:
         x = torch.randn(M, K, device="cuda").bfloat16()
         y = torch.empty(M, N, device="cuda")
         ms = C.c_double()
-        ctx.check(ctx.lib.bass_gemm_bench(handle.handle, L.GEMM_TC, M, N, K, C.c_void_p(x.data_ptr()),
+        ctx.check(ctx.lib.bass_gemm_bench(handle.handle, gmode, M, N, K, C.c_void_p(x.data_ptr()),
                                           C.c_void_p(w.data_ptr()), C.c_void_p(y.data_ptr()), reps, n_w,
                                           C.byref(ms)))
         t = ms.value / 1e3

@@ -1,0 +1,107 @@
+"""Per-CTA timeline of one C2 speculative generation (bass_trace_enable):
+every GEMM / attention / LayerNorm CTA records {start, end, SM} with the
+globaltimer.  Prints per-class totals, the launch-to-launch gaps (negative =
+overlap via PDL) and one main-model layer's timeline.
+
+    python tools/trace_gen.py [out.npy]
+"""
+import ctypes as C
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2404_15778_b200 as B  # noqa: E402
+
+CLS = {1: "gemm", 2: "attn", 3: "norm", 4: "combine"}
+
+
+def main():
+    cfg = bench.CONFIGS["c2"]
+    ctx = B.CudaContext(0)
+    stream = torch.cuda.Stream()
+    ctx.set_stream(stream.cuda_stream)
+    wm = B.DeviceWeights.random(B.ModelConfig(*cfg["main"]), seed=1000, ctx=ctx)
+    wd = B.DeviceWeights.random(B.ModelConfig(*cfg["draft"]), seed=2000, ctx=ctx)
+    b, P, new = cfg["batch"], cfg["prompt"], cfg["new"]
+    cap = P + new + 40
+    main_m, draft_m = B.CudaModel(wm, b, "ragged", capacity=cap), B.CudaModel(wd, b, "ragged", capacity=cap)
+    eng = B.CudaEngine(main_m, draft_m)
+    prompts = [np.random.default_rng(1_000_003 + i).integers(0, 50272, P).tolist() for i in range(b)]
+    req = B.GenerationRequest(prompts, new, temperature=0.0, seed=1234, sequence_ids=list(range(b)))
+
+    def reset():
+        for m in (main_m, draft_m):
+            for s in range(b):
+                m.rollback(s, 0)
+
+    reset()
+    _, rd_arr, _ = eng.run(req, None, speculative=False)
+    for it in range(2):
+        reset()
+        if it == 1:
+            ctx.check(ctx.lib.bass_trace_enable(ctx.handle, 8 << 20))
+        res = eng.run(req, B.AdaptiveDraftController(B.DraftLengthParams()), speculative=True, align=0.874,
+                      align_seed=99, align_tokens=rd_arr["tokens"])
+    buf = np.zeros((8 << 20) * 4, np.uint64)
+    n = C.c_int64()
+    ctx.check(ctx.lib.bass_trace_read(ctx.handle, buf.ctypes.data_as(C.POINTER(C.c_uint64)), 8 << 20, C.byref(n)))
+    ctx.check(ctx.lib.bass_trace_enable(ctx.handle, 0))
+    rec = buf[: 4 * n.value].reshape(-1, 4).astype(np.int64)
+    if len(sys.argv) > 1:
+        np.save(sys.argv[1], rec)
+    analyse(rec)
+
+
+def analyse(rec):
+    rec = rec[rec[:, 0] > 0]
+    t0 = rec[:, 0].min()
+    seq = rec[:, 3] >> 4
+    order = np.argsort(seq, kind="stable")
+    rec, seq = rec[order], seq[order]
+    bounds = np.flatnonzero(np.diff(seq)) + 1
+    launches = []
+    for r in np.split(rec, bounds):
+        launches.append(dict(cls=CLS.get(int(r[0, 3] & 15), "?"), grid=len(r), s0=(r[:, 0].min() - t0) / 1e3,
+                             s1=(r[:, 0].max() - t0) / 1e3, e0=(r[:, 1].min() - t0) / 1e3,
+                             e1=(r[:, 1].max() - t0) / 1e3, sms=len(np.unique(r[:, 2])),
+                             maxper=int(np.bincount(r[:, 2]).max())))
+    total = launches[-1]["e1"] - launches[0]["s0"]
+    print(f"launches {len(launches)}  span {total / 1e3:.2f} ms")
+    by = {}
+    for i, l in enumerate(launches):
+        d = by.setdefault(l["cls"], [0, 0.0, 0.0, 0.0])
+        d[0] += 1
+        d[1] += l["e1"] - l["s0"]                      # launch span
+        d[2] += l["e1"] - l["s1"]                      # from last CTA start to last end
+        if i + 1 < len(launches):
+            d[3] += launches[i + 1]["s0"] - l["e1"]    # gap to next launch (negative = overlap)
+    for k, (cnt, span, tail, gap) in by.items():
+        print(f"{k:8s} n={cnt:6d} span={span / 1e3:8.2f} ms  avg={span / cnt:7.2f} us  avg_gap_after={gap / cnt:6.2f} us")
+    # layer periods: attention launches of the main (largest grid) and draft models
+    att = [l for l in launches if l["cls"] == "attn"]
+    gmax = max(l["grid"] for l in att)
+    for name, sel in (("main", [l for l in att if l["grid"] == gmax]), ("draft", [l for l in att if l["grid"] != gmax])):
+        d = np.diff([l["s0"] for l in sel])
+        d = d[d < 200]   # consecutive layers of one forward
+        if len(d):
+            print(f"{name} layer period: median {np.median(d):.1f} us  (n={len(d)})")
+    # a main-model layer in the middle
+    mid = next(i for i in range(len(launches) // 2, len(launches)) if launches[i]["cls"] == "attn" and launches[i]["grid"] == gmax)
+    print("\ntimeline around the middle (us, relative):")
+    base = launches[mid]["s0"]
+    for l in launches[mid: mid + 24]:
+        print(f"{l['cls']:8s} grid={l['grid']:4d} sms={l['sms']:3d} max/SM={l['maxper']}  start {l['s0'] - base:8.2f}..{l['s1'] - base:8.2f}"
+              f"  end {l['e0'] - base:8.2f}..{l['e1'] - base:8.2f}  span {l['e1'] - l['s0']:7.2f}")
+
+
+if __name__ == "__main__":
+    if len(sys.argv) > 2 and sys.argv[1] == "--load":
+        analyse(np.load(sys.argv[2]))
+    else:
+        main()
