@@ -222,10 +222,10 @@ void gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, i
     if (m.gemm_mode == BASS_GEMM_TC && !tc)
         throw Error(BASS_ERR_STATE, "tcgen05 GEMM requested but unsupported for this shape/dtype");
     if (tc) {
-        // default: split-K clusters (gemm_tc.cu); BASS_GEMM_IMPL=sk: persistent stream-K (gemm_sk.cu)
-        static const bool skm = getenv("BASS_GEMM_IMPL") && std::string(getenv("BASS_GEMM_IMPL")) == "sk";
-        if (skm) sk_gemm(m, mode, X, W, M, N, K, e, packed);
-        else tc_gemm(m, mode, X, W, M, N, K, e, packed);
+        // split-K clusters (gemm_tc.cu).  Persistent alternatives were measured
+        // slower inside the PDL chain (static stream-K: staggered SM release;
+        // dynamic k-chunks: per-chunk reduction latency) — DESIGN.md section 4
+        tc_gemm(m, mode, X, W, M, N, K, e, packed);
         return;
     }
 #define BASS_GEMM_CASE(MD)                                                            \
@@ -408,15 +408,6 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
     void* f = m.f.need((size_t)M * 4 * d * es, st);
     static DevBuf work_buf;   // per-process attention work list (tiny)
 
-    if (m.dtype == BASS_BF16)
-        BASS_CUDA(launch_pdl(embed_kernel<__nv_bfloat16>, dim3(M), dim3(128), 0, st,
-                             (const __nv_bfloat16*)m.tok_emb, (const __nv_bfloat16*)m.pos_emb, rows, proposals,
-                             pstride, d, x));
-    else
-        BASS_CUDA(launch_pdl(embed_kernel<float>, dim3(M), dim3(128), 0, st, (const float*)m.tok_emb,
-                             (const float*)m.pos_emb, rows, proposals, pstride, d, x));
-    check_launch(ctx);
-
     // tcgen05 attention: one plan (work list, Q map) for all layers of this forward
     AttnPlan plan;
     double attn_bytes = 0.0, attn_flops = 0.0;
@@ -434,21 +425,12 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
         }
     }
 
-    for (int li = 0; li < g.n_layer; ++li) {
-        const bass_layer& L = m.layers[li];
-        launch_layernorm_any(m, x, nullptr, L.ln1_g, L.ln1_b, M, h);
-        Epi e{};
-        e.out = q;
-        e.kc = (char*)kv.k + li * kv.layer_elems() * es;
-        e.vc = (char*)kv.v + li * kv.layer_elems() * es;
-        e.row_slot = rows.slot;
-        e.row_pos = rows.pos;
-        e.d = d; e.dh = dh; e.H = H; e.cap = kv.cap;
-        gemm(m, EPI_QKV, h, L.wqkv, M, 3 * d, d, e, m.packed);
+    // layer li's attention (its Q from the QKV projection; K/V rows appended there)
+    auto run_attention = [&](int li, void* kc, void* vc) {
         if (plan.valid) {
             ProfScope prof(ctx, BASS_PROF_ATTN, attn_bytes, attn_flops);
             if (plan.stream) {
-                stream_attention_run(ctx, plan, e.kc, e.vc, seqs, pa_o, pa_ml, cx);
+                stream_attention_run(ctx, plan, kc, vc, seqs, pa_o, pa_ml, cx);
                 if (plan.needs_combine) {
                     BASS_CUDA(launch_pdl(attn_combine_kernel<__nv_bfloat16, 128>, dim3(M, H), dim3(128), 0, st,
                                          (const float*)pa_o, (const float*)pa_ml, rows.pos, H, plan.mc,
@@ -456,7 +438,7 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
                     check_launch(ctx);
                 }
             } else {
-                tc_attention_run(ctx, plan, e.kc, e.vc, seqs, pa_o, pa_ml, cx);
+                tc_attention_run(ctx, plan, kc, vc, seqs, pa_o, pa_ml, cx);
                 if (!plan.fused) {
                     BASS_CUDA(launch_pdl(attn_combine_kernel<__nv_bfloat16, 128>, dim3(M, H), dim3(128), 0, st,
                                          (const float*)pa_o, (const float*)pa_ml, rows.pos, H, plan.mc, 128,
@@ -465,23 +447,110 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
                 }
             }
         } else {
-            launch_attention(ctx, m.dtype, dh, strategy, q, e.kc, e.vc, seqs, b.qn, b.off, rows.pos, M, H, kv.cap,
+            launch_attention(ctx, m.dtype, dh, strategy, q, kc, vc, seqs, b.qn, b.off, rows.pos, M, H, kv.cap,
                              kv.n_slots, work_buf, m.part_o, m.part_ml, cx);
         }
-        Epi r{};
-        r.x = x;
+        (void)li;
+    };
+    auto kc_of = [&](int li) { return (void*)((char*)kv.k + li * kv.layer_elems() * es); };
+    auto vc_of = [&](int li) { return (void*)((char*)kv.v + li * kv.layer_elems() * es); };
+    auto qkv_epi = [&](int li) {
+        Epi e{};
+        e.out = q;
+        e.kc = kc_of(li);
+        e.vc = vc_of(li);
+        e.row_slot = rows.slot;
+        e.row_pos = rows.pos;
+        e.d = d; e.dh = dh; e.H = H; e.cap = kv.cap;
+        return e;
+    };
+    Epi r{};
+    r.x = x;
+    Epi ge{};
+    ge.out = f;
+    Epi so{};
+    so.out = logits_out;
+    void* hs = R > 0 ? m.hs.need((size_t)R * d * es, st) : nullptr;
+
+    if (mega_supported(m)) {
+        // layer megakernels: [LN1, QKV]_0, attn_0, [O, LN2, FC, proj, LN1, QKV]_1, attn_1, ...,
+        // [O, LN2, FC, proj, LN_f, head]
+        auto ln = [&](const float* g_, const float* b_, const int32_t* gather, void* out, int rows_) {
+            MegaPhase p;
+            p.gemm = false;
+            p.x = x; p.gather = gather; p.g = g_; p.b = b_; p.out = out; p.rows = rows_; p.d = d;
+            return p;
+        };
+        auto mm = [&](const void* X, const void* W, int mode, int Mr, int N, int K, const Epi& e) {
+            MegaPhase p;
+            p.X = X; p.W = W; p.mode = mode; p.M = Mr; p.N = N; p.K = K; p.e = e;
+            return p;
+        };
+        std::vector<MegaLaunch> launches(g.n_layer + 1);
+        std::vector<double> lbytes(g.n_layer + 1, 0.0);
+        auto add = [&](int l, const MegaPhase& p) {
+            launches[l].phases.push_back(p);
+            launches[l].M_tile = M;
+            lbytes[l] += p.gemm ? gemm_bytes(m, p.mode, p.M, p.N, p.K) : (double)p.rows * d * (4.0 + es);
+        };
+        add(0, ln(m.layers[0].ln1_g, m.layers[0].ln1_b, nullptr, h, M));
+        add(0, mm(h, m.layers[0].wqkv, EPI_QKV, M, 3 * d, d, qkv_epi(0)));
+        for (int li = 0; li < g.n_layer; ++li) {
+            const bass_layer& L = m.layers[li];
+            add(li + 1, mm(cx, L.wo, EPI_RESID, M, d, d, r));
+            add(li + 1, ln(L.ln2_g, L.ln2_b, nullptr, h, M));
+            add(li + 1, mm(h, L.wfc, EPI_GELU, M, 4 * d, d, ge));
+            add(li + 1, mm(f, L.wproj, EPI_RESID, M, d, 4 * d, r));
+            if (li + 1 < g.n_layer) {
+                add(li + 1, ln(m.layers[li + 1].ln1_g, m.layers[li + 1].ln1_b, nullptr, h, M));
+                add(li + 1, mm(h, m.layers[li + 1].wqkv, EPI_QKV, M, 3 * d, d, qkv_epi(li + 1)));
+            } else if (R > 0) {
+                add(li + 1, ln(m.lnf_g, m.lnf_b, lrows, hs, R));
+                add(li + 1, mm(hs, m.head, EPI_STORE, R, V, d, so));
+            }
+        }
+        mega_prepare(m, launches);   // one descriptor upload, before the forward's first kernel
+        if (m.dtype == BASS_BF16)
+            BASS_CUDA(launch_pdl(embed_kernel<__nv_bfloat16>, dim3(M), dim3(128), 0, st,
+                                 (const __nv_bfloat16*)m.tok_emb, (const __nv_bfloat16*)m.pos_emb, rows, proposals,
+                                 pstride, d, x));
+        else
+            BASS_CUDA(launch_pdl(embed_kernel<float>, dim3(M), dim3(128), 0, st, (const float*)m.tok_emb,
+                                 (const float*)m.pos_emb, rows, proposals, pstride, d, x));
+        check_launch(ctx);
+        {
+            ProfScope prof(ctx, BASS_PROF_GEMM, lbytes[0]);
+            mega_launch(m, 0);
+        }
+        for (int li = 0; li < g.n_layer; ++li) {
+            run_attention(li, kc_of(li), vc_of(li));
+            ProfScope prof(ctx, BASS_PROF_GEMM, lbytes[li + 1]);
+            mega_launch(m, li + 1);
+        }
+        return;
+    }
+
+    if (m.dtype == BASS_BF16)
+        BASS_CUDA(launch_pdl(embed_kernel<__nv_bfloat16>, dim3(M), dim3(128), 0, st,
+                             (const __nv_bfloat16*)m.tok_emb, (const __nv_bfloat16*)m.pos_emb, rows, proposals,
+                             pstride, d, x));
+    else
+        BASS_CUDA(launch_pdl(embed_kernel<float>, dim3(M), dim3(128), 0, st, (const float*)m.tok_emb,
+                             (const float*)m.pos_emb, rows, proposals, pstride, d, x));
+    check_launch(ctx);
+
+    for (int li = 0; li < g.n_layer; ++li) {
+        const bass_layer& L = m.layers[li];
+        launch_layernorm_any(m, x, nullptr, L.ln1_g, L.ln1_b, M, h);
+        gemm(m, EPI_QKV, h, L.wqkv, M, 3 * d, d, qkv_epi(li), m.packed);
+        run_attention(li, kc_of(li), vc_of(li));
         gemm(m, EPI_RESID, cx, L.wo, M, d, d, r, m.packed);
         launch_layernorm_any(m, x, nullptr, L.ln2_g, L.ln2_b, M, h);
-        Epi ge{};
-        ge.out = f;
         gemm(m, EPI_GELU, h, L.wfc, M, 4 * d, d, ge, m.packed);
         gemm(m, EPI_RESID, f, L.wproj, M, d, 4 * d, r, m.packed);
     }
     if (R > 0) {
-        void* hs = m.hs.need((size_t)R * d * es, st);
         launch_layernorm_any(m, x, lrows, m.lnf_g, m.lnf_b, R, hs);
-        Epi so{};
-        so.out = logits_out;
         gemm(m, EPI_STORE, hs, m.head, R, V, d, so, m.packed);
     }
 }
@@ -645,7 +714,7 @@ int bass_model_destroy(bass_model* m) {
     cudaSetDevice(m->ctx->device);
     cudaStreamSynchronize(m->ctx->stream);
     tc_release(*m);
-    sk_release(*m);
+    mega_release(*m);
     cudaFree(m->wblob);
     cudaFree(m->fblob);
     for (DevBuf* b : {&m->x, &m->h, &m->q, &m->ctxb, &m->f, &m->hs, &m->meta, &m->part_o, &m->part_ml,

@@ -86,7 +86,7 @@ struct bass_ctx {
     }
 };
 // trace tags (kernel classes)
-enum { BASS_TR_GEMM = 1, BASS_TR_ATTN = 2, BASS_TR_NORM = 3, BASS_TR_COMBINE = 4 };
+enum { BASS_TR_GEMM = 1, BASS_TR_ATTN = 2, BASS_TR_NORM = 3, BASS_TR_COMBINE = 4, BASS_TR_MEGA = 5 };
 
 namespace bass {
 // RAII timer around one launch (no-op unless ctx->profile)
@@ -133,7 +133,7 @@ struct bass_model {
     // workspace (grown on demand)
     bass::DevBuf x, h, q, ctxb, f, hs, meta, part_o, part_ml, logits_tmp;
     void* tc_state = nullptr;        // tcgen05 split-K GEMM descriptors (gemm_tc.cu)
-    void* sk_state = nullptr;        // stream-K GEMM descriptors / workspace (gemm_sk.cu)
+    void* mega_state = nullptr;      // layer megakernel descriptors / workspace (layer_mega.cu)
 };
 
 struct bass_kv {
@@ -173,11 +173,34 @@ bool tc_gemm_supported(const bass_model& m, int N, int K);
 void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K,
              const Epi& e, bool packed);
 void tc_release(bass_model& m);
-// persistent stream-K tcgen05 GEMM (gemm_sk.cu): the default bf16 path
-void sk_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K, const Epi& e, bool packed);
 // pack n_mat contiguous [N, K] bf16 matrices into the packed layout (dst: n_mat * packed_rows(N) * K)
 void pack_weights(cudaStream_t st, const void* src, void* dst, int N, int K, int n_mat);
-void sk_release(bass_model& m);
+
+// layer megakernel (layer_mega.cu): GEMM (packed weights, fused epilogue) and
+// LayerNorm phases of one launch, separated by grid barriers
+struct MegaPhase {
+    bool gemm = true;
+    // GEMM: Y[M, N] = X[M, K] W^T -> epilogue `mode`
+    const void* X = nullptr;
+    const void* W = nullptr;
+    int mode = 0, M = 0, N = 0, K = 0;
+    Epi e{};
+    // LayerNorm: out[r] = LN(x[gather ? gather[r] : r]) (bf16), r < rows
+    const float* x = nullptr;
+    const int32_t* gather = nullptr;
+    const float* g = nullptr;
+    const float* b = nullptr;
+    void* out = nullptr;
+    int rows = 0, d = 0;
+};
+struct MegaLaunch {
+    std::vector<MegaPhase> phases;
+    int M_tile = 0;   // largest row count of the launch (token tile)
+};
+bool mega_supported(const bass_model& m);
+void mega_prepare(bass_model& m, const std::vector<MegaLaunch>& launches);
+void mega_launch(bass_model& m, int idx);
+void mega_release(bass_model& m);
 
 // tcgen05 attention (attn_tc.cu).  A plan (work list + Q tensor map) is
 // built once per forward and reused by every layer.

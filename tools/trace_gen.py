@@ -18,7 +18,7 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 import paper_2404_15778_b200 as B  # noqa: E402
 
-CLS = {1: "gemm", 2: "attn", 3: "norm", 4: "combine"}
+CLS = {1: "gemm", 2: "attn", 3: "norm", 4: "combine", 5: "mega"}
 
 
 def main():
@@ -58,8 +58,45 @@ def main():
     analyse(rec)
 
 
+def analyse_mega(rec, t0):
+    """Per-phase view of the layer megakernels: producer X-ready, epilogue done,
+    barrier release (us from the launch's first CTA start)."""
+    tag = rec[:, 3]
+    kern = rec[(tag & 15) == 5]
+    ph = rec[(tag & 15) == 13]
+    if not len(kern):
+        return
+    kseq = kern[:, 3] >> 4
+    pseq = (ph[:, 3] >> 4) & ((1 << 36) - 1)
+    pidx = ph[:, 3] >> 40
+    seqs = np.unique(kseq)
+    rows = []
+    for sq in seqs:
+        k = kern[kseq == sq]
+        s0 = k[:, 0].min()
+        P = ph[pseq == sq]
+        phases = []
+        for p in np.unique(P[:, 3] >> 40):
+            r = P[(P[:, 3] >> 40) == p]
+            rdy = r[:, 2][r[:, 2] > 0]
+            phases.append(((r[:, 0].min() - s0) / 1e3, (r[:, 0].max() - s0) / 1e3, (r[:, 1].max() - s0) / 1e3,
+                           ((rdy.min() - s0) / 1e3) if len(rdy) else -1, ((rdy.max() - s0) / 1e3) if len(rdy) else -1))
+        rows.append(((k[:, 0].max() - s0) / 1e3, (k[:, 1].max() - s0) / 1e3, phases))
+    by = {}
+    for r in rows:
+        by.setdefault(len(r[2]), []).append(r)
+    for n, rs in sorted(by.items()):
+        print(f"\nmega launches with {n} phases: {len(rs)}; median span {np.median([r[1] for r in rs]):.1f} us")
+        mid = rs[len(rs) // 2]
+        print(f"  example: CTA starts spread {mid[0]:.1f} us, end {mid[1]:.1f} us")
+        for i, (d0, d1, rel, r0, r1) in enumerate(mid[2]):
+            print(f"  phase {i}: x-ready {r0:7.1f}..{r1:7.1f}  done {d0:7.1f}..{d1:7.1f}  released {rel:7.1f}")
+
+
 def analyse(rec):
     rec = rec[rec[:, 0] > 0]
+    analyse_mega(rec, rec[:, 0].min())
+    rec = rec[(rec[:, 3] & 15) != 13]
     t0 = rec[:, 0].min()
     seq = rec[:, 3] >> 4
     order = np.argsort(seq, kind="stable")
@@ -71,6 +108,11 @@ def analyse(rec):
                              s1=(r[:, 0].max() - t0) / 1e3, e0=(r[:, 1].min() - t0) / 1e3,
                              e1=(r[:, 1].max() - t0) / 1e3, sms=len(np.unique(r[:, 2])),
                              maxper=int(np.bincount(r[:, 2]).max())))
+    if os.environ.get("TRACE_CSV"):
+        with open(os.environ["TRACE_CSV"], "w") as fh:
+            fh.write("cls,grid,s0,s1,e0,e1,sms,maxper\n")
+            for l in launches:
+                fh.write(f"{l['cls']},{l['grid']},{l['s0']:.2f},{l['s1']:.2f},{l['e0']:.2f},{l['e1']:.2f},{l['sms']},{l['maxper']}\n")
     total = launches[-1]["e1"] - launches[0]["s0"]
     print(f"launches {len(launches)}  span {total / 1e3:.2f} ms")
     by = {}
@@ -85,6 +127,8 @@ def analyse(rec):
         print(f"{k:8s} n={cnt:6d} span={span / 1e3:8.2f} ms  avg={span / cnt:7.2f} us  avg_gap_after={gap / cnt:6.2f} us")
     # layer periods: attention launches of the main (largest grid) and draft models
     att = [l for l in launches if l["cls"] == "attn"]
+    if not att:
+        return
     gmax = max(l["grid"] for l in att)
     for name, sel in (("main", [l for l in att if l["grid"] == gmax]), ("draft", [l for l in att if l["grid"] != gmax])):
         d = np.diff([l["s0"] for l in sel])
