@@ -262,11 +262,76 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
                 }
             }
         }
+    } else if ((size_t)rows * NB * BN * 4 <= (size_t)C::STAGES * C::STAGE) {
+        // split-K through distributed shared memory: the S CTAs of this tile
+        // are one cluster.  Each parks its fp32 partial [token][row] in its own
+        // (now idle) stage ring, the cluster barrier publishes it, and CTA
+        // `split` reduces token rows [split*R/S, (split+1)*R/S) reading every
+        // rank's partial over DSMEM, in fixed split order (same arithmetic as
+        // the L2 path below).
+        constexpr int WR = NB * BN;
+        float* part = reinterpret_cast<float*>(smem);
+#pragma unroll
+        for (int sub = 0; sub < NB; ++sub) {
+            const int nn = sub * BN + warp * 32 + lane;
+#pragma unroll 1
+            for (int c0 = 0; c0 < TT; c0 += 16) {
+                if (c0 >= rows) break;
+                float v[16];
+                tmem_ld16(trow + sub * TT + c0, v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (c0 + j < rows) part[(c0 + j) * WR + nn] = v[j];
+            }
+        }
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        const int r0 = split * rows / sp.S, r1 = (split + 1) * rows / sp.S;
+        const uint32_t part_s = su32(part);
+#pragma unroll
+        for (int sub = 0; sub < NB; ++sub) {
+            const int nn = sub * BN + warp * 32 + lane, n = n0 + nn;
+            if (n < N) {
+                int r = r0;
+                for (; r + 4 <= r1; r += 4) {   // 4 rows x S partials in flight
+                    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                    for (int s = 0; s < sp.S; ++s) {
+                        float p[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            uint32_t ra;
+                            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                                         : "=r"(ra)
+                                         : "r"(part_s + (uint32_t)(((r + u) * WR + nn) * 4)), "r"(s));
+                            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(p[u]) : "r"(ra) : "memory");
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) acc[u] += p[u];
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) epilogue<MODE, __nv_bfloat16>(e, m0 + r + u, n, N, acc[u]);
+                }
+                for (; r < r1; ++r) {
+                    float acc = 0.f;
+                    for (int s = 0; s < sp.S; ++s) {
+                        uint32_t ra;
+                        float pv;
+                        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                                     : "=r"(ra)
+                                     : "r"(part_s + (uint32_t)((r * WR + nn) * 4)), "r"(s));
+                        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(pv) : "r"(ra) : "memory");
+                        acc += pv;
+                    }
+                    epilogue<MODE, __nv_bfloat16>(e, m0 + r, n, N, acc);
+                }
+            }
+        }
+        // no CTA may leave (and free its shared memory) while others still read it
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     } else {
-        // split-K: the S CTAs of this tile are one thread-block cluster.  Each
-        // writes its fp32 partial tile (L2-resident scratch), the cluster
-        // barrier publishes them, and CTA `split` reduces token rows
-        // [split*R/S, (split+1)*R/S) of the tile in fixed split order.
+        // split-K through L2: the S CTAs of this tile are one thread-block
+        // cluster.  Each writes its fp32 partial tile (L2-resident scratch),
+        // the cluster barrier publishes them, and CTA `split` reduces token
+        // rows [split*R/S, (split+1)*R/S) of the tile in fixed split order.
         constexpr int WR = NB * BN;   // partial row width
         float* blk = sp.ws + (int64_t)(tile * gridDim.z + group) * sp.S * TT * WR;
 #pragma unroll
@@ -458,8 +523,8 @@ bool tc_gemm_supported(const bass_model& m, int N, int K) {
 void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K, const Epi& e, bool packed) {
     using namespace tc;
     State& S = state(m);
-    // token tile: smallest of 16/32/64/128/256 covering M (groups of 256 beyond)
-    const int TT = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
+    // token tile: smallest of 16/32/64/128/160/192/256 covering M (groups of 256 beyond)
+    const int TT = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : M <= 160 ? 160 : M <= 192 ? 192 : 256;
     // NB = 2: 256-row CTA tiles (two accumulators sharing each X tile)
     static const int nb_env = getenv("BASS_GEMM_NB") ? atoi(getenv("BASS_GEMM_NB")) : 0;
     // (measured: NB = 1 wins at every benchmark shape, profiles/r1_gemm_nb_split_sweep.txt)
@@ -490,6 +555,8 @@ void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N
         case 32: launch_nb<32>(m, mode, packed, NB, a, e); break;
         case 64: launch_nb<64>(m, mode, packed, NB, a, e); break;
         case 128: launch_nb<128>(m, mode, packed, NB, a, e); break;
+        case 160: launch_nb<160>(m, mode, packed, NB, a, e); break;
+        case 192: launch_nb<192>(m, mode, packed, NB, a, e); break;
         default: launch_nb<256>(m, mode, packed, NB, a, e); break;
     }
     m.ctx->launches++;
