@@ -144,7 +144,7 @@ def run_reference_arm(args, cfg):
     # acceptance regime of the GPU arm's harness: alignment a -> expected
     # tokens/step with k = Alg.1's steady state; use the closed form
     # (ref perf.py:149-159) at the default l0 = 7 for a bounded run
-    a, k = args.align, 7
+    a, k = max(args.align, 0.0), 7   # natural acceptance of a random-init draft ~ 0
     tps_step = (1 - a ** (k + 1)) / (1 - a) if a < 1 else k + 1.0
     # each step is one bounded sample (~10-30 s of host work); no warm-up
     # is needed for the CPU port, W is accepted for the interface only
@@ -171,7 +171,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--align", type=float, default=0.874)
+    ap.add_argument("--align", type=float, default=None,
+                    help="keyed-override acceptance (greedy configs; default 0.874). Sampled configs run the "
+                         "natural acceptance: an overridden proposal may have zero draft probability")
     ap.add_argument("--strategy", default="ragged", choices=["pad", "split", "ragged"])
     ap.add_argument("--gemm", default="auto", choices=["auto", "simt", "tc"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -182,6 +184,10 @@ def main():
                     help="per-kernel CUDA-event timing inside the timed region (0: off)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.align is None:
+        args.align = 0.874 if cfg["temperature"] == 0.0 else -1.0
+    if cfg["temperature"] > 0.0 and args.align >= 0.0:
+        raise SystemExit("--align is for greedy configs: sampled acceptance needs proposals drawn from the draft")
     if args.impl == "reference":
         run_reference_arm(args, cfg)
         return
@@ -324,9 +330,11 @@ def main():
     step_b_ms = dev_s / args.steps * 1e3 * gens_b   # pass-A device time for as many generations
     traffic = None
     tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    traffic_src = None
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+            tj = json.load(open(tp))
+            traffic, traffic_src = tj.get("dram_bytes_per_launch"), tj.get("shape")
         except Exception:
             traffic = None
     step_ms = dev_s / args.steps * 1e3
@@ -340,7 +348,8 @@ def main():
         "dtype": "bf16", "data": "synthetic (random-init weights, uniform prompt ids)",
         "config": {"workload": cfg["workload"], "batch_per_gpu": b, "global_batch": b * world,
                    "prompt_len": P, "max_new_tokens": new, "step": "one full generation",
-                   "draft_harness": f"keyed override, align={args.align}",
+                   "draft_harness": (f"keyed override, align={args.align}" if args.align >= 0
+                                     else "natural acceptance (draft samples its own proposals)"),
                    "strategy": args.strategy, "gemm": args.gemm,
                    "l2": "weights (17 GB/replica) >> L2; no flush needed",
                    "parallelism": f"seq-sharded replicas x{world}"},
@@ -359,12 +368,12 @@ def main():
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": "gemm_tc_kernel (tcgen05 weight streaming)",
                      "achieved": gemm_gbs, "peak": hbm, "unit": "GB/s", "frac": gemm_gbs / hbm,
-                     "traffic": traffic, "peak_kind": peak_kind,
+                     "traffic": traffic, "traffic_launch": traffic_src, "peak_kind": peak_kind,
                      "launches_per_generation": g["launches"] / gens_b,
                      "share_of_step": g["ms"] / step_b_ms if step_b_ms else None,
                      "note": "CUDA-event time per launch from an instrumented repeat of the timed "
                              "generations (events between kernels disable PDL overlap)"},
-        "attention_roofline": {"kernel": "attn_tc_kernel + combine", "achieved": attn_gbs, "peak": hbm,
+        "attention_roofline": {"kernel": "attn_stream_kernel (+ split combine)", "achieved": attn_gbs, "peak": hbm,
                                "unit": "GB/s", "frac": attn_gbs / hbm,
                                "launches_per_generation": a["launches"] / gens_b,
                                "share_of_step": a["ms"] / step_b_ms if step_b_ms else None},

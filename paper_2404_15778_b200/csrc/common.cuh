@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <utility>
 
 #define BASS_DEV __device__ __forceinline__
@@ -57,7 +58,8 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    static const bool pdl = !(getenv("BASS_PDL") && atoi(getenv("BASS_PDL")) == 0);   // BASS_PDL=0: debug
+    at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
@@ -184,8 +186,11 @@ BASS_DEV ArgMax block_argmax(ArgMax a, float* sv, int* si) {
 
 // Exclusive block scan of one value per thread (fixed order).  `scratch`
 // holds 33 elements.  Returns the exclusive prefix; *total = sum.
+// Not inlined: inlined into the sampled-verify kernel, nvcc 12.9 derived the
+// warp slot of `scratch[w]` as (tid >> 3) without the low-bit mask — a
+// misaligned shared store (compute-sanitizer, C3 sampled config).
 template <typename T>
-BASS_DEV T block_exclusive_scan(T v, T* scratch, T* total) {
+__device__ __noinline__ T block_exclusive_scan(T v, T* scratch, T* total) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     T incl = v;
 #pragma unroll
