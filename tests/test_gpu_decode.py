@@ -335,3 +335,66 @@ def test_fused_and_split_attention_bitwise_equal(tmp_path):
     # the streaming (online-softmax) kernel differs only in rounding
     err = np.abs(outs[2] - outs[0]).max(axis=1) / np.abs(outs[0]).max(axis=1)
     assert float(err.max()) < 1e-2, float(err.max())
+
+
+_MEGA_PROBE = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2404_15778_b200 as B
+from oracle import ragged as OR
+g = OR.Geometry(3, 4, 512, 128, 1500, 600)
+dw = B.DeviceWeights.from_reference(OR.init_weights(g, 51), "bf16")
+dd = B.DeviceWeights.from_reference(OR.init_weights(OR.Geometry(1, 4, 512, 128, 1500, 600), 52), "bf16")
+rng = np.random.default_rng(8)
+prompts = [rng.integers(0, 1500, n).tolist() for n in (40, 9, 70, 25)]
+m = B.CudaModel(dw, 4)
+for s, p in enumerate(prompts):
+    m.prefill(s, p)
+out = m.forward([0, 1, 2, 3], [rng.integers(0, 1500, n).tolist() for n in (5, 1, 12, 3)])
+np.save(sys.argv[2], np.concatenate(out))
+req = B.GenerationRequest(prompts, 24, temperature=0.0)
+base = B.decode_regular(B.CudaModel(dw, 4), req)
+spec = B.decode_speculative(B.CudaModel(dw, 4), B.CudaModel(dd, 4), req, B.AdaptiveDraftController())
+assert spec.tokens == base.tokens, "mega: greedy speculative != regular"
+print("ok")
+"""
+
+
+def test_layer_megakernel_matches_per_kernel_path(tmp_path):
+    """BASS_MEGA=1 (persistent O->LN2->FC->proj->LN1->QKV launches with grid
+    barriers) gives logits within 1e-2 of the default per-kernel path and
+    keeps greedy speculative == regular."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    probe = tmp_path / "probe.py"
+    probe.write_text(_MEGA_PROBE)
+    outs = []
+    for env_extra in ({"BASS_MEGA": "0"}, {"BASS_MEGA": "1"}):
+        path = tmp_path / f"out{len(outs)}.npy"
+        env = dict(os.environ, **env_extra)
+        subprocess.run([sys.executable, str(probe), root, str(path)], check=True, env=env, timeout=300)
+        outs.append(np.load(path))
+    err = np.abs(outs[1] - outs[0]).max(axis=1) / np.abs(outs[0]).max(axis=1)
+    assert float(err.max()) < 1e-2, float(err.max())
+
+
+def test_timeline_trace_records_every_cta(B):
+    """bass_trace_enable / bass_trace_read: one record per CTA of every traced
+    launch, with ordered timestamps and valid SM ids."""
+    import ctypes as C
+    w = _bf16_round(OR.init_weights(OR.Geometry(2, 4, 512, 128, 1500, 600), 61))
+    m = B.CudaModel(B.DeviceWeights.from_reference(w, "bf16"), 2)
+    ctx = m.ctx
+    ctx.check(ctx.lib.bass_trace_enable(ctx.handle, 1 << 16))
+    m.prefill(0, list(range(1, 30)))
+    buf = np.zeros((1 << 16) * 4, np.uint64)
+    n = C.c_int64()
+    ctx.check(ctx.lib.bass_trace_read(ctx.handle, buf.ctypes.data_as(C.POINTER(C.c_uint64)), 1 << 16, C.byref(n)))
+    ctx.check(ctx.lib.bass_trace_enable(ctx.handle, 0))
+    rec = buf[: 4 * n.value].reshape(-1, 4).astype(np.int64)
+    assert n.value > 0
+    assert (rec[:, 1] >= rec[:, 0]).all() and (rec[:, 0] > 0).all()
+    assert (rec[:, 2] < 1024).all()
+    classes = set((rec[:, 3] & 15).tolist())
+    assert {1, 2, 3} <= classes   # GEMM, attention, LayerNorm
