@@ -75,7 +75,7 @@ struct Cfg {
     static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
     // full[S] empty[S] acc_full[2] acc_empty[2] xready
     static constexpr int NBAR = 2 * STAGES + 5;
-    static constexpr int SMEM = STAGES * STAGE + 1024 + NBAR * 8 + 16 + 64 * 4 + 16 * 8;
+    static constexpr int SMEM = STAGES * STAGE + 1024 + NBAR * 8 + 16 + 64 * 4 + 32 * 8;
     static constexpr int TMEM_COLS = 2 * TT <= 32 ? 32 : 2 * TT <= 64 ? 64 : 2 * TT <= 128 ? 128 : 2 * TT <= 256 ? 256 : 512;
 };
 
@@ -121,17 +121,15 @@ struct SegIter {
     }
 };
 
-// grid-wide barrier (one thread per CTA): bar[0] arrivals, bar[1] generation
+// grid-wide barrier (one thread per CTA, after a CTA-level barrier): the
+// arrival counter only grows — barrier number `gen` completes when it reaches
+// (gen + 1) * G — so one release-add per CTA and acquire polling suffice
+// (no reset, no last-arriver flag round trip).
 __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned G, unsigned gen) {
-    __threadfence();
-    const unsigned prev = atomicAdd(&bar[0], 1u);
-    if (prev == G - 1) {
-        atomicExch(&bar[0], 0u);
-        __threadfence();
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(gen + 1) : "memory");
-    } else {
-        while (ld_acquire_u(bar + 1) != gen + 1) {
-        }
+    unsigned old;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+    const unsigned target = (gen + 1) * G;
+    while ((int)(ld_acquire_u(bar) - target) < 0) {
     }
 }
 
@@ -155,13 +153,14 @@ __global__ void __launch_bounds__(THREADS, 1) mega_kernel(const Phase* __restric
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
     float* red = reinterpret_cast<float*>(tmem_slot + 4);   // LN block reductions [2][4]
     unsigned long long* t_ready = reinterpret_cast<unsigned long long*>(red + 8);   // [16] producer X-ready times
+    unsigned long long* t_wait = t_ready + 16;                                        // [16] producer starts waiting
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int b = blockIdx.x, G = gridDim.x;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < C::NBAR; ++i) mbar_init(su32(&bars[i]), 1);
         for (int i = 0; i < 2; ++i) mbar_init(su32(&acc_empty[i]), 4);   // one arrival per epilogue warp
-        for (int i = 0; i < 16; ++i) t_ready[i] = 0ull;
+        for (int i = 0; i < 32; ++i) t_ready[i] = 0ull;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -187,6 +186,7 @@ __global__ void __launch_bounds__(THREADS, 1) mega_kernel(const Phase* __restric
                 // X of this phase may be read once the previous phase is complete
                 // everywhere: the previous kernel (p == 0) or this launch's grid barrier
                 auto make_ready = [&]() {
+                    if (tr.buf) t_wait[p] = gtimer();
                     if (p == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
                     else mbar_wait(su32(xready), (nx++) & 1);
                     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -444,8 +444,8 @@ __global__ void __launch_bounds__(THREADS, 1) mega_kernel(const Phase* __restric
             const unsigned long long t_done = tr.buf ? gtimer() : 0ull;
             if (p + 1 < n_phases) {
                 // phase boundary: every CTA's writes of this phase are visible
-                // (to generic loads and to the TMA reads of the next GEMM phase)
-                __threadfence();
+                // (to generic loads and to the TMA reads of the next GEMM phase):
+                // CTA barrier, then tid 0's gpu-scope release covers them
                 fence_proxy_async_global();
                 named_bar(1, 128);
                 if (tid == 0) grid_sync(gbar, (unsigned)G, gen);
@@ -459,6 +459,12 @@ __global__ void __launch_bounds__(THREADS, 1) mega_kernel(const Phase* __restric
                 rec[1] = gtimer();
                 rec[2] = 0;
                 rec[3] = (unsigned long long)(tr.tag | (1 << 3)) | ((unsigned long long)p << 40);
+                // second record of the phase: {producer wait start, 0, 0, tag | p}
+                unsigned long long* rec2 = tr.buf + 4 * (tr.base + (long long)(n_phases + 1 + p) * G + b);
+                rec2[0] = 0;
+                rec2[1] = 0;
+                rec2[2] = 0;
+                rec2[3] = (unsigned long long)(tr.tag | (1 << 3)) | ((unsigned long long)p << 40) | (1ull << 62);
             }
         }
     }
@@ -466,7 +472,10 @@ __global__ void __launch_bounds__(THREADS, 1) mega_kernel(const Phase* __restric
     __syncthreads();
     if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
     if (tr.buf && threadIdx.x == 0)
-        for (int p = 0; p < n_phases; ++p) tr.buf[4 * (tr.base + (long long)(p + 1) * G + b) + 2] = t_ready[p];
+        for (int p = 0; p < n_phases; ++p) {
+            tr.buf[4 * (tr.base + (long long)(p + 1) * G + b) + 2] = t_ready[p];
+            tr.buf[4 * (tr.base + (long long)(n_phases + 1 + p) * G + b)] = t_wait[p];
+        }
     trace_end(tr, t_start);
 }
 
@@ -528,7 +537,7 @@ static void launch(bass_model& m, int G, const Phase* dph, int n, float* ws, int
         attr = true;
     }
     BASS_CUDA(launch_pdl(mega_kernel<TT>, dim3(G), dim3(THREADS), (size_t)C::SMEM, m.ctx->stream, dph, n, ws, flags,
-                         epoch, gbar, gen, m.ctx->trace(G * (n + 1), BASS_TR_MEGA)));
+                         epoch, gbar, gen, m.ctx->trace(G * (2 * n + 1), BASS_TR_MEGA)));
 }
 
 }  // namespace mg

@@ -63,7 +63,10 @@ def analyse_mega(rec, t0):
     barrier release (us from the launch's first CTA start)."""
     tag = rec[:, 3]
     kern = rec[(tag & 15) == 5]
-    ph = rec[(tag & 15) == 13]
+    second = (tag >> 62) & 1
+    ph = rec[((tag & 15) == 13) & (second == 0)]
+    ph2 = rec[((tag & 15) == 13) & (second == 1)]
+    p2seq = (ph2[:, 3] >> 4) & ((1 << 36) - 1)
     if not len(kern):
         return
     kseq = kern[:, 3] >> 4
@@ -75,12 +78,16 @@ def analyse_mega(rec, t0):
         k = kern[kseq == sq]
         s0 = k[:, 0].min()
         P = ph[pseq == sq]
+        P2 = ph2[p2seq == sq]
         phases = []
         for p in np.unique(P[:, 3] >> 40):
             r = P[(P[:, 3] >> 40) == p]
+            r2 = P2[((P2[:, 3] >> 40) & 0x3fffff) == p]
             rdy = r[:, 2][r[:, 2] > 0]
+            wt = r2[:, 0][r2[:, 0] > 0] if len(r2) else np.array([])
             phases.append(((r[:, 0].min() - s0) / 1e3, (r[:, 0].max() - s0) / 1e3, (r[:, 1].max() - s0) / 1e3,
-                           ((rdy.min() - s0) / 1e3) if len(rdy) else -1, ((rdy.max() - s0) / 1e3) if len(rdy) else -1))
+                           ((rdy.min() - s0) / 1e3) if len(rdy) else -1, ((rdy.max() - s0) / 1e3) if len(rdy) else -1,
+                           ((wt.min() - s0) / 1e3) if len(wt) else -1, ((wt.max() - s0) / 1e3) if len(wt) else -1))
         rows.append(((k[:, 0].max() - s0) / 1e3, (k[:, 1].max() - s0) / 1e3, phases))
     by = {}
     for r in rows:
@@ -89,14 +96,16 @@ def analyse_mega(rec, t0):
         print(f"\nmega launches with {n} phases: {len(rs)}; median span {np.median([r[1] for r in rs]):.1f} us")
         mid = rs[len(rs) // 2]
         print(f"  example: CTA starts spread {mid[0]:.1f} us, end {mid[1]:.1f} us")
-        for i, (d0, d1, rel, r0, r1) in enumerate(mid[2]):
-            print(f"  phase {i}: x-ready {r0:7.1f}..{r1:7.1f}  done {d0:7.1f}..{d1:7.1f}  released {rel:7.1f}")
+        for i, (d0, d1, rel, r0, r1, w0, w1) in enumerate(mid[2]):
+            print(f"  phase {i}: prod-wait {w0:7.1f}..{w1:7.1f}  x-ready {r0:7.1f}..{r1:7.1f}  "
+                  f"done {d0:7.1f}..{d1:7.1f}  released {rel:7.1f}")
 
 
 def analyse(rec):
     rec = rec[rec[:, 0] > 0]
     analyse_mega(rec, rec[:, 0].min())
     rec = rec[(rec[:, 3] & 15) != 13]
+    rec = rec[(rec[:, 3] >> 62) == 0]
     t0 = rec[:, 0].min()
     seq = rec[:, 3] >> 4
     order = np.argsort(seq, kind="stable")
