@@ -53,7 +53,7 @@ struct Cfg {
     static constexpr int BUDGET = (110 * 1024 - 2048) / STAGE >= 2 ? 110 * 1024 - 2048 : 200 * 1024;
     static constexpr int STAGES_RAW = BUDGET / STAGE;
     static constexpr int STAGES = STAGES_RAW > 8 ? 8 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
-    static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/ + 2 * TT * 4 /*XN row stats*/;
     static constexpr int COLS = NB * TT;
     static constexpr int TMEM_COLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128 : COLS <= 256 ? 256 : 512;
 };
@@ -133,12 +133,28 @@ struct Split {
     float* ws;         // per (tile, token group): [S][TT][NB*BN] fp32 partials (S > 1)
 };
 
+// LayerNorm folded into the GEMM (XN):  LN(x) W^T = rstd * ((x*g) W^T - mean * c) + e
+// with c = W g and e = W b per output column (precomputed), X = bf16(x * g)
+// written by the previous residual epilogue, and the row mean / rstd from
+// the per-(tile, row) sums that epilogue emitted (`stats`, `stat_tiles`).
+struct XNorm {
+    const float* stats;    // [stat_tiles][M] {sum, sum of squares}
+    const float* c;        // [N] sum_k g_k W[n, k]
+    const float* e;        // [N] sum_k b_k W[n, k]
+    int stat_tiles;
+};
+
 // PACKED: W in the packed tile layout (1-D bulk copies); else W [N, K] via `tw`.
-template <int TT, int MODE, int NB, bool PACKED>
+// LNF: 0 plain; 1 (consumer) the LayerNorm preceding this GEMM is folded in
+// (see XNorm); 2 (residual producer) the epilogue also emits the next
+// LayerNorm's row sums and X = bf16(x * g_next).  Compile-time, so the plain
+// kernels carry none of it.
+template <int TT, int MODE, int NB, bool PACKED, int LNF>
 __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tw,
                                                              const __grid_constant__ CUtensorMap tx,
                                                              const __nv_bfloat16* __restrict__ wpk, int M, int N,
-                                                             Split sp, Epi e, TraceArg tr) {
+                                                             Split sp, Epi e, XNorm xn, TraceArg tr) {
+    constexpr bool XN = LNF == 1;
     const unsigned long long t_start = tr.buf ? gtimer() : 0ull;
     using C = Cfg<TT, NB>;
     extern __shared__ uint8_t smem_raw[];
@@ -238,14 +254,41 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
             umma_commit(su32(&bars[2 * C::STAGES]));
         }
         __syncwarp();
+    } else if (XN && warp == 2) {
+        // ---- folded LayerNorm (warp 2, idle during the main loop): row mean /
+        // rstd of this CTA's token rows from the per-(tile, row) sums
+        const int K = sp.k_iters * BK;
+        float* s_mean = reinterpret_cast<float*>(tmem_slot + 4);   // [TT]
+        float* s_rstd = s_mean + TT;                                // [TT]
+        asm volatile("griddepcontrol.wait;" ::: "memory");        // the sums are complete
+        for (int r = lane; r < TT; r += 32) {
+            const int m = m0 + r;
+            float mean = 0.f, rstd = 0.f;
+            if (m < M) {
+                float sm = 0.f, sq = 0.f;
+                for (int t = 0; t < xn.stat_tiles; ++t) {   // fixed tile order
+                    const float2 v = __ldcg(reinterpret_cast<const float2*>(xn.stats) + (int64_t)t * M + m);
+                    sm += v.x;
+                    sq += v.y;
+                }
+                mean = sm / (float)K;
+                const float var = fmaxf(sq / (float)K - mean * mean, 0.f);
+                rstd = 1.0f / sqrtf(var + 1e-5f);
+            }
+            s_mean[r] = mean;
+            s_rstd[r] = rstd;
+        }
     }
+    __syncwarp();
 
     // ---- epilogue: TMEM lane = weight row n0 + sub*128 + 32*warp + lane; columns = tokens
     asm volatile("griddepcontrol.wait;" ::: "memory");   // previous kernel's writes visible
+    if constexpr (XN) __syncthreads();                    // row mean / rstd (warp 2) visible
     mbar_wait(su32(&bars[2 * C::STAGES]), 0);
     fence_after();
     const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
     const int rows = min(TT, M - m0);
+    if constexpr (LNF == 0) {
     if (sp.S == 1) {
 #pragma unroll
         for (int sub = 0; sub < NB; ++sub) {
@@ -375,6 +418,228 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
             }
         }
     }
+    } else {
+    // RESID with row statistics for the next LayerNorm: x += acc, and the
+    // 128 columns' {sum, sum of squares} of the new x per row, reduced in a
+    // fixed order (warp shuffle, then warps 0..3) — see XNorm
+    constexpr bool stats = MODE == EPI_RESID && LNF == 2;
+    float2* red = nullptr;        // [local row][warp] per-warp row sums (idle stage ring)
+    const float* s_mean = reinterpret_cast<const float*>(tmem_slot + 4);
+    const float* s_rstd = s_mean + TT;
+    // per-thread column constants (NB == 1: one weight row n per thread)
+    const int n_t = n0 + warp * 32 + lane;
+    float g_n = 0.f, c_n = 0.f, e_n = 0.f;
+    if (n_t < N) {
+        if constexpr (stats) g_n = __ldg(e.xg + n_t);
+        if constexpr (XN) {
+            c_n = __ldg(xn.c + n_t);
+            e_n = __ldg(xn.e + n_t);
+        }
+    }
+    // returns the new x (stats) — the row reduction is done 4 rows at a time by stat4
+    auto put = [&](int r_local, int m, int n, float acc) -> float {
+        float nv = 0.f;
+        if (n < N) {
+            if constexpr (stats) {
+                float* px = e.x + (int64_t)m * N + n;
+                nv = *px + acc;
+                *px = nv;
+                // X of the next GEMM (its LayerNorm folded): bf16(x * g_next)
+                e.xb[(int64_t)m * N + n] = __float2bfloat16_rn(nv * g_n);
+            } else {
+                if constexpr (XN) {
+                    const int r = m - m0;
+                    acc = s_rstd[r] * (acc - s_mean[r] * c_n) + e_n;
+                }
+                epilogue<MODE, __nv_bfloat16>(e, m, n, N, acc);
+            }
+        }
+        (void)r_local;
+        return nv;
+    };
+    // {sum, sum^2} over the warp's 32 columns for 4 rows at once (transpose-
+    // reduce: 9 shuffles), lane (4 i + 0) ends with value i = 2 * row + stat
+    auto stat4 = [&](int r_local0, int count, float n0v, float n1v, float n2v, float n3v) {
+        if constexpr (stats) {
+            float a[8] = {n0v, n0v * n0v, n1v, n1v * n1v, n2v, n2v * n2v, n3v, n3v * n3v};
+            {
+                const bool up = lane & 16;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float snd = up ? a[i] : a[i + 4], kp = up ? a[i + 4] : a[i];
+                    a[i] = kp + __shfl_xor_sync(0xffffffffu, snd, 16);
+                }
+            }
+            {
+                const bool up = lane & 8;
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const float snd = up ? a[i] : a[i + 2], kp = up ? a[i + 2] : a[i];
+                    a[i] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
+                }
+            }
+            {
+                const bool up = lane & 4;
+                const float snd = up ? a[0] : a[1], kp = up ? a[1] : a[0];
+                a[0] = kp + __shfl_xor_sync(0xffffffffu, snd, 4);
+            }
+            a[0] += __shfl_xor_sync(0xffffffffu, a[0], 2);
+            a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
+            const int idx = (lane >> 2) & 7, row = idx >> 1;
+            if ((lane & 3) == 0 && row < count) {
+                float* dst = reinterpret_cast<float*>(&red[(r_local0 + row) * 4 + warp]);
+                dst[idx & 1] = a[0];
+            }
+        }
+    };
+    auto flush_stats = [&](int r_first, int nrows) {
+        if constexpr (!stats) return;
+        __syncthreads();
+        for (int t = threadIdx.x; t < nrows; t += THREADS) {
+            const float2 a = red[t * 4], b = red[t * 4 + 1], c2 = red[t * 4 + 2], d = red[t * 4 + 3];
+            reinterpret_cast<float2*>(e.stats)[(int64_t)tile * M + m0 + r_first + t] =
+                make_float2((a.x + b.x) + (c2.x + d.x), (a.y + b.y) + (c2.y + d.y));
+        }
+    };
+    if (sp.S == 1) {
+        red = reinterpret_cast<float2*>(smem);
+#pragma unroll
+        for (int sub = 0; sub < NB; ++sub) {
+            const int n = n0 + sub * BN + warp * 32 + lane;
+#pragma unroll 1
+            for (int c0 = 0; c0 < TT; c0 += 16) {
+                if (c0 >= rows) break;
+                float v[16];
+                tmem_ld16(trow + sub * TT + c0, v);
+#pragma unroll
+                for (int j0 = 0; j0 < 16; j0 += 4) {
+                    float nv[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (c0 + j0 + j < rows) nv[j] = put(c0 + j0 + j, m0 + c0 + j0 + j, n, v[j0 + j]);
+                    if (c0 + j0 < rows) stat4(c0 + j0, min(4, rows - c0 - j0), nv[0], nv[1], nv[2], nv[3]);
+                }
+            }
+        }
+        flush_stats(0, rows);
+    } else if ((size_t)rows * (NB * BN * 4 + (stats ? 32 : 0)) <= (size_t)C::STAGES * C::STAGE) {
+        // split-K through distributed shared memory: the S CTAs of this tile
+        // are one cluster.  Each parks its fp32 partial [token][row] in its own
+        // (now idle) stage ring, the cluster barrier publishes it, and CTA
+        // `split` reduces token rows [split*R/S, (split+1)*R/S) reading every
+        // rank's partial over DSMEM, in fixed split order (same arithmetic as
+        // the L2 path below).
+        constexpr int WR = NB * BN;
+        float* part = reinterpret_cast<float*>(smem);
+        red = reinterpret_cast<float2*>(smem + (size_t)rows * WR * 4);
+#pragma unroll
+        for (int sub = 0; sub < NB; ++sub) {
+            const int nn = sub * BN + warp * 32 + lane;
+#pragma unroll 1
+            for (int c0 = 0; c0 < TT; c0 += 16) {
+                if (c0 >= rows) break;
+                float v[16];
+                tmem_ld16(trow + sub * TT + c0, v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (c0 + j < rows) part[(c0 + j) * WR + nn] = v[j];
+            }
+        }
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        const int r0 = split * rows / sp.S, r1 = (split + 1) * rows / sp.S;
+        const uint32_t part_s = su32(part);
+#pragma unroll
+        for (int sub = 0; sub < NB; ++sub) {
+            const int nn = sub * BN + warp * 32 + lane, n = n0 + nn;
+            int r = r0;
+            for (; r + 4 <= r1; r += 4) {   // 4 rows x S partials in flight
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                for (int s = 0; s < sp.S; ++s) {
+                    float p[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        uint32_t ra;
+                        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                                     : "=r"(ra)
+                                     : "r"(part_s + (uint32_t)(((r + u) * WR + nn) * 4)), "r"(s));
+                        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(p[u]) : "r"(ra) : "memory");
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) acc[u] += p[u];
+                }
+                float nv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) nv[u] = put(r + u - r0, m0 + r + u, n, acc[u]);
+                stat4(r - r0, 4, nv[0], nv[1], nv[2], nv[3]);
+            }
+            for (; r < r1; ++r) {
+                float acc = 0.f;
+                for (int s = 0; s < sp.S; ++s) {
+                    uint32_t ra;
+                    float pv;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                                 : "=r"(ra)
+                                 : "r"(part_s + (uint32_t)((r * WR + nn) * 4)), "r"(s));
+                    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(pv) : "r"(ra) : "memory");
+                    acc += pv;
+                }
+                stat4(r - r0, 1, put(r - r0, m0 + r, n, acc), 0.f, 0.f, 0.f);
+            }
+        }
+        flush_stats(r0, r1 - r0);
+        // no CTA may leave (and free its shared memory) while others still read it
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    } else {
+        // split-K through L2: the S CTAs of this tile are one thread-block
+        // cluster.  Each writes its fp32 partial tile (L2-resident scratch),
+        // the cluster barrier publishes them, and CTA `split` reduces token
+        // rows [split*R/S, (split+1)*R/S) of the tile in fixed split order.
+        constexpr int WR = NB * BN;   // partial row width
+        float* blk = sp.ws + (int64_t)(tile * gridDim.z + group) * sp.S * TT * WR;
+        red = reinterpret_cast<float2*>(smem);
+#pragma unroll
+        for (int sub = 0; sub < NB; ++sub) {
+            const int nn = sub * BN + warp * 32 + lane;
+#pragma unroll 1
+            for (int c0 = 0; c0 < TT; c0 += 16) {
+                if (c0 >= rows) break;
+                float v[16];
+                tmem_ld16(trow + sub * TT + c0, v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (c0 + j < rows) __stcg(&blk[((int64_t)split * TT + c0 + j) * WR + nn], v[j]);
+            }
+        }
+        __threadfence();
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        const int r0 = split * rows / sp.S, r1 = (split + 1) * rows / sp.S;
+#pragma unroll
+        for (int sub = 0; sub < NB; ++sub) {
+            const int nn = sub * BN + warp * 32 + lane, n = n0 + nn;
+            int r = r0;
+            for (; r + 4 <= r1; r += 4) {   // 4 rows x S partials in flight
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                for (int s = 0; s < sp.S; ++s) {
+                    float p[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) p[u] = __ldcg(&blk[((int64_t)s * TT + r + u) * WR + nn]);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) acc[u] += p[u];
+                }
+                float nv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) nv[u] = put(r + u - r0, m0 + r + u, n, acc[u]);
+                stat4(r - r0, 4, nv[0], nv[1], nv[2], nv[3]);
+            }
+            for (; r < r1; ++r) {
+                float acc = 0.f;
+                for (int s = 0; s < sp.S; ++s) acc += __ldcg(&blk[((int64_t)s * TT + r) * WR + nn]);
+                stat4(r - r0, 1, put(r - r0, m0 + r, n, acc), 0.f, 0.f, 0.f);
+            }
+        }
+        flush_stats(r0, r1 - r0);
+    }
+    }
     fence_before();
     __syncthreads();
     if (warp == 2)
@@ -462,14 +727,16 @@ struct LaunchArgs {
     const void* W;
     int M, N;
     Split sp;
+    XNorm xn;
 };
 
-template <int TT, int MODE, int NB, bool PACKED>
+template <int TT, int MODE, bool PACKED, int LNF>
 static void launch_k(bass_model& m, const LaunchArgs& a, const Epi& e) {
+    constexpr int NB = 1;   // (NB = 2 measured slower at every benchmark shape: profiles/r1_gemm_nb_split_sweep.txt)
     using C = Cfg<TT, NB>;
     static bool attr = false;
     if (!attr) {
-        BASS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<TT, MODE, NB, PACKED>,
+        BASS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<TT, MODE, NB, PACKED, LNF>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
         attr = true;
     }
@@ -489,29 +756,33 @@ static void launch_k(bass_model& m, const LaunchArgs& a, const Epi& e) {
     cfg.attrs = at;
     cfg.numAttrs = a.sp.S > 1 ? 2 : 1;
     const int nblk = (int)(cfg.gridDim.x * cfg.gridDim.y * cfg.gridDim.z);
-    BASS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TT, MODE, NB, PACKED>, *a.wm, *a.xm,
-                                 (const __nv_bfloat16*)a.W, a.M, a.N, a.sp, e, m.ctx->trace(nblk, BASS_TR_GEMM)));
-}
-
-template <int TT, int NB>
-static void launch_mode(bass_model& m, int mode, bool packed, const LaunchArgs& a, const Epi& e) {
-    if (!packed) {   // raw [N, K] pointers (bass_gemm): plain fp32 store
-        if (mode != EPI_STORE) throw Error(BASS_ERR_STATE, "tcgen05 GEMM: fused epilogues need packed weights");
-        launch_k<TT, EPI_STORE, NB, false>(m, a, e);
-        return;
-    }
-    switch (mode) {
-        case EPI_QKV: launch_k<TT, EPI_QKV, NB, true>(m, a, e); break;
-        case EPI_RESID: launch_k<TT, EPI_RESID, NB, true>(m, a, e); break;
-        case EPI_GELU: launch_k<TT, EPI_GELU, NB, true>(m, a, e); break;
-        default: launch_k<TT, EPI_STORE, NB, true>(m, a, e); break;
-    }
+    BASS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TT, MODE, NB, PACKED, LNF>, *a.wm, *a.xm,
+                                 (const __nv_bfloat16*)a.W, a.M, a.N, a.sp, e, a.xn,
+                                 m.ctx->trace(nblk, BASS_TR_GEMM)));
 }
 
 template <int TT>
-static void launch_nb(bass_model& m, int mode, bool packed, int nb, const LaunchArgs& a, const Epi& e) {
-    if (nb == 2) launch_mode<TT, 2>(m, mode, packed, a, e);
-    else launch_mode<TT, 1>(m, mode, packed, a, e);
+static void launch_mode(bass_model& m, int mode, bool packed, bool xn, const LaunchArgs& a, const Epi& e) {
+    if (!packed) {   // raw [N, K] pointers (bass_gemm): plain fp32 store
+        if (mode != EPI_STORE || xn) throw Error(BASS_ERR_STATE, "tcgen05 GEMM: fused epilogues need packed weights");
+        launch_k<TT, EPI_STORE, false, 0>(m, a, e);
+        return;
+    }
+    if (xn) {   // LayerNorm folded in: the two projections that follow a LayerNorm
+        if (mode == EPI_QKV) launch_k<TT, EPI_QKV, true, 1>(m, a, e);
+        else if (mode == EPI_GELU) launch_k<TT, EPI_GELU, true, 1>(m, a, e);
+        else throw Error(BASS_ERR_STATE, "tcgen05 GEMM: folded LayerNorm only for QKV / FC");
+        return;
+    }
+    switch (mode) {
+        case EPI_QKV: launch_k<TT, EPI_QKV, true, 0>(m, a, e); break;
+        case EPI_RESID:
+            if (e.stats) launch_k<TT, EPI_RESID, true, 2>(m, a, e);   // emits the next LayerNorm's inputs
+            else launch_k<TT, EPI_RESID, true, 0>(m, a, e);
+            break;
+        case EPI_GELU: launch_k<TT, EPI_GELU, true, 0>(m, a, e); break;
+        default: launch_k<TT, EPI_STORE, true, 0>(m, a, e); break;
+    }
 }
 
 }  // namespace tc
@@ -520,15 +791,13 @@ bool tc_gemm_supported(const bass_model& m, int N, int K) {
     return m.dtype == BASS_BF16 && K % tc::BK == 0 && K >= tc::BK && N >= tc::BN;
 }
 
-void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K, const Epi& e, bool packed) {
+void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K, const Epi& e, bool packed,
+             const TcNorm* norm) {
     using namespace tc;
     State& S = state(m);
     // token tile: smallest of 16/32/64/128/160/192/256 covering M (groups of 256 beyond)
     const int TT = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : M <= 160 ? 160 : M <= 192 ? 192 : 256;
-    // NB = 2: 256-row CTA tiles (two accumulators sharing each X tile)
-    static const int nb_env = getenv("BASS_GEMM_NB") ? atoi(getenv("BASS_GEMM_NB")) : 0;
-    // (measured: NB = 1 wins at every benchmark shape, profiles/r1_gemm_nb_split_sweep.txt)
-    const int NB = nb_env == 2 ? 2 : 1;
+    constexpr int NB = 1;
     static CUtensorMap dummy{};
     const CUtensorMap* wm = &dummy;
     if (!packed) {
@@ -537,9 +806,12 @@ void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N
         if (it == S.wmaps.end()) it = S.wmaps.emplace(key, make_map(W, N, K, BN)).first;
         wm = &it->second;
     }
+    XNorm xn{};
+    if (norm) xn = XNorm{norm->stats, norm->c, norm->e, norm->stat_tiles};   // X = bf16(x * g) (caller)
     auto xkey = std::make_tuple(X, M, K, TT);
     auto xit = S.xmaps.find(xkey);
     if (xit == S.xmaps.end()) xit = S.xmaps.emplace(xkey, make_map(X, M, K, TT)).first;
+    const CUtensorMap* xm = &xit->second;
     auto sk = std::make_pair(N, K);
     auto si = S.splits.find(sk);
     if (si == S.splits.end()) si = S.splits.emplace(sk, choose_splits(m.ctx->sm_count, N, K)).first;
@@ -549,15 +821,16 @@ void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N
         const size_t blocks = (size_t)((N + NB * BN - 1) / (NB * BN)) * ((M + TT - 1) / TT);
         sp.ws = (float*)S.ws.need(blocks * sp.S * TT * NB * BN * 4, m.ctx->stream);
     }
-    LaunchArgs a{wm, &xit->second, W, M, N, sp};
+    LaunchArgs a{wm, xm, W, M, N, sp, xn};
+    const bool xnb = norm != nullptr;
     switch (TT) {
-        case 16: launch_nb<16>(m, mode, packed, NB, a, e); break;
-        case 32: launch_nb<32>(m, mode, packed, NB, a, e); break;
-        case 64: launch_nb<64>(m, mode, packed, NB, a, e); break;
-        case 128: launch_nb<128>(m, mode, packed, NB, a, e); break;
-        case 160: launch_nb<160>(m, mode, packed, NB, a, e); break;
-        case 192: launch_nb<192>(m, mode, packed, NB, a, e); break;
-        default: launch_nb<256>(m, mode, packed, NB, a, e); break;
+        case 16: launch_mode<16>(m, mode, packed, xnb, a, e); break;
+        case 32: launch_mode<32>(m, mode, packed, xnb, a, e); break;
+        case 64: launch_mode<64>(m, mode, packed, xnb, a, e); break;
+        case 128: launch_mode<128>(m, mode, packed, xnb, a, e); break;
+        case 160: launch_mode<160>(m, mode, packed, xnb, a, e); break;
+        case 192: launch_mode<192>(m, mode, packed, xnb, a, e); break;
+        default: launch_mode<256>(m, mode, packed, xnb, a, e); break;
     }
     m.ctx->launches++;
     cudaError_t err = cudaGetLastError();

@@ -27,17 +27,31 @@ struct Seqs {                    // one entry per sequence in the block
 // ------------------------------------------------------------- embedding
 // x[r] = tok_emb[id] + pos_emb[pos]   (ref:model.py:203-209)
 template <typename TW>
+// `stats` (optional): {sum, sum of squares} of the row for a LayerNorm fused
+// into the next GEMM (one 'tile' covering the whole row, fixed-order sums).
 __global__ void embed_kernel(const TW* __restrict__ tok_emb, const TW* __restrict__ pos_emb,
                              Rows rows, const int32_t* __restrict__ proposals, int pstride,
-                             int d, float* __restrict__ x) {
+                             int d, float* __restrict__ x, float* __restrict__ stats,
+                             __nv_bfloat16* __restrict__ xb, const float* __restrict__ xg) {
+    __shared__ float red[2][33];
     pdl_trigger();
     pdl_wait();
     const int r = blockIdx.x;
     int id = rows.tok[r];
     if (id < 0) id = proposals[rows.slot[r] * pstride + (-id - 1)];
     const int p = rows.pos[r];
-    for (int c = threadIdx.x; c < d; c += blockDim.x)
-        x[(int64_t)r * d + c] = ld(tok_emb, (int64_t)id * d + c) + ld(pos_emb, (int64_t)p * d + c);
+    float s1 = 0.f, s2 = 0.f;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        const float v = ld(tok_emb, (int64_t)id * d + c) + ld(pos_emb, (int64_t)p * d + c);
+        x[(int64_t)r * d + c] = v;
+        if (xb) xb[(int64_t)r * d + c] = __float2bfloat16_rn(v * xg[c]);
+        s1 += v;
+        s2 += v * v;
+    }
+    if (stats) {
+        const float a = block_sum(s1, red[0]), b = block_sum(s2, red[1]);
+        if (threadIdx.x == 0) reinterpret_cast<float2*>(stats)[r] = make_float2(a, b);
+    }
 }
 
 // ------------------------------------------------------------- layernorm
@@ -105,6 +119,9 @@ enum EpiMode { EPI_QKV = 0, EPI_RESID = 1, EPI_GELU = 2, EPI_STORE = 3 };
 
 struct Epi {
     float* x;            // EPI_RESID: x[m, n] += acc (fp32 residual stream)
+    float* stats;        // EPI_RESID (tcgen05 path, optional): per (128-column tile, row) {sum x, sum x^2} of the new x
+    __nv_bfloat16* xb;   //   ... with it: bf16(x_new * xg) = X of the next GEMM (its LayerNorm folded)
+    const float* xg;     //   the next LayerNorm's gain
     void* out;           // EPI_QKV: q [M, d] (act); EPI_GELU: [M, N] (act); EPI_STORE: [M, N] fp32
     void* kc;            // EPI_QKV: this layer's K cache [slot][H][cap][dh] (act dtype)
     void* vc;

@@ -209,23 +209,63 @@ static double gemm_bytes(const bass_model& m, int mode, int M, int N, int K) {
     return es * N * K + es * M * K + out;
 }
 
+// c[n] = sum_k g[k] W[n, k], e[n] = sum_k b[k] W[n, k] (W packed bf16): the
+// per-column constants of a LayerNorm folded into the following GEMM.  One
+// warp per column, fixed-order sums.
+__global__ void ln_fold_kernel(const __nv_bfloat16* __restrict__ w, int N, int K, const float* __restrict__ g,
+                               const float* __restrict__ b, float* __restrict__ c, float* __restrict__ e) {
+    const int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (n >= N) return;
+    float sc = 0.f, se = 0.f;
+    for (int k = lane; k < K; k += 32) {
+        const float v = __bfloat162float(w[packed_index(n, k, K)]);
+        sc = fmaf(g[k], v, sc);
+        se = fmaf(b[k], v, se);
+    }
+    sc = warp_sum(sc);
+    se = warp_sum(se);
+    if (lane == 0) {
+        c[n] = sc;
+        e[n] = se;
+    }
+}
+
+static void ln_fold_prepare(bass_model& m) {
+    if (m.lnfold_valid) return;
+    const int d = m.g.d_model, L = m.g.n_layer;
+    const size_t per = (size_t)(2 * 3 * d + 2 * 4 * d);
+    float* base = (float*)m.lnfold.need(per * L * 4, m.ctx->stream);
+    for (int l = 0; l < L; ++l) {
+        float* p = base + per * l;
+        const bass_layer& ly = m.layers[l];
+        ln_fold_kernel<<<(3 * d + 7) / 8, 256, 0, m.ctx->stream>>>((const __nv_bfloat16*)ly.wqkv, 3 * d, d, ly.ln1_g,
+                                                                    ly.ln1_b, p, p + 3 * d);
+        ln_fold_kernel<<<(4 * d + 7) / 8, 256, 0, m.ctx->stream>>>((const __nv_bfloat16*)ly.wfc, 4 * d, d, ly.ln2_g,
+                                                                    ly.ln2_b, p + 6 * d, p + 10 * d);
+    }
+    BASS_CUDA(cudaGetLastError());
+    m.lnfold_valid = true;
+}
+
 void pack_weights(cudaStream_t st, const void* src, void* dst, int N, int K, int n_mat) {
     pack_kernel<<<1184, 256, 0, st>>>((const __nv_bfloat16*)src, (__nv_bfloat16*)dst, N, K, (int64_t)N * K,
                                       packed_rows(N) * K, n_mat);
     BASS_CUDA(cudaGetLastError());
 }
 
-void gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K, const Epi& e, bool packed) {
+void gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K, const Epi& e, bool packed,
+          const TcNorm* norm) {
     if (M == 0) return;
     ProfScope prof(m.ctx, BASS_PROF_GEMM, gemm_bytes(m, mode, M, N, K), 2.0 * M * N * K);
     const bool tc = m.dtype == BASS_BF16 && m.gemm_mode != BASS_GEMM_SIMT && tc_gemm_supported(m, N, K);
     if (m.gemm_mode == BASS_GEMM_TC && !tc)
         throw Error(BASS_ERR_STATE, "tcgen05 GEMM requested but unsupported for this shape/dtype");
+    BASS_REQUIRE(!norm || tc, "fused LayerNorm needs the tcgen05 GEMM");
     if (tc) {
         // split-K clusters (gemm_tc.cu).  Persistent alternatives were measured
         // slower inside the PDL chain (static stream-K: staggered SM release;
         // dynamic k-chunks: per-chunk reduction latency) — DESIGN.md section 4
-        tc_gemm(m, mode, X, W, M, N, K, e, packed);
+        tc_gemm(m, mode, X, W, M, N, K, e, packed, norm);
         return;
     }
 #define BASS_GEMM_CASE(MD)                                                            \
@@ -513,10 +553,11 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
         if (m.dtype == BASS_BF16)
             BASS_CUDA(launch_pdl(embed_kernel<__nv_bfloat16>, dim3(M), dim3(128), 0, st,
                                  (const __nv_bfloat16*)m.tok_emb, (const __nv_bfloat16*)m.pos_emb, rows, proposals,
-                                 pstride, d, x));
+                                 pstride, d, x, (float*)nullptr, (__nv_bfloat16*)nullptr, (const float*)nullptr));
         else
             BASS_CUDA(launch_pdl(embed_kernel<float>, dim3(M), dim3(128), 0, st, (const float*)m.tok_emb,
-                                 (const float*)m.pos_emb, rows, proposals, pstride, d, x));
+                                 (const float*)m.pos_emb, rows, proposals, pstride, d, x, (float*)nullptr,
+                                 (__nv_bfloat16*)nullptr, (const float*)nullptr));
         check_launch(ctx);
         {
             ProfScope prof(ctx, BASS_PROF_GEMM, lbytes[0]);
@@ -530,14 +571,60 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
         return;
     }
 
+    // LayerNorms folded into the QKV / FC GEMMs (bf16 tcgen05 path):
+    //   LN(x) W^T = rstd * ((x * g) W^T - mean * c) + e,  c = W g, e = W b.
+    // The embedding and the residual GEMMs write X = bf16(x * g_next) and
+    // per-(128-column tile, row) {sum, sum^2}; the next GEMM applies rstd /
+    // mean in its epilogue — no LayerNorm kernels between projections.
+    static const bool lnfuse_env = !(getenv("BASS_LNFUSE") && atoi(getenv("BASS_LNFUSE")) == 0);
+    const bool lnfuse = lnfuse_env && m.dtype == BASS_BF16 && m.packed && m.gemm_mode != BASS_GEMM_SIMT &&
+                        tc_gemm_supported(m, d, d) && d % 8 == 0;
+    const int stat_tiles = (d + 127) / 128;
+    float* lstats = nullptr;
+    if (lnfuse) {
+        ln_fold_prepare(m);
+        lstats = (float*)m.lnstats.need((size_t)stat_tiles * M * 2 * 4, st);
+    }
     if (m.dtype == BASS_BF16)
         BASS_CUDA(launch_pdl(embed_kernel<__nv_bfloat16>, dim3(M), dim3(128), 0, st,
                              (const __nv_bfloat16*)m.tok_emb, (const __nv_bfloat16*)m.pos_emb, rows, proposals,
-                             pstride, d, x));
+                             pstride, d, x, lstats, lnfuse ? (__nv_bfloat16*)h : (__nv_bfloat16*)nullptr,
+                             (const float*)m.layers[0].ln1_g));
     else
         BASS_CUDA(launch_pdl(embed_kernel<float>, dim3(M), dim3(128), 0, st, (const float*)m.tok_emb,
-                             (const float*)m.pos_emb, rows, proposals, pstride, d, x));
+                             (const float*)m.pos_emb, rows, proposals, pstride, d, x, (float*)nullptr,
+                             (__nv_bfloat16*)nullptr, (const float*)nullptr));
     check_launch(ctx);
+    if (lnfuse) {
+        const size_t per = (size_t)(2 * 3 * d + 2 * 4 * d);
+        const float* fold = (const float*)m.lnfold.p;
+        for (int li = 0; li < g.n_layer; ++li) {
+            const bass_layer& L = m.layers[li];
+            const float* fl = fold + per * li;
+            const TcNorm n1{lstats, fl, fl + 3 * d, li == 0 ? 1 : stat_tiles};
+            gemm(m, EPI_QKV, h, L.wqkv, M, 3 * d, d, qkv_epi(li), m.packed, &n1);
+            run_attention(li, kc_of(li), vc_of(li));
+            Epi ro = r;               // x += ctx Wo^T; X of FC = bf16(x * ln2_g)
+            ro.stats = lstats;
+            ro.xb = (__nv_bfloat16*)h;
+            ro.xg = L.ln2_g;
+            gemm(m, EPI_RESID, cx, L.wo, M, d, d, ro, m.packed);
+            const TcNorm n2{lstats, fl + 6 * d, fl + 10 * d, stat_tiles};
+            gemm(m, EPI_GELU, h, L.wfc, M, 4 * d, d, ge, m.packed, &n2);
+            Epi rp = r;               // x += f Wproj^T; X of the next QKV = bf16(x * ln1_g)
+            if (li + 1 < g.n_layer) {
+                rp.stats = lstats;
+                rp.xb = (__nv_bfloat16*)h;
+                rp.xg = m.layers[li + 1].ln1_g;
+            }
+            gemm(m, EPI_RESID, f, L.wproj, M, d, 4 * d, rp, m.packed);
+        }
+        if (R > 0) {
+            launch_layernorm_any(m, x, lrows, m.lnf_g, m.lnf_b, R, hs);
+            gemm(m, EPI_STORE, hs, m.head, R, V, d, so, m.packed);
+        }
+        return;
+    }
 
     for (int li = 0; li < g.n_layer; ++li) {
         const bass_layer& L = m.layers[li];
@@ -718,7 +805,7 @@ int bass_model_destroy(bass_model* m) {
     cudaFree(m->wblob);
     cudaFree(m->fblob);
     for (DevBuf* b : {&m->x, &m->h, &m->q, &m->ctxb, &m->f, &m->hs, &m->meta, &m->part_o, &m->part_ml,
-                      &m->logits_tmp})
+                      &m->logits_tmp, &m->lnstats, &m->lnfold})
         b->release();
     delete m;
     return BASS_OK;
@@ -726,6 +813,7 @@ int bass_model_destroy(bass_model* m) {
 
 int bass_model_set_weight(bass_model* m, int tensor, int layer, const float* host, int64_t n) {
     return guarded(m->ctx, [&] {
+        m->lnfold_valid = false;
         const bass_geometry& g = m->g;
         const int64_t d = g.d_model, V = g.vocab_size, S = g.max_seq_len;
         BASS_REQUIRE(tensor >= BASS_W_TOK_EMB && tensor <= BASS_W_HEAD, "unknown tensor id");
@@ -788,6 +876,7 @@ int bass_model_set_weight(bass_model* m, int tensor, int layer, const float* hos
 
 int bass_model_init_random(bass_model* m, uint64_t seed, float std) {
     return guarded(m->ctx, [&] {
+        m->lnfold_valid = false;
         const int64_t n = m->weight_bytes / (int64_t)m->esize;
         if (m->dtype == BASS_BF16)
             random_normal<<<m->ctx->sm_count * 8, 256, 0, m->ctx->stream>>>((__nv_bfloat16*)m->wblob, n, seed, std);

@@ -132,6 +132,9 @@ struct bass_model {
     std::vector<bass_layer> layers;
     // workspace (grown on demand)
     bass::DevBuf x, h, q, ctxb, f, hs, meta, part_o, part_ml, logits_tmp;
+    bass::DevBuf lnstats;            // {sum, sum^2} per (128-column tile, row) for folded LayerNorms
+    bass::DevBuf lnfold;             // per layer: c, e of LN1 -> QKV and LN2 -> FC (c = W g, e = W b)
+    bool lnfold_valid = false;       // recomputed after any weight / LN parameter change
     void* tc_state = nullptr;        // tcgen05 split-K GEMM descriptors (gemm_tc.cu)
     void* mega_state = nullptr;      // layer megakernel descriptors / workspace (layer_mega.cu)
 };
@@ -164,14 +167,25 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
 
 // GEMM dispatch (SIMT or tcgen05) — Y = X W^T with a fused epilogue.
 // `packed`: W is in the packed tile layout (packed_index) — the model's own
-// weights; raw [N, K] pointers (bass_gemm) pass false.
+// weights; raw [N, K] pointers (bass_gemm) pass false.  `norm`: LayerNorm
+// fused into X (tcgen05 path only; see TcNorm).
+struct TcNorm;
 void gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K,
-          const Epi& e, bool packed);
+          const Epi& e, bool packed, const TcNorm* norm = nullptr);
 
 // tcgen05 GEMM (gemm_tc.cu); returns false when the shape is unsupported.
 bool tc_gemm_supported(const bass_model& m, int N, int K);
+// LayerNorm folded into a tcgen05 GEMM: X = bf16(x * g) (written by the
+// previous residual epilogue / the embedding), row mean / rstd from the
+// {sum, sum^2} per (128-column tile, row) they emitted, c = W g, e = W b.
+struct TcNorm {
+    const float* stats;
+    const float* c;
+    const float* e;
+    int stat_tiles;
+};
 void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K,
-             const Epi& e, bool packed);
+             const Epi& e, bool packed, const TcNorm* norm = nullptr);
 void tc_release(bass_model& m);
 // pack n_mat contiguous [N, K] bf16 matrices into the packed layout (dst: n_mat * packed_rows(N) * K)
 void pack_weights(cudaStream_t st, const void* src, void* dst, int N, int K, int n_mat);

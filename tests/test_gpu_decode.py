@@ -379,6 +379,26 @@ def test_layer_megakernel_matches_per_kernel_path(tmp_path):
     assert float(err.max()) < 1e-2, float(err.max())
 
 
+def test_folded_layernorm_matches_unfused(tmp_path):
+    """Default path (LayerNorms folded into the QKV / FC GEMM epilogues, row
+    statistics produced by the residual epilogues) vs BASS_LNFUSE=0 (separate
+    LayerNorm kernels): logits within 1e-2, greedy speculative == regular in
+    both (checked inside the probe)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    probe = tmp_path / "probe.py"
+    probe.write_text(_MEGA_PROBE)
+    outs = []
+    for env_extra in ({"BASS_MEGA": "0", "BASS_LNFUSE": "0"}, {"BASS_MEGA": "0", "BASS_LNFUSE": "1"}):
+        path = tmp_path / f"out{len(outs)}.npy"
+        env = dict(os.environ, **env_extra)
+        subprocess.run([sys.executable, str(probe), root, str(path)], check=True, env=env, timeout=300)
+        outs.append(np.load(path))
+    err = np.abs(outs[1] - outs[0]).max(axis=1) / np.abs(outs[0]).max(axis=1)
+    assert float(err.max()) < 1e-2, float(err.max())
+
+
 def test_timeline_trace_records_every_cta(B):
     """bass_trace_enable / bass_trace_read: one record per CTA of every traced
     launch, with ordered timestamps and valid SM ids."""
