@@ -166,7 +166,10 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile = blockIdx.x, split = blockIdx.y, group = blockIdx.z;
+    // grid (token groups, splits, tiles): the token groups of one weight tile are
+    // adjacent in launch order, so for large M (prefill) the tile is read from
+    // HBM once and re-served from L2 to the other groups
+    const int tile = blockIdx.z, split = blockIdx.y, group = blockIdx.x;
     const int n0 = tile * NB * BN, m0 = group * TT;
     const int it0 = (int)((int64_t)split * sp.k_iters / sp.S);
     const int it1 = (int)((int64_t)(split + 1) * sp.k_iters / sp.S);
@@ -376,7 +379,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
         // the cluster barrier publishes them, and CTA `split` reduces token
         // rows [split*R/S, (split+1)*R/S) of the tile in fixed split order.
         constexpr int WR = NB * BN;   // partial row width
-        float* blk = sp.ws + (int64_t)(tile * gridDim.z + group) * sp.S * TT * WR;
+        float* blk = sp.ws + (int64_t)(tile * gridDim.x + group) * sp.S * TT * WR;
 #pragma unroll
         for (int sub = 0; sub < NB; ++sub) {
             const int nn = sub * BN + warp * 32 + lane;
@@ -595,7 +598,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
         // the cluster barrier publishes them, and CTA `split` reduces token
         // rows [split*R/S, (split+1)*R/S) of the tile in fixed split order.
         constexpr int WR = NB * BN;   // partial row width
-        float* blk = sp.ws + (int64_t)(tile * gridDim.z + group) * sp.S * TT * WR;
+        float* blk = sp.ws + (int64_t)(tile * gridDim.x + group) * sp.S * TT * WR;
         red = reinterpret_cast<float2*>(smem);
 #pragma unroll
         for (int sub = 0; sub < NB; ++sub) {
@@ -741,7 +744,7 @@ static void launch_k(bass_model& m, const LaunchArgs& a, const Epi& e) {
         attr = true;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((a.N + NB * BN - 1) / (NB * BN), a.sp.S, (a.M + TT - 1) / TT);
+    cfg.gridDim = dim3((a.M + TT - 1) / TT, a.sp.S, (a.N + NB * BN - 1) / (NB * BN));
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = m.ctx->stream;
