@@ -201,6 +201,19 @@ struct ItemIter {
     }
 };
 
+#ifdef BASS_ATTN_PROBE
+// debug build only: per-CTA clock64() stamps of the pipeline events (CTAs < 16)
+__device__ unsigned long long* g_attn_probe;
+#define APROBE(i)                                                                           \
+    do {                                                                                    \
+        if (g_attn_probe && blockIdx.x < 16) g_attn_probe[blockIdx.x * 32 + (i)] = clock64(); \
+    } while (0)
+#else
+#define APROBE(i) \
+    do {          \
+    } while (0)
+#endif
+
 template <int NQ>
 struct Cfg {
     static constexpr int STAGES = NQ >= 64 ? 2 : 3;
@@ -227,6 +240,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
     const unsigned long long t_start = tr.buf ? gtimer() : 0ull;
     using Cf = Cfg<NQ>;
     constexpr int ST = Cf::STAGES;
+    if (threadIdx.x == 0) APROBE(0);
     extern __shared__ uint8_t smem_raw[];
     pdl_trigger();
 
@@ -277,9 +291,11 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
     __syncthreads();
     fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) APROBE(1);
     // Q and this layer's K/V rows come from the QKV GEMM; the output buffer
     // is read by earlier kernels of the stream
     pdl_wait();
+    if (threadIdx.x == 0) APROBE(2);
 
     // every role walks the same item sequence (ItemIter) and skips the same idle items
 
@@ -298,6 +314,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
                     tma_2d(&tq, base + Cf::OFF_Q + (2 * qb + s) * Cf::R_TILE, su32(&q_full[qb]), h * DH + s * 64,
                            q0row + wk.t0);
                 const int kv_row0 = (slot * H + h) * cap + wk.split * SPLIT;
+                if (n == 0) APROBE(3);
                 for (int c = 0; c < wk.nch; ++c, ++g) {
                     const int st = g % ST;
                     if (g >= ST) mbar_wait(su32(&kv_empty[st]), ((g / ST) - 1) & 1);
@@ -308,6 +325,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
                     for (int s = 0; s < 2; ++s)
                         tma_2d(&tv, sb + (2 + s) * Cf::KV_TILE, su32(&v_full[st]), s * 64, kv_row0 + c * CH);
                 }
+                if (n < 2) APROBE(4 + n);
                 ++n;
             }
         }
@@ -345,9 +363,11 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
             while (items.next(wk, h)) {
                 const int qb = n & 1, ob = n & 1;
                 mbar_wait(su32(&q_full[qb]), (n >> 1) & 1);
+                if (n < 2) APROBE(6 + n);
                 for (int c = 0; c < wk.nch; ++c, ++g) {
                     const int st = g % ST, sb = g & 1;
                     mbar_wait(su32(&k_full[st]), (g / ST) & 1);
+                    if (g < 4) APROBE(8 + g);
                     if (g >= 2) mbar_wait(su32(&s_free[sb]), ((g >> 1) - 1) & 1);
                     fence_after();
                     const uint32_t ks = base + st * Cf::STAGE;
@@ -396,6 +416,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
                 const int sb = g & 1;
                 const bool first = c == 0;
                 mbar_wait(su32(&s_full[sb]), (g >> 1) & 1);
+                if (g < 4 && tid == 0) APROBE(12 + g);
                 fence_after();
                 float x[NQ];
 #pragma unroll
@@ -484,10 +505,13 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // P -> tensor core
                 __syncwarp();
                 if (lane == 0) mbar_arrive(su32(&p_full[sb]));
+                if (g < 4 && tid == 0) APROBE(16 + g);
             }
             // ---- epilogue: l per column (fixed-order block sum), O^T lane = head dim
             col_reduce<NQ, false>(l_t, red, fin, wq, lane, tid);
+            if (n < 2 && tid == 0) APROBE(20 + n);
             mbar_wait(su32(&o_full[ob]), (n >> 1) & 1);
+            if (n < 2 && tid == 0) APROBE(22 + n);
             fence_after();
             float o[NQ];
 #pragma unroll
@@ -513,11 +537,13 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
                     }
                 }
             }
+            if (n < 2 && tid == 0) APROBE(24 + n);
             ++n;
         }
     }
     fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) APROBE(26);
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cf::TMEM_COLS)
                      : "memory");
@@ -527,6 +553,10 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+#ifdef BASS_ATTN_PROBE
+void attn_probe_set(void* p) { BASS_CUDA(cudaMemcpyToSymbol(g_attn_probe, &p, sizeof(p))); }
+#endif
 
 static CUtensorMap map2d(const void* ptr, int64_t rows, int64_t cols, int64_t row_stride_elems, int box_rows) {
     static EncodeFn fn = nullptr;
@@ -578,9 +608,16 @@ int stream_split_len() { return ast::SPLIT; }
 
 // Plan: work items (seq, q tile, split, chunks seen) — RAGGED/SPLIT exact,
 // PAD over the padded [max q] x [max L] grid (padded keys streamed, masked).
-void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, int n_slots,
-                           const std::vector<int32_t>& slot, const std::vector<int32_t>& qn,
-                           const std::vector<int32_t>& off, int H, int cap, DevBuf& work_buf, AttnPlan& plan) {
+// query tile: smallest of 16 / 32 / 64 columns covering the longest block
+static int stream_nq(const std::vector<int32_t>& qn) {
+    int max_qn = 0;
+    for (int v : qn) max_qn = std::max(max_qn, v);
+    return max_qn <= 16 ? 16 : max_qn <= 32 ? 32 : 64;
+}
+
+// work items (Work, 8 int32 each) in sequence order; first[i] = sequence i's first item
+static bool stream_items(int strategy, const std::vector<int32_t>& slot, const std::vector<int32_t>& qn,
+                         const std::vector<int32_t>& off, std::vector<int32_t>& w, std::vector<int>* first) {
     using namespace ast;
     const int n_seq = (int)qn.size();
     int max_qn = 0, max_L = 0;
@@ -588,14 +625,12 @@ void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, in
         max_qn = std::max(max_qn, qn[i]);
         max_L = std::max(max_L, off[i] + qn[i]);
     }
-    // query tile: smallest of 16 / 32 / 64 columns covering the longest block
-    const int NQ = max_qn <= 16 ? 16 : max_qn <= 32 ? 32 : 64;
-    std::vector<int32_t> w;
-    std::vector<int> first(n_seq + 1, 0);
+    const int NQ = stream_nq(qn);
+    const size_t w0 = w.size();
     bool multi = false;
     int q0 = 0;   // rows are laid out sequence after sequence
     for (int i = 0; i < n_seq; ++i) {
-        first[i] = (int)w.size() / 8;
+        if (first) (*first)[i] = (int)(w.size() - w0) / 8;
         const int rows = strategy == BASS_PAD ? max_qn : qn[i];
         for (int t0 = 0; t0 < rows; t0 += NQ) {
             const int last = strategy == BASS_PAD ? max_L - 1 : off[i] + std::min(qn[i], t0 + NQ) - 1;
@@ -607,16 +642,41 @@ void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, in
         }
         q0 += qn[i];
     }
-    first[n_seq] = (int)w.size() / 8;
-    Work* wd = (Work*)work_buf.need(std::max<size_t>(w.size(), 8) * 4, ctx->stream);
-    void* hst = ctx->staging.take(w.size() * 4);
-    if (!hst) {
-        ctx->sync();
-        hst = ctx->staging.take(w.size() * 4);
+    if (first) (*first)[n_seq] = (int)(w.size() - w0) / 8;
+    return multi;
+}
+
+void stream_attention_work(int strategy, const std::vector<int32_t>& slot, const std::vector<int32_t>& qn,
+                           const std::vector<int32_t>& off, std::vector<int32_t>& w) {
+    stream_items(strategy, slot, qn, off, w, nullptr);
+}
+
+void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, int n_slots,
+                           const std::vector<int32_t>& slot, const std::vector<int32_t>& qn,
+                           const std::vector<int32_t>& off, int H, int cap, DevBuf& work_buf, AttnPlan& plan,
+                           const void* pre_work) {
+    using namespace ast;
+    const int n_seq = (int)qn.size();
+    int max_L = 0;
+    for (int i = 0; i < n_seq; ++i) max_L = std::max(max_L, off[i] + qn[i]);
+    const int NQ = stream_nq(qn);
+    std::vector<int32_t> w;
+    std::vector<int> first(n_seq + 1, 0);
+    const bool multi = stream_items(strategy, slot, qn, off, w, &first);
+    Work* wd;
+    if (pre_work) {   // uploaded with the step's metadata (forward_premeta)
+        wd = (Work*)const_cast<void*>(pre_work);
+    } else {
+        wd = (Work*)work_buf.need(std::max<size_t>(w.size(), 8) * 4, ctx->stream);
+        void* hst = ctx->staging.take(w.size() * 4);
+        if (!hst) {
+            ctx->sync();
+            hst = ctx->staging.take(w.size() * 4);
+        }
+        std::memcpy(hst, w.data(), w.size() * 4);
+        BASS_CUDA(cudaMemcpyAsync(wd, hst, w.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+        ctx->h2d_bytes += (int64_t)w.size() * 4;
     }
-    std::memcpy(hst, w.data(), w.size() * 4);
-    BASS_CUDA(cudaMemcpyAsync(wd, hst, w.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-    ctx->h2d_bytes += (int64_t)w.size() * 4;
     plan.tq = map2d(q, M, (int64_t)H * DH, (int64_t)H * DH, NQ);
     plan.NQ = NQ;
     plan.pad_len = strategy == BASS_PAD ? max_L : 0;

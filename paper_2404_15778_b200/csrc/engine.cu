@@ -26,7 +26,7 @@ struct bass_engine {
     int strategy = BASS_RAGGED;
     static constexpr int kPstride = kMaxEmit;
     int32_t* proposals = nullptr;     // [n_slots][kPstride]
-    DevBuf vlog, dlog, vamax, vlse, accf, corr, bonus, scratch, slotbuf, stepbuf, align_tok;
+    DevBuf vlog, dlog, vamax, vlse, accf, corr, bonus, scratch, slotbuf, stepbuf, align_tok, arena;
     SlotStep* step_host = nullptr;    // pinned
     int32_t* small_host = nullptr;    // pinned staging for tiny per-step arrays
 };
@@ -149,7 +149,7 @@ int bass_engine_destroy(bass_engine* e) {
     cudaFreeHost(e->step_host);
     cudaFreeHost(e->small_host);
     for (DevBuf* b : {&e->vlog, &e->dlog, &e->vamax, &e->vlse, &e->accf, &e->corr, &e->bonus, &e->scratch,
-                      &e->slotbuf, &e->stepbuf, &e->align_tok})
+                      &e->slotbuf, &e->stepbuf, &e->align_tok, &e->arena})
         b->release();
     delete e;
     return BASS_OK;
@@ -243,8 +243,7 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
         int32_t* corr = (int32_t*)e->corr.need((size_t)b * Lmax * 4, st);
         int32_t* btok = (int32_t*)e->bonus.need((size_t)b * 4, st);
         double* scratch = greedy ? nullptr : (double*)e->scratch.need((size_t)b * Lmax * 2 * V * 8, st);
-        SlotStep* step_dev = (SlotStep*)e->stepbuf.need((size_t)b * sizeof(SlotStep) + (size_t)b * 4 * 4, st);
-        int32_t* per = (int32_t*)(step_dev + b);       // [4][nA]: slot, committed, generated, pos
+        SlotStep* step_dev = (SlotStep*)e->stepbuf.need((size_t)b * sizeof(SlotStep), st);
 
         while (true) {
             std::vector<int> A;
@@ -254,45 +253,73 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
             ++step;
             const auto ts = clk::now();
             const int l = ctl.length(), nA = (int)A.size();
-            // per-active tables: slot, committed C, generated count, (draft pos filled per j)
-            {
-                std::vector<int32_t> h(3 * nA);
-                for (int i = 0; i < nA; ++i) {
-                    h[i] = A[i];
-                    h[nA + i] = (int32_t)com[A[i]].size();
-                    h[2 * nA + i] = ngen[A[i]];
-                }
-                up(c, per, h.data(), h.size() * 4);
+            // ---- the step's metadata in ONE upload (one PDL chain from the
+            // first draft kernel to finalize): per-active tables (slot,
+            // committed C, generated count), every draft forward's and the
+            // verify forward's batch metadata, the draft positions per j.  All
+            // of it is known on the host before the step's first kernel.
+            const int nd = l + (greedy ? 0 : 1);   // draft forwards (sampled: + the bonus row)
+            std::vector<Batch> dbt(nd);
+            Batch vbt;
+            std::vector<int32_t> ar(3 * nA);
+            for (int i = 0; i < nA; ++i) {
+                ar[i] = A[i];
+                ar[nA + i] = (int32_t)com[A[i]].size();
+                ar[2 * nA + i] = ngen[A[i]];
             }
-            const int32_t* d_slot = per;
-            const int32_t* d_com = per + nA;
-            const int32_t* d_gen = per + 2 * nA;
-            int32_t* d_pos = per + 3 * nA;
-
-            // ---------------------------------------------- draft phase
-            for (int j = 0; j < l + (greedy ? 0 : 1); ++j) {
-                Batch bt;
-                std::vector<int32_t> pos(nA);
+            std::vector<PreMetaOff> doff(nd);
+            std::vector<size_t> pos_off(nd);
+            PreMetaOff voff;
+            {
+                std::vector<int> dl(nA);
+                for (int i = 0; i < nA; ++i) dl[i] = e->kv_draft->len[A[i]];
+                for (int j = 0; j < nd; ++j) {
+                    Batch& bt = dbt[j];
+                    for (int i = 0; i < nA; ++i) {
+                        const int s = A[i];
+                        if (j == 0) {
+                            const int C = (int)com[s].size();
+                            BASS_REQUIRE(dl[i] < C, "draft cache ahead of committed prefix");
+                            bt.add_seq(s, dl[i], com[s].data() + dl[i], C - dl[i]);
+                        } else {
+                            const int32_t ind = -j;   // proposals[s][j-1]
+                            bt.add_seq(s, dl[i], &ind, 1);
+                        }
+                        bt.logit_rows.push_back(bt.rows() - 1);
+                        dl[i] += bt.qn[i];
+                    }
+                    doff[j] = forward_premeta(D, bt, e->strategy, ar);
+                    ar.resize((ar.size() + 7) & ~(size_t)7, 0);
+                    pos_off[j] = ar.size();
+                    for (int i = 0; i < nA; ++i) ar.push_back((int32_t)com[A[i]].size() + j);
+                }
+                std::vector<int32_t> blk;
                 for (int i = 0; i < nA; ++i) {
                     const int s = A[i];
-                    const int dl = e->kv_draft->len[s];
-                    if (j == 0) {
-                        const int C = (int)com[s].size();
-                        BASS_REQUIRE(dl < C, "draft cache ahead of committed prefix");
-                        bt.add_seq(s, dl, com[s].data() + dl, C - dl);
-                    } else {
-                        const int32_t ind = -j;   // proposals[s][j-1]
-                        bt.add_seq(s, dl, &ind, 1);
-                    }
-                    bt.logit_rows.push_back(bt.rows() - 1);
-                    pos[i] = (int)com[s].size() + j;
+                    const int ml = e->kv_main->len[s];
+                    blk.assign(com[s].begin() + ml, com[s].end());
+                    for (int j = 0; j < l; ++j) blk.push_back(-(j + 1));
+                    vbt.add_seq(s, ml, blk.data(), (int)blk.size());
+                    for (int j = 0; j <= l; ++j) vbt.logit_rows.push_back(vbt.rows() - (l + 1) + j);
                 }
+                voff = forward_premeta(M, vbt, e->strategy, ar);
+            }
+            int32_t* dar = (int32_t*)e->arena.need(ar.size() * 4, st);
+            up(c, dar, ar.data(), ar.size() * 4);
+            const int32_t* d_slot = dar;
+            const int32_t* d_com = dar + nA;
+            const int32_t* d_gen = dar + 2 * nA;
+
+            // ---------------------------------------------- draft phase
+            for (int j = 0; j < nd; ++j) {
+                const Batch& bt = dbt[j];
                 float* out = dlog + (size_t)j * nA * V;
-                forward(D, *e->kv_draft, bt, e->strategy, out, e->proposals, bass_engine::kPstride);
+                const PreMeta pm = premeta_at(dar, doff[j]);
+                forward(D, *e->kv_draft, bt, e->strategy, out, e->proposals, bass_engine::kPstride, &pm);
                 for (int i = 0; i < nA; ++i) e->kv_draft->len[A[i]] += bt.qn[i];
                 if (j == l) break;   // sampled bonus row: no pick here
                 draft_calls += nA;
-                up(c, d_pos, pos.data(), nA * 4);
+                const int32_t* d_pos = dar + pos_off[j];
                 DraftPick dp{d_slot, d_sid, d_pos, e->proposals, bass_engine::kPstride, j,
                              r->align, r->align_seed, d_align, d_plen, maxnew};
                 ProfScope prof(c, BASS_PROF_SAMPLE, (double)nA * V * 4);
@@ -304,18 +331,9 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
             }
             // ---------------------------------------------- verify
             {
-                Batch bt;
-                std::vector<int32_t> blk;
-                for (int i = 0; i < nA; ++i) {
-                    const int s = A[i];
-                    const int ml = e->kv_main->len[s], C = (int)com[s].size();
-                    blk.assign(com[s].begin() + ml, com[s].end());
-                    for (int j = 0; j < l; ++j) blk.push_back(-(j + 1));
-                    bt.add_seq(s, ml, blk.data(), (int)blk.size());
-                    for (int j = 0; j <= l; ++j) bt.logit_rows.push_back(bt.rows() - (l + 1) + j);
-                    (void)C;
-                }
-                forward(M, *e->kv_main, bt, e->strategy, vlog, e->proposals, bass_engine::kPstride);
+                const Batch& bt = vbt;
+                const PreMeta pm = premeta_at(dar, voff);
+                forward(M, *e->kv_main, bt, e->strategy, vlog, e->proposals, bass_engine::kPstride, &pm);
                 for (int i = 0; i < nA; ++i) e->kv_main->len[A[i]] += bt.qn[i];
                 main_calls += nA;
             }

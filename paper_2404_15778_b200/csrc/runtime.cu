@@ -415,19 +415,8 @@ static void launch_attention(bass_ctx* ctx, int dtype, int dh, int strategy, con
 #undef BASS_ATT
 }
 
-void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* logits_out,
-             const int32_t* proposals, int pstride) {
-    bass_ctx* ctx = m.ctx;
-    cudaStream_t st = ctx->stream;
-    const bass_geometry& g = m.g;
-    const int M = b.rows(), n_seq = (int)b.slot.size(), R = (int)b.logit_rows.size();
-    const int d = g.d_model, H = g.n_head, dh = g.d_head, V = g.vocab_size;
-    const size_t es = m.esize;
-    // metadata: tok, row_slot, row_pos | slot, q0, qn, off | logit_rows | attention work (separate)
-    const size_t nmeta = 3 * (size_t)M + 4 * (size_t)n_seq + R;
-    int32_t* meta = (int32_t*)m.meta.need(nmeta * 4, st);
-    std::vector<int32_t> hm;
-    hm.reserve(nmeta);
+// forward's metadata block: tok, row_slot, row_pos | slot, q0, qn, off | logit_rows
+static void append_meta(const Batch& b, std::vector<int32_t>& hm) {
     hm.insert(hm.end(), b.tok.begin(), b.tok.end());
     hm.insert(hm.end(), b.row_slot.begin(), b.row_slot.end());
     hm.insert(hm.end(), b.row_pos.begin(), b.row_pos.end());
@@ -436,7 +425,47 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
     hm.insert(hm.end(), b.qn.begin(), b.qn.end());
     hm.insert(hm.end(), b.off.begin(), b.off.end());
     hm.insert(hm.end(), b.logit_rows.begin(), b.logit_rows.end());
-    upload_i32(ctx, meta, hm.data(), hm.size());
+}
+
+// the forward's attention runs the stream kernel (its work list can be pre-staged)
+static bool uses_stream_attention(const bass_model& m) {
+    return m.dtype == BASS_BF16 && tc_attention_supported(BASS_BF16, m.g.d_head) && attn_stream_mode();
+}
+
+PreMetaOff forward_premeta(const bass_model& m, const Batch& b, int strategy, std::vector<int32_t>& h) {
+    auto align8 = [&] { h.resize((h.size() + 7) & ~(size_t)7, 0); };   // 32-byte sections
+    PreMetaOff o;
+    align8();
+    o.meta = h.size();
+    append_meta(b, h);
+    if (uses_stream_attention(m)) {
+        align8();
+        o.work = h.size();
+        o.has_work = true;
+        stream_attention_work(strategy, b.slot, b.qn, b.off, h);
+    }
+    return o;
+}
+
+void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* logits_out,
+             const int32_t* proposals, int pstride, const PreMeta* pre) {
+    bass_ctx* ctx = m.ctx;
+    cudaStream_t st = ctx->stream;
+    const bass_geometry& g = m.g;
+    const int M = b.rows(), n_seq = (int)b.slot.size(), R = (int)b.logit_rows.size();
+    const int d = g.d_model, H = g.n_head, dh = g.d_head, V = g.vocab_size;
+    const size_t es = m.esize;
+    int32_t* meta;
+    if (pre && pre->meta) {
+        meta = const_cast<int32_t*>(pre->meta);
+    } else {
+        const size_t nmeta = 3 * (size_t)M + 4 * (size_t)n_seq + R;
+        meta = (int32_t*)m.meta.need(nmeta * 4, st);
+        std::vector<int32_t> hm;
+        hm.reserve(nmeta);
+        append_meta(b, hm);
+        upload_i32(ctx, meta, hm.data(), hm.size());
+    }
     Rows rows{meta, meta + M, meta + 2 * M};
     Seqs seqs{meta + 3 * M, meta + 3 * M + n_seq, meta + 3 * M + 2 * n_seq, meta + 3 * M + 3 * n_seq};
     const int32_t* lrows = meta + 3 * M + 4 * n_seq;
@@ -454,7 +483,8 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
     float *pa_o = nullptr, *pa_ml = nullptr;
     if (m.dtype == BASS_BF16 && tc_attention_supported(BASS_BF16, dh)) {
         if (attn_stream_mode())
-            stream_attention_plan(ctx, strategy, q, M, kv.n_slots, b.slot, b.qn, b.off, H, kv.cap, work_buf, plan);
+            stream_attention_plan(ctx, strategy, q, M, kv.n_slots, b.slot, b.qn, b.off, H, kv.cap, work_buf, plan,
+                                  pre ? pre->work : nullptr);
         else
             tc_attention_plan(ctx, strategy, q, M, kv.n_slots, b.qn, b.off, H, kv.cap, work_buf, plan);
         pa_o = (float*)m.part_o.need((size_t)M * H * plan.mc * dh * 4, st);
@@ -1090,6 +1120,11 @@ int bass_trace_read(bass_ctx* c, uint64_t* host, int64_t max_records, int64_t* n
     });
 }
 
+#ifdef BASS_ATTN_PROBE
+}
+namespace bass { namespace ast { void attn_probe_set(void* p); } }
+extern "C" {
+#endif
 int bass_attention_bench(bass_ctx* c, int strategy, int n_seq, int n_head, const int32_t* cu_q, const int32_t* offsets,
                          const void* q, const void* k, const void* v, int kv_stride, int n_kv, void* out, int reps,
                          double* ms_per_call) {
@@ -1141,6 +1176,26 @@ int bass_attention_bench(bass_ctx* c, int strategy, int n_seq, int n_head, const
         *ms_per_call = ms / reps;
         cudaEventDestroy(a);
         cudaEventDestroy(b);
+#ifdef BASS_ATTN_PROBE
+        {   // one more call with the pipeline stamps on (debug build)
+            unsigned long long* dp;
+            BASS_CUDA(cudaMalloc(&dp, 16 * 32 * 8));
+            BASS_CUDA(cudaMemset(dp, 0, 16 * 32 * 8));
+            ast::attn_probe_set(dp);
+            call(0);
+            c->sync();
+            ast::attn_probe_set(nullptr);
+            std::vector<unsigned long long> hp(16 * 32);
+            BASS_CUDA(cudaMemcpy(hp.data(), dp, hp.size() * 8, cudaMemcpyDeviceToHost));
+            cudaFree(dp);
+            for (int b2 = 0; b2 < 16; ++b2) {
+                fprintf(stderr, "probe cta %2d:", b2);
+                for (int i = 1; i < 27; ++i)
+                    fprintf(stderr, " %6.0f", hp[b2 * 32 + i] ? (double)(hp[b2 * 32 + i] - hp[b2 * 32]) / 1.965 : -1.0);
+                fprintf(stderr, "\n");
+            }
+        }
+#endif
     });
 }
 

@@ -161,9 +161,29 @@ struct Batch {
     int rows() const { return (int)tok.size(); }
 };
 
+// Step-level metadata staging: the per-forward metadata (rows, sequences,
+// logit rows, attention work list) of every forward of a speculative step is
+// laid out in one host arena and uploaded with ONE copy before the step's
+// first kernel, so the step's kernels form a single PDL chain (a host->device
+// copy between kernels is a full stream barrier).
+struct PreMeta {
+    const int32_t* meta = nullptr;   // device: the forward's meta block
+    const void* work = nullptr;      // device: stream-attention work list (nullptr: forward uploads its own)
+};
+struct PreMetaOff {
+    size_t meta = 0, work = 0;       // offsets into the arena (int32 units, 32-byte aligned)
+    bool has_work = false;
+};
+// append forward(m, b)'s metadata to the host arena `h`
+PreMetaOff forward_premeta(const bass_model& m, const Batch& b, int strategy, std::vector<int32_t>& h);
+inline PreMeta premeta_at(const int32_t* dev_arena, const PreMetaOff& o) {
+    return PreMeta{dev_arena + o.meta, o.has_work ? (const void*)(dev_arena + o.work) : nullptr};
+}
+
 // Run `b` through model m over cache kv; logits [logit_rows, V] fp32 -> logits_out (device).
+// `pre`: metadata already on the device (forward_premeta + one upload).
 void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* logits_out,
-             const int32_t* proposals, int pstride);
+             const int32_t* proposals, int pstride, const PreMeta* pre = nullptr);
 
 // GEMM dispatch (SIMT or tcgen05) — Y = X W^T with a fused epilogue.
 // `packed`: W is in the packed tile layout (packed_index) — the model's own
@@ -237,7 +257,11 @@ bool tc_attention_supported(int dtype, int dh);
 int stream_split_len();
 void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, int n_slots,
                            const std::vector<int32_t>& slot, const std::vector<int32_t>& qn,
-                           const std::vector<int32_t>& off, int H, int cap, DevBuf& work_buf, AttnPlan& plan);
+                           const std::vector<int32_t>& off, int H, int cap, DevBuf& work_buf, AttnPlan& plan,
+                           const void* pre_work = nullptr);
+// the stream attention's work list for a batch (what stream_attention_plan uploads)
+void stream_attention_work(int strategy, const std::vector<int32_t>& slot, const std::vector<int32_t>& qn,
+                           const std::vector<int32_t>& off, std::vector<int32_t>& w);
 void stream_attention_run(bass_ctx* ctx, const AttnPlan& plan, const void* kc, const void* vc, const Seqs& seqs_dev,
                           float* part_o, float* part_ml, void* out);
 void tc_attention(bass_ctx* ctx, int strategy, const void* q, int M, const void* kc, const void* vc, int n_slots,
