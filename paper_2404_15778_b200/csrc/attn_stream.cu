@@ -176,7 +176,9 @@ __device__ __forceinline__ void col_reduce(float (&v)[NQ], float* red, float* fi
 // kernel; the sequence's metadata is folded in so an item costs one 32-byte load.
 struct alignas(16) Work {
     int32_t slot, q0row, qn, off;   // KV slot, first Q / out row, rows, committed length
-    int32_t t0, split, nch, pad;    // nch: 128-key chunks of this split the tile's last row sees
+    int32_t t0, split, nch, safe;   // nch: 128-key chunks of this split the tile's last row sees;
+                                    // safe: K/V rows [0, safe) were complete before this launch's
+                                    // chain began (loadable before griddepcontrol.wait)
 };
 
 // Items of this CTA: blockIdx.x, + gridDim.x, ...; the next item's entry is
@@ -292,10 +294,11 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
     fence_after();
     const uint32_t tmem = *tmem_slot;
     if (threadIdx.x == 0) APROBE(1);
-    // Q and this layer's K/V rows come from the QKV GEMM; the output buffer
-    // is read by earlier kernels of the stream
-    pdl_wait();
-    if (threadIdx.x == 0) APROBE(2);
+    // Q and this layer's new K/V rows come from the QKV GEMM and the output
+    // buffer is read by earlier kernels of the stream, so the producer (before
+    // its Q load and any unsafe chunk) and the softmax warps (before their
+    // first write) wait for the predecessor; the work list and history rows
+    // below `safe` were uploaded / written before the chain began.
 
     // every role walks the same item sequence (ItemIter) and skips the same idle items
 
@@ -305,7 +308,27 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
             ItemIter items(work, n_items, H);
             Work wk;
             int h;
-            while (items.next(wk, h)) {
+            bool have = items.next(wk, h);
+            auto load_kv = [&](int kv_row0, int c) {
+                const int st = g % ST;
+                if (g >= ST) mbar_wait(su32(&kv_empty[st]), ((g / ST) - 1) & 1);
+                const uint32_t sb = base + st * Cf::STAGE;
+                mbar_expect_tx(su32(&k_full[st]), 2 * Cf::KV_TILE);
+                for (int s = 0; s < 2; ++s) tma_2d(&tk, sb + s * Cf::KV_TILE, su32(&k_full[st]), s * 64, kv_row0 + c * CH);
+                mbar_expect_tx(su32(&v_full[st]), 2 * Cf::KV_TILE);
+                for (int s = 0; s < 2; ++s)
+                    tma_2d(&tv, sb + (2 + s) * Cf::KV_TILE, su32(&v_full[st]), s * 64, kv_row0 + c * CH);
+                ++g;
+            };
+            // first item: its leading history chunks before the dependency wait
+            int pre = 0;
+            if (have) {
+                const int kv_row0 = (wk.slot * H + h) * cap + wk.split * SPLIT;
+                while (pre < wk.nch && pre < ST && wk.split * SPLIT + (pre + 1) * CH <= wk.safe) load_kv(kv_row0, pre++);
+            }
+            pdl_wait();
+            if (threadIdx.x == 0) APROBE(2);
+            while (have) {
                 const int slot = wk.slot, q0row = wk.q0row;
                 const int qb = n & 1;
                 if (n >= 2) mbar_wait(su32(&q_empty[qb]), ((n >> 1) - 1) & 1);
@@ -315,18 +338,10 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
                            q0row + wk.t0);
                 const int kv_row0 = (slot * H + h) * cap + wk.split * SPLIT;
                 if (n == 0) APROBE(3);
-                for (int c = 0; c < wk.nch; ++c, ++g) {
-                    const int st = g % ST;
-                    if (g >= ST) mbar_wait(su32(&kv_empty[st]), ((g / ST) - 1) & 1);
-                    const uint32_t sb = base + st * Cf::STAGE;
-                    mbar_expect_tx(su32(&k_full[st]), 2 * Cf::KV_TILE);
-                    for (int s = 0; s < 2; ++s) tma_2d(&tk, sb + s * Cf::KV_TILE, su32(&k_full[st]), s * 64, kv_row0 + c * CH);
-                    mbar_expect_tx(su32(&v_full[st]), 2 * Cf::KV_TILE);
-                    for (int s = 0; s < 2; ++s)
-                        tma_2d(&tv, sb + (2 + s) * Cf::KV_TILE, su32(&v_full[st]), s * 64, kv_row0 + c * CH);
-                }
+                for (int c = n == 0 ? pre : 0; c < wk.nch; ++c) load_kv(kv_row0, c);
                 if (n < 2) APROBE(4 + n);
                 ++n;
+                have = items.next(wk, h);
             }
         }
         __syncwarp();
@@ -392,6 +407,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
         __syncwarp();
     } else {
         // ---------------- softmax / epilogue (warps 2-5)
+        pdl_wait();
         const int wq = warp & 3;                 // TMEM lane quarter this warp may access
         const int key = wq * 32 + lane;          // key within the chunk (S^T lane) = head dim (O^T lane)
         const int tid = threadIdx.x - 64;        // 0..127
@@ -617,7 +633,8 @@ static int stream_nq(const std::vector<int32_t>& qn) {
 
 // work items (Work, 8 int32 each) in sequence order; first[i] = sequence i's first item
 static bool stream_items(int strategy, const std::vector<int32_t>& slot, const std::vector<int32_t>& qn,
-                         const std::vector<int32_t>& off, std::vector<int32_t>& w, std::vector<int>* first) {
+                         const std::vector<int32_t>& off, const std::vector<int32_t>* safe, std::vector<int32_t>& w,
+                         std::vector<int>* first) {
     using namespace ast;
     const int n_seq = (int)qn.size();
     int max_qn = 0, max_L = 0;
@@ -636,7 +653,8 @@ static bool stream_items(int strategy, const std::vector<int32_t>& slot, const s
             const int last = strategy == BASS_PAD ? max_L - 1 : off[i] + std::min(qn[i], t0 + NQ) - 1;
             const int n_chunks = last / CH + 1;
             for (int s = 0; s * SPLIT_CH < n_chunks; ++s) {
-                w.insert(w.end(), {slot[i], q0, qn[i], off[i], t0, s, std::min(SPLIT_CH, n_chunks - s * SPLIT_CH), 0});
+                const int sf = std::min(off[i], safe ? (*safe)[i] : off[i]);
+                w.insert(w.end(), {slot[i], q0, qn[i], off[i], t0, s, std::min(SPLIT_CH, n_chunks - s * SPLIT_CH), sf});
                 if (s > 0) multi = true;
             }
         }
@@ -647,8 +665,9 @@ static bool stream_items(int strategy, const std::vector<int32_t>& slot, const s
 }
 
 void stream_attention_work(int strategy, const std::vector<int32_t>& slot, const std::vector<int32_t>& qn,
-                           const std::vector<int32_t>& off, std::vector<int32_t>& w) {
-    stream_items(strategy, slot, qn, off, w, nullptr);
+                           const std::vector<int32_t>& off, const std::vector<int32_t>& safe,
+                           std::vector<int32_t>& w) {
+    stream_items(strategy, slot, qn, off, &safe, w, nullptr);
 }
 
 void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, int n_slots,
@@ -662,7 +681,8 @@ void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, in
     const int NQ = stream_nq(qn);
     std::vector<int32_t> w;
     std::vector<int> first(n_seq + 1, 0);
-    const bool multi = stream_items(strategy, slot, qn, off, w, &first);
+    // uploaded right here (a copy is a full barrier): every committed row is safe
+    const bool multi = stream_items(strategy, slot, qn, off, nullptr, w, &first);
     Work* wd;
     if (pre_work) {   // uploaded with the step's metadata (forward_premeta)
         wd = (Work*)const_cast<void*>(pre_work);

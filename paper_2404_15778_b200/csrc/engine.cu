@@ -26,7 +26,7 @@ struct bass_engine {
     int strategy = BASS_RAGGED;
     static constexpr int kPstride = kMaxEmit;
     int32_t* proposals = nullptr;     // [n_slots][kPstride]
-    DevBuf vlog, dlog, vamax, vlse, accf, corr, bonus, scratch, slotbuf, stepbuf, align_tok, arena;
+    DevBuf vlog, dlog, vamax, vlse, accf, corr, bonus, scratch, slotbuf, stepbuf, align_tok, arena, pick;
     SlotStep* step_host = nullptr;    // pinned
     int32_t* small_host = nullptr;    // pinned staging for tiny per-step arrays
 };
@@ -149,7 +149,7 @@ int bass_engine_destroy(bass_engine* e) {
     cudaFreeHost(e->step_host);
     cudaFreeHost(e->small_host);
     for (DevBuf* b : {&e->vlog, &e->dlog, &e->vamax, &e->vlse, &e->accf, &e->corr, &e->bonus, &e->scratch,
-                      &e->slotbuf, &e->stepbuf, &e->align_tok, &e->arena})
+                      &e->slotbuf, &e->stepbuf, &e->align_tok, &e->arena, &e->pick})
         b->release();
     delete e;
     return BASS_OK;
@@ -244,6 +244,12 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
         int32_t* btok = (int32_t*)e->bonus.need((size_t)b * 4, st);
         double* scratch = greedy ? nullptr : (double*)e->scratch.need((size_t)b * Lmax * 2 * V * 8, st);
         SlotStep* step_dev = (SlotStep*)e->stepbuf.need((size_t)b * sizeof(SlotStep), st);
+        // split greedy draft pick: partials [b][P] {value, index} + per-row arrival counters (zeroed here,
+        // re-armed by the kernel)
+        float* pick_v = (float*)e->pick.need((size_t)b * (2 * GREEDY_PARTS + 1) * 4, st);
+        int* pick_i = (int*)(pick_v + (size_t)b * GREEDY_PARTS);
+        int* pick_cnt = pick_i + (size_t)b * GREEDY_PARTS;
+        BASS_CUDA(cudaMemsetAsync(pick_cnt, 0, (size_t)b * 4, st));
 
         while (true) {
             std::vector<int> A;
@@ -272,7 +278,11 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
             PreMetaOff voff;
             {
                 std::vector<int> dl(nA);
-                for (int i = 0; i < nA; ++i) dl[i] = e->kv_draft->len[A[i]];
+                std::vector<int32_t> dsafe(nA), vsafe(nA);   // cache lengths at the step's upload
+                for (int i = 0; i < nA; ++i) {
+                    dl[i] = dsafe[i] = e->kv_draft->len[A[i]];
+                    vsafe[i] = e->kv_main->len[A[i]];
+                }
                 for (int j = 0; j < nd; ++j) {
                     Batch& bt = dbt[j];
                     for (int i = 0; i < nA; ++i) {
@@ -288,7 +298,7 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                         bt.logit_rows.push_back(bt.rows() - 1);
                         dl[i] += bt.qn[i];
                     }
-                    doff[j] = forward_premeta(D, bt, e->strategy, ar);
+                    doff[j] = forward_premeta(D, bt, e->strategy, dsafe, ar);
                     ar.resize((ar.size() + 7) & ~(size_t)7, 0);
                     pos_off[j] = ar.size();
                     for (int i = 0; i < nA; ++i) ar.push_back((int32_t)com[A[i]].size() + j);
@@ -302,7 +312,7 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                     vbt.add_seq(s, ml, blk.data(), (int)blk.size());
                     for (int j = 0; j <= l; ++j) vbt.logit_rows.push_back(vbt.rows() - (l + 1) + j);
                 }
-                voff = forward_premeta(M, vbt, e->strategy, ar);
+                voff = forward_premeta(M, vbt, e->strategy, vsafe, ar);
             }
             int32_t* dar = (int32_t*)e->arena.need(ar.size() * 4, st);
             up(c, dar, ar.data(), ar.size() * 4);
@@ -323,8 +333,8 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                 DraftPick dp{d_slot, d_sid, d_pos, e->proposals, bass_engine::kPstride, j,
                              r->align, r->align_seed, d_align, d_plen, maxnew};
                 ProfScope prof(c, BASS_PROF_SAMPLE, (double)nA * V * 4);
-                if (greedy) BASS_CUDA(launch_pdl(draft_greedy_kernel, dim3(nA), dim3(SM_THREADS), 0, st,
-                                                 (const float*)out, V, dp));
+                if (greedy) BASS_CUDA(launch_pdl(draft_greedy_split_kernel, dim3(nA, GREEDY_PARTS), dim3(256), 0, st,
+                                                 (const float*)out, V, dp, pick_v, pick_i, pick_cnt));
                 else draft_sample_kernel<<<nA, SM_THREADS, 0, st>>>(out, V, r->temperature, r->top_p, r->seed,
                                                                      scratch, dp);
                 launched(c);

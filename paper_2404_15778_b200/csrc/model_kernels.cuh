@@ -5,6 +5,8 @@
 // the launch: a row's result is bitwise independent of batch composition and
 // block length (the reference's purity contract, ref:model.py:267-271).
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace bass {
@@ -41,6 +43,50 @@ __global__ void embed_kernel(const TW* __restrict__ tok_emb, const TW* __restric
     if (id < 0) id = proposals[rows.slot[r] * pstride + (-id - 1)];
     const int p = rows.pos[r];
     float s1 = 0.f, s2 = 0.f;
+    if constexpr (std::is_same<TW, __nv_bfloat16>::value) {
+        if ((d & 7) == 0) {   // 16-byte rows: every load of the row issued before the first use
+            constexpr int NV = 4;   // d <= 8 * NV * blockDim
+            const int n8 = d >> 3;
+            uint4 te[NV], pe[NV];
+#pragma unroll
+            for (int u = 0; u < NV; ++u) {
+                const int c8 = threadIdx.x + u * blockDim.x;
+                if (c8 < n8) {
+                    te[u] = __ldg(reinterpret_cast<const uint4*>(tok_emb + (int64_t)id * d) + c8);
+                    pe[u] = __ldg(reinterpret_cast<const uint4*>(pos_emb + (int64_t)p * d) + c8);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < NV; ++u) {
+                const int c8 = threadIdx.x + u * blockDim.x;
+                if (c8 >= n8) continue;
+                const __nv_bfloat16* tb = reinterpret_cast<const __nv_bfloat16*>(&te[u]);
+                const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(&pe[u]);
+                float v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    v[k] = __bfloat162float(tb[k]) + __bfloat162float(pb[k]);
+                    s1 += v[k];
+                    s2 += v[k] * v[k];
+                }
+                float4* xo = reinterpret_cast<float4*>(x + (int64_t)r * d) + 2 * c8;
+                xo[0] = make_float4(v[0], v[1], v[2], v[3]);
+                xo[1] = make_float4(v[4], v[5], v[6], v[7]);
+                if (xb) {
+                    const float4 g0 = __ldg(reinterpret_cast<const float4*>(xg) + 2 * c8);
+                    const float4 g1 = __ldg(reinterpret_cast<const float4*>(xg) + 2 * c8 + 1);
+                    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+                    uint4 ob;
+                    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&ob);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) o[k] = __float2bfloat16_rn(v[k] * gg[k]);
+                    reinterpret_cast<uint4*>(xb + (int64_t)r * d)[c8] = ob;
+                }
+            }
+            if (n8 <= NV * (int)blockDim.x) goto stats_out;
+            s1 = s2 = 0.f;   // row too long for the register path: generic loop below
+        }
+    }
     for (int c = threadIdx.x; c < d; c += blockDim.x) {
         const float v = ld(tok_emb, (int64_t)id * d + c) + ld(pos_emb, (int64_t)p * d + c);
         x[(int64_t)r * d + c] = v;
@@ -48,6 +94,7 @@ __global__ void embed_kernel(const TW* __restrict__ tok_emb, const TW* __restric
         s1 += v;
         s2 += v * v;
     }
+stats_out:
     if (stats) {
         const float a = block_sum(s1, red[0]), b = block_sum(s2, red[1]);
         if (threadIdx.x == 0) reinterpret_cast<float2*>(stats)[r] = make_float2(a, b);

@@ -432,7 +432,8 @@ static bool uses_stream_attention(const bass_model& m) {
     return m.dtype == BASS_BF16 && tc_attention_supported(BASS_BF16, m.g.d_head) && attn_stream_mode();
 }
 
-PreMetaOff forward_premeta(const bass_model& m, const Batch& b, int strategy, std::vector<int32_t>& h) {
+PreMetaOff forward_premeta(const bass_model& m, const Batch& b, int strategy, const std::vector<int32_t>& safe,
+                           std::vector<int32_t>& h) {
     auto align8 = [&] { h.resize((h.size() + 7) & ~(size_t)7, 0); };   // 32-byte sections
     PreMetaOff o;
     align8();
@@ -442,7 +443,7 @@ PreMetaOff forward_premeta(const bass_model& m, const Batch& b, int strategy, st
         align8();
         o.work = h.size();
         o.has_work = true;
-        stream_attention_work(strategy, b.slot, b.qn, b.off, h);
+        stream_attention_work(strategy, b.slot, b.qn, b.off, safe, h);
     }
     return o;
 }
@@ -581,7 +582,7 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
         }
         mega_prepare(m, launches);   // one descriptor upload, before the forward's first kernel
         if (m.dtype == BASS_BF16)
-            BASS_CUDA(launch_pdl(embed_kernel<__nv_bfloat16>, dim3(M), dim3(128), 0, st,
+            BASS_CUDA(launch_pdl(embed_kernel<__nv_bfloat16>, dim3(M), dim3(256), 0, st,
                                  (const __nv_bfloat16*)m.tok_emb, (const __nv_bfloat16*)m.pos_emb, rows, proposals,
                                  pstride, d, x, (float*)nullptr, (__nv_bfloat16*)nullptr, (const float*)nullptr));
         else
@@ -616,7 +617,7 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
         lstats = (float*)m.lnstats.need((size_t)stat_tiles * M * 2 * 4, st);
     }
     if (m.dtype == BASS_BF16)
-        BASS_CUDA(launch_pdl(embed_kernel<__nv_bfloat16>, dim3(M), dim3(128), 0, st,
+        BASS_CUDA(launch_pdl(embed_kernel<__nv_bfloat16>, dim3(M), dim3(256), 0, st,
                              (const __nv_bfloat16*)m.tok_emb, (const __nv_bfloat16*)m.pos_emb, rows, proposals,
                              pstride, d, x, lstats, lnfuse ? (__nv_bfloat16*)h : (__nv_bfloat16*)nullptr,
                              (const float*)m.layers[0].ln1_g));

@@ -174,8 +174,11 @@ struct PreMetaOff {
     size_t meta = 0, work = 0;       // offsets into the arena (int32 units, 32-byte aligned)
     bool has_work = false;
 };
-// append forward(m, b)'s metadata to the host arena `h`
-PreMetaOff forward_premeta(const bass_model& m, const Batch& b, int strategy, std::vector<int32_t>& h);
+// append forward(m, b)'s metadata to the host arena `h`.  safe[i]: sequence
+// i's K/V rows below it were written before the upload (earlier steps) — the
+// attention may load them before its dependency wait.
+PreMetaOff forward_premeta(const bass_model& m, const Batch& b, int strategy, const std::vector<int32_t>& safe,
+                           std::vector<int32_t>& h);
 inline PreMeta premeta_at(const int32_t* dev_arena, const PreMetaOff& o) {
     return PreMeta{dev_arena + o.meta, o.has_work ? (const void*)(dev_arena + o.work) : nullptr};
 }
@@ -261,7 +264,8 @@ void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, in
                            const void* pre_work = nullptr);
 // the stream attention's work list for a batch (what stream_attention_plan uploads)
 void stream_attention_work(int strategy, const std::vector<int32_t>& slot, const std::vector<int32_t>& qn,
-                           const std::vector<int32_t>& off, std::vector<int32_t>& w);
+                           const std::vector<int32_t>& off, const std::vector<int32_t>& safe,
+                           std::vector<int32_t>& w);
 void stream_attention_run(bass_ctx* ctx, const AttnPlan& plan, const void* kc, const void* vc, const Seqs& seqs_dev,
                           float* part_o, float* part_ml, void* out);
 void tc_attention(bass_ctx* ctx, int strategy, const void* q, int M, const void* kc, const void* vc, int n_slots,

@@ -292,6 +292,61 @@ static __global__ void __launch_bounds__(SM_THREADS) draft_greedy_kernel(const f
     }
 }
 
+// Greedy draft step over P CTAs per row: CTA (i, p) takes the argmax of
+// columns [p V/P, (p+1) V/P), parks it, and the row's last-arriving CTA
+// combines the P partials (max value, then first index — order-free, so the
+// result equals draft_greedy_kernel's bit for bit) and writes the proposal.
+// `cnt` [rows] must be zero; the last CTA re-arms it.
+constexpr int GREEDY_PARTS = 16;
+static __global__ void __launch_bounds__(256) draft_greedy_split_kernel(const float* __restrict__ logits, int V,
+                                                                        DraftPick d, float* __restrict__ pv,
+                                                                        int* __restrict__ pi, int* __restrict__ cnt) {
+    pdl_trigger();
+    pdl_wait();
+    __shared__ float fv[33];
+    __shared__ int iv[33];
+    __shared__ bool last;
+    const int i = blockIdx.x, part = blockIdx.y, P = gridDim.y;
+    const float* row = logits + (int64_t)i * V;
+    // 4-aligned column range so the float4 path stays aligned
+    const int n4 = V >> 2;
+    const int c0 = (int)((int64_t)part * n4 / P) * 4;
+    const int c1 = part == P - 1 ? V : (int)((int64_t)(part + 1) * n4 / P) * 4;
+    ArgMax a{-INFINITY, 0x7fffffff};
+    if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
+        const float4* r4 = reinterpret_cast<const float4*>(row);
+        const int e4 = c1 >> 2;
+#pragma unroll 4
+        for (int k = (c0 >> 2) + threadIdx.x; k < e4; k += blockDim.x) {
+            const float4 v = __ldcg(r4 + k);
+            a = better(a, ArgMax{v.x, 4 * k});
+            a = better(a, ArgMax{v.y, 4 * k + 1});
+            a = better(a, ArgMax{v.z, 4 * k + 2});
+            a = better(a, ArgMax{v.w, 4 * k + 3});
+        }
+        for (int k = (e4 << 2) + threadIdx.x; k < c1; k += blockDim.x) a = better(a, ArgMax{row[k], k});
+    } else {
+        for (int k = c0 + threadIdx.x; k < c1; k += blockDim.x) a = better(a, ArgMax{row[k], k});
+    }
+    a = block_argmax(a, fv, iv);
+    if (threadIdx.x == 0) {
+        pv[i * P + part] = a.v;
+        pi[i * P + part] = a.i;
+        __threadfence();
+        last = atomicAdd(&cnt[i], 1) == P - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        ArgMax r{-INFINITY, 0x7fffffff};
+        for (int q = 0; q < P; ++q) r = better(r, ArgMax{__ldcg(pv + i * P + q), __ldcg(pi + i * P + q)});
+        cnt[i] = 0;
+        const int slot = d.slot[i];
+        d.proposals[slot * d.pstride + d.j] = aligned_override(d, slot, d.pos[i], V, r.i);
+    }
+}
+
 // sampled draft step: proposal ~ shape(row), uniform = RNG(seed, sid, DRAFT, pos)
 static __global__ void __launch_bounds__(SM_THREADS) draft_sample_kernel(const float* __restrict__ logits,
                                                                   int V, double T, double top_p,
