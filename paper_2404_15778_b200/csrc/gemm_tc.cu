@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -712,6 +713,13 @@ static int choose_splits(int sm_count, int N, int K) {
     static const struct { int N, K, S; } tuned[] = {
         {13824, 4608, 2}, {4608, 4608, 6}, {18432, 4608, 2}, {4608, 18432, 6}, {50272, 4608, 1},
         {6144, 2048, 4},  {2048, 2048, 8}, {8192, 2048, 4},  {2048, 8192, 8},  {50272, 2048, 1}};
+    if (const char* ov = getenv("BASS_SPLIT_OVERRIDE")) {   // tuning only: "NxK:S,NxK:S"
+        int n_, k_, s_, used = 0;
+        for (const char* q = ov; sscanf(q, "%dx%d:%d%n", &n_, &k_, &s_, &used) == 3; q += used + (q[used] == ',')) {
+            if (n_ == N && k_ == K) return s_;
+            if (!q[used]) break;
+        }
+    }
     if (sm_count == 148 && !getenv("BASS_NO_SPLIT_TABLE"))
         for (const auto& t : tuned)
             if (t.N == N && t.K == K) return t.S;
