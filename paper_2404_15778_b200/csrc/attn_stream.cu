@@ -65,6 +65,15 @@ __device__ __forceinline__ void tma_2d(const CUtensorMap* map, uint32_t dst, uin
         "l"(map), "r"(bar), "r"(c0), "r"(c1)
         : "memory");
 }
+// K/V history: read once per forward -> L2 evict-first (keeps activations / code resident)
+__device__ __forceinline__ void tma_2d_ef(const CUtensorMap* map, uint32_t dst, uint32_t bar, int c0, int c1,
+                                          uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
+        "%4}], [%2], %5;" ::"r"(dst),
+        "l"(map), "r"(bar), "r"(c0), "r"(c1), "l"(pol)
+        : "memory");
+}
 // shared-memory matrix descriptor, 128-byte swizzle, version 1
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
     return (uint64_t)((addr & 0x3FFFF) >> 4) | ((uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16) |
@@ -309,15 +318,18 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
             Work wk;
             int h;
             bool have = items.next(wk, h);
+            uint64_t kpol;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(kpol));
             auto load_kv = [&](int kv_row0, int c) {
                 const int st = g % ST;
                 if (g >= ST) mbar_wait(su32(&kv_empty[st]), ((g / ST) - 1) & 1);
                 const uint32_t sb = base + st * Cf::STAGE;
                 mbar_expect_tx(su32(&k_full[st]), 2 * Cf::KV_TILE);
-                for (int s = 0; s < 2; ++s) tma_2d(&tk, sb + s * Cf::KV_TILE, su32(&k_full[st]), s * 64, kv_row0 + c * CH);
+                for (int s = 0; s < 2; ++s)
+                    tma_2d_ef(&tk, sb + s * Cf::KV_TILE, su32(&k_full[st]), s * 64, kv_row0 + c * CH, kpol);
                 mbar_expect_tx(su32(&v_full[st]), 2 * Cf::KV_TILE);
                 for (int s = 0; s < 2; ++s)
-                    tma_2d(&tv, sb + (2 + s) * Cf::KV_TILE, su32(&v_full[st]), s * 64, kv_row0 + c * CH);
+                    tma_2d_ef(&tv, sb + (2 + s) * Cf::KV_TILE, su32(&v_full[st]), s * 64, kv_row0 + c * CH, kpol);
                 ++g;
             };
             // first item: its leading history chunks before the dependency wait

@@ -93,6 +93,21 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
 }
+// L2 policy for data read once per forward (weights, K/V history): evict first,
+// so the stream does not push activations and kernel code out of L2
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                              uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+}
 // UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B
 // apart (SBO = 64 x 16 B), LBO = 1 (unused for swizzled K-major), version 1.
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
@@ -132,6 +147,7 @@ struct Split {
     int S;             // number of K splits
     int k_iters;       // K / BK
     float* ws;         // per (tile, token group): [S][TT][NB*BN] fp32 partials (S > 1)
+    int evict_first;   // weights streamed with an L2 evict-first policy
 };
 
 // LayerNorm folded into the GEMM (XN):  LN(x) W^T = rstd * ((x*g) W^T - mean * c) + e
@@ -201,12 +217,17 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
     // PDL: let the next kernel's CTAs start their own prologue / weight
     // prefetch as soon as SMs free up
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const uint64_t wpol = sp.evict_first ? policy_evict_first() : 0ull;
     auto load_w = [&](uint32_t dst, uint32_t bar, int kb) {
 #pragma unroll
         for (int sub = 0; sub < NB; ++sub) {
             if constexpr (PACKED) {
                 const int nt = tile * NB + sub;   // 128-row packed tile
-                bulk_g2s(dst + sub * BN * BK * 2, wpk + ((int64_t)nt * sp.k_iters + kb) * (BN * BK), BN * BK * 2, bar);
+                if (wpol)
+                    bulk_g2s_hint(dst + sub * BN * BK * 2, wpk + ((int64_t)nt * sp.k_iters + kb) * (BN * BK),
+                                  BN * BK * 2, bar, wpol);
+                else
+                    bulk_g2s(dst + sub * BN * BK * 2, wpk + ((int64_t)nt * sp.k_iters + kb) * (BN * BK), BN * BK * 2, bar);
             } else {
                 tma_2d(&tw, dst + sub * BN * BK * 2, bar, kb * BK, n0 + sub * BN);
             }
@@ -826,7 +847,9 @@ void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N
     auto sk = std::make_pair(N, K);
     auto si = S.splits.find(sk);
     if (si == S.splits.end()) si = S.splits.emplace(sk, choose_splits(m.ctx->sm_count, N, K)).first;
-    Split sp{si->second, K / BK, nullptr};
+    static const int wevict = getenv("BASS_W_EVICT") ? atoi(getenv("BASS_W_EVICT")) : 1;
+    // one token group: every weight byte is read once (prefill re-reads it per group from L2)
+    Split sp{si->second, K / BK, nullptr, (wevict && packed && M <= TT) ? 1 : 0};
     if (const char* fs = getenv("BASS_FORCE_SPLIT")) sp.S = std::max(1, std::min(8, atoi(fs)));   // tuning only
     if (sp.S > 1) {
         const size_t blocks = (size_t)((N + NB * BN - 1) / (NB * BN)) * ((M + TT - 1) / TT);

@@ -1125,6 +1125,21 @@ int bass_trace_read(bass_ctx* c, uint64_t* host, int64_t max_records, int64_t* n
 }
 namespace bass { namespace ast { void attn_probe_set(void* p); } }
 extern "C" {
+// debug build: on = 1 arms the stamps (every attention launch overwrites
+// them), on = 0 copies the last launch's [16][32] stamps to `out` and disarms
+int bass_attn_probe(int on, unsigned long long* out) {
+    static unsigned long long* dp = nullptr;
+    if (on) {
+        if (!dp) cudaMalloc(&dp, 16 * 32 * 8);
+        cudaMemset(dp, 0, 16 * 32 * 8);
+        bass::ast::attn_probe_set(dp);
+    } else if (dp) {
+        cudaDeviceSynchronize();
+        bass::ast::attn_probe_set(nullptr);
+        cudaMemcpy(out, dp, 16 * 32 * 8, cudaMemcpyDeviceToHost);
+    }
+    return 0;
+}
 #endif
 int bass_attention_bench(bass_ctx* c, int strategy, int n_seq, int n_head, const int32_t* cu_q, const int32_t* offsets,
                          const void* q, const void* k, const void* v, int kv_stride, int n_kv, void* out, int reps,

@@ -1,0 +1,1 @@
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/t.log 2>&1; echo rc=$?; tail -3 gpurun_out/t.log
