@@ -461,6 +461,22 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
             e_n = __ldg(xn.e + n_t);
         }
     }
+    // QKV: this thread's column is a fixed destination — q [M, d] (column nn)
+    // or the K / V cache of head h at dim c (row (slot, pos) per token row)
+    __nv_bfloat16* qkv_base = nullptr;
+    bool qkv_cache = false;
+    if constexpr (MODE == EPI_QKV) {
+        if (n_t < N) {
+            const int part = n_t / e.d, nn = n_t - part * e.d;
+            if (part == 0) {
+                qkv_base = reinterpret_cast<__nv_bfloat16*>(e.out) + nn;
+            } else {
+                const int h = nn / e.dh, c = nn - h * e.dh;
+                qkv_base = reinterpret_cast<__nv_bfloat16*>(part == 1 ? e.kc : e.vc) + (int64_t)h * e.cap * e.dh + c;
+                qkv_cache = true;
+            }
+        }
+    }
     // returns the new x (stats) — the row reduction is done 4 rows at a time by stat4
     auto put = [&](int r_local, int m, int n, float acc) -> float {
         float nv = 0.f;
@@ -476,7 +492,13 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
                     const int r = m - m0;
                     acc = s_rstd[r] * (acc - s_mean[r] * c_n) + e_n;
                 }
-                epilogue<MODE, __nv_bfloat16>(e, m, n, N, acc);
+                if constexpr (MODE == EPI_QKV) {   // KV append (ref:kv_cache.py:63-84)
+                    const int64_t off = qkv_cache ? ((int64_t)__ldg(e.row_slot + m) * e.H * e.cap + __ldg(e.row_pos + m)) * e.dh
+                                                  : (int64_t)m * e.d;
+                    qkv_base[off] = __float2bfloat16_rn(acc);
+                } else {
+                    epilogue<MODE, __nv_bfloat16>(e, m, n, N, acc);
+                }
             }
         }
         (void)r_local;
