@@ -161,6 +161,51 @@ struct XNorm {
     int stat_tiles;
 };
 
+// Split-K reduction of U consecutive partial rows: all S x U loads are issued
+// before the first add, then summed in split order s = 0..S-1 (the fixed
+// order every path uses, so the bits do not depend on the path or on M).
+constexpr int MAX_S = 8;
+template <int U>
+__device__ __forceinline__ void dsmem_sum(uint32_t addr0, uint32_t row_stride, int S, float* acc) {
+    float p[MAX_S][U];
+#pragma unroll
+    for (int s = 0; s < MAX_S; ++s)
+        if (s < S) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                uint32_t ra;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(addr0 + u * row_stride), "r"(s));
+                asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(p[s][u]) : "r"(ra));
+            }
+        }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[u] = 0.f;
+#pragma unroll
+    for (int s = 0; s < MAX_S; ++s)
+        if (s < S) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc[u] += p[s][u];
+        }
+}
+template <int U>
+__device__ __forceinline__ void l2_sum(const float* p0, int64_t split_stride, int64_t row_stride, int S, float* acc) {
+    float p[MAX_S][U];
+#pragma unroll
+    for (int s = 0; s < MAX_S; ++s)
+        if (s < S) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) p[s][u] = __ldcg(p0 + s * split_stride + u * row_stride);
+        }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[u] = 0.f;
+#pragma unroll
+    for (int s = 0; s < MAX_S; ++s)
+        if (s < S) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc[u] += p[s][u];
+        }
+}
+
 // PACKED: W in the packed tile layout (1-D bulk copies); else W [N, K] via `tw`.
 // LNF: 0 plain; 1 (consumer) the LayerNorm preceding this GEMM is folded in
 // (see XNorm); 2 (residual producer) the epilogue also emits the next
@@ -361,34 +406,14 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
             if (n < N) {
                 int r = r0;
                 for (; r + 4 <= r1; r += 4) {   // 4 rows x S partials in flight
-                    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-                    for (int s = 0; s < sp.S; ++s) {
-                        float p[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            uint32_t ra;
-                            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
-                                         : "=r"(ra)
-                                         : "r"(part_s + (uint32_t)(((r + u) * WR + nn) * 4)), "r"(s));
-                            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(p[u]) : "r"(ra) : "memory");
-                        }
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) acc[u] += p[u];
-                    }
+                    float acc[4];
+                    dsmem_sum<4>(part_s + (uint32_t)((r * WR + nn) * 4), WR * 4, sp.S, acc);
 #pragma unroll
                     for (int u = 0; u < 4; ++u) epilogue<MODE, __nv_bfloat16>(e, m0 + r + u, n, N, acc[u]);
                 }
                 for (; r < r1; ++r) {
-                    float acc = 0.f;
-                    for (int s = 0; s < sp.S; ++s) {
-                        uint32_t ra;
-                        float pv;
-                        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
-                                     : "=r"(ra)
-                                     : "r"(part_s + (uint32_t)((r * WR + nn) * 4)), "r"(s));
-                        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(pv) : "r"(ra) : "memory");
-                        acc += pv;
-                    }
+                    float acc;
+                    dsmem_sum<1>(part_s + (uint32_t)((r * WR + nn) * 4), WR * 4, sp.S, &acc);
                     epilogue<MODE, __nv_bfloat16>(e, m0 + r, n, N, acc);
                 }
             }
@@ -424,20 +449,14 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
             if (n < N) {
                 int r = r0;
                 for (; r + 4 <= r1; r += 4) {   // 4 rows x S partials in flight
-                    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-                    for (int s = 0; s < sp.S; ++s) {
-                        float p[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) p[u] = __ldcg(&blk[((int64_t)s * TT + r + u) * WR + nn]);
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) acc[u] += p[u];
-                    }
+                    float acc[4];
+                    l2_sum<4>(blk + (int64_t)r * WR + nn, (int64_t)TT * WR, WR, sp.S, acc);
 #pragma unroll
                     for (int u = 0; u < 4; ++u) epilogue<MODE, __nv_bfloat16>(e, m0 + r + u, n, N, acc[u]);
                 }
                 for (; r < r1; ++r) {
-                    float acc = 0.f;
-                    for (int s = 0; s < sp.S; ++s) acc += __ldcg(&blk[((int64_t)s * TT + r) * WR + nn]);
+                    float acc;
+                    l2_sum<1>(blk + (int64_t)r * WR + nn, (int64_t)TT * WR, WR, sp.S, &acc);
                     epilogue<MODE, __nv_bfloat16>(e, m0 + r, n, N, acc);
                 }
             }
@@ -600,36 +619,16 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
             const int nn = sub * BN + warp * 32 + lane, n = n0 + nn;
             int r = r0;
             for (; r + 4 <= r1; r += 4) {   // 4 rows x S partials in flight
-                float acc[4] = {0.f, 0.f, 0.f, 0.f};
-                for (int s = 0; s < sp.S; ++s) {
-                    float p[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        uint32_t ra;
-                        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
-                                     : "=r"(ra)
-                                     : "r"(part_s + (uint32_t)(((r + u) * WR + nn) * 4)), "r"(s));
-                        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(p[u]) : "r"(ra) : "memory");
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) acc[u] += p[u];
-                }
+                float acc[4];
+                dsmem_sum<4>(part_s + (uint32_t)((r * WR + nn) * 4), WR * 4, sp.S, acc);
                 float nv[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) nv[u] = put(r + u - r0, m0 + r + u, n, acc[u]);
                 stat4(r - r0, 4, nv[0], nv[1], nv[2], nv[3]);
             }
             for (; r < r1; ++r) {
-                float acc = 0.f;
-                for (int s = 0; s < sp.S; ++s) {
-                    uint32_t ra;
-                    float pv;
-                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
-                                 : "=r"(ra)
-                                 : "r"(part_s + (uint32_t)((r * WR + nn) * 4)), "r"(s));
-                    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(pv) : "r"(ra) : "memory");
-                    acc += pv;
-                }
+                float acc;
+                dsmem_sum<1>(part_s + (uint32_t)((r * WR + nn) * 4), WR * 4, sp.S, &acc);
                 stat4(r - r0, 1, put(r - r0, m0 + r, n, acc), 0.f, 0.f, 0.f);
             }
         }
@@ -665,22 +664,16 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
             const int nn = sub * BN + warp * 32 + lane, n = n0 + nn;
             int r = r0;
             for (; r + 4 <= r1; r += 4) {   // 4 rows x S partials in flight
-                float acc[4] = {0.f, 0.f, 0.f, 0.f};
-                for (int s = 0; s < sp.S; ++s) {
-                    float p[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) p[u] = __ldcg(&blk[((int64_t)s * TT + r + u) * WR + nn]);
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) acc[u] += p[u];
-                }
+                float acc[4];
+                l2_sum<4>(blk + (int64_t)r * WR + nn, (int64_t)TT * WR, WR, sp.S, acc);
                 float nv[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) nv[u] = put(r + u - r0, m0 + r + u, n, acc[u]);
                 stat4(r - r0, 4, nv[0], nv[1], nv[2], nv[3]);
             }
             for (; r < r1; ++r) {
-                float acc = 0.f;
-                for (int s = 0; s < sp.S; ++s) acc += __ldcg(&blk[((int64_t)s * TT + r) * WR + nn]);
+                float acc;
+                l2_sum<1>(blk + (int64_t)r * WR + nn, (int64_t)TT * WR, WR, sp.S, &acc);
                 stat4(r - r0, 1, put(r - r0, m0 + r, n, acc), 0.f, 0.f, 0.f);
             }
         }
@@ -872,7 +865,8 @@ void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N
     static const int wevict = getenv("BASS_W_EVICT") ? atoi(getenv("BASS_W_EVICT")) : 1;
     // one token group: every weight byte is read once (prefill re-reads it per group from L2)
     Split sp{si->second, K / BK, nullptr, (wevict && packed && M <= TT) ? 1 : 0};
-    if (const char* fs = getenv("BASS_FORCE_SPLIT")) sp.S = std::max(1, std::min(8, atoi(fs)));   // tuning only
+    if (const char* fs = getenv("BASS_FORCE_SPLIT")) sp.S = atoi(fs);   // tuning only
+    sp.S = std::max(1, std::min(MAX_S, sp.S));   // reduction loops and cluster size hold <= 8
     if (sp.S > 1) {
         const size_t blocks = (size_t)((N + NB * BN - 1) / (NB * BN)) * ((M + TT - 1) / TT);
         sp.ws = (float*)S.ws.need(blocks * sp.S * TT * NB * BN * 4, m.ctx->stream);
