@@ -497,13 +497,28 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
         }
     }
     // returns the new x (stats) — the row reduction is done 4 rows at a time by stat4
-    auto put = [&](int r_local, int m, int n, float acc) -> float {
+    // row-dependent epilogue inputs (old residual / KV-cache row offset), loaded
+    // before the split-K reduction so their latency overlaps it
+    struct RowIn {
+        float x;
+        int64_t off;
+    };
+    auto pre = [&](int m, int n) -> RowIn {
+        RowIn ri{0.f, 0};
+        if (n < N) {
+            if constexpr (stats) ri.x = e.x[(int64_t)m * N + n];
+            if constexpr (MODE == EPI_QKV)
+                ri.off = qkv_cache ? ((int64_t)__ldg(e.row_slot + m) * e.H * e.cap + __ldg(e.row_pos + m)) * e.dh
+                                   : (int64_t)m * e.d;
+        }
+        return ri;
+    };
+    auto put = [&](int m, int n, float acc, const RowIn& ri) -> float {
         float nv = 0.f;
         if (n < N) {
             if constexpr (stats) {
-                float* px = e.x + (int64_t)m * N + n;
-                nv = *px + acc;
-                *px = nv;
+                nv = ri.x + acc;
+                e.x[(int64_t)m * N + n] = nv;
                 // X of the next GEMM (its LayerNorm folded): bf16(x * g_next)
                 e.xb[(int64_t)m * N + n] = __float2bfloat16_rn(nv * g_n);
             } else {
@@ -511,16 +526,10 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
                     const int r = m - m0;
                     acc = s_rstd[r] * (acc - s_mean[r] * c_n) + e_n;
                 }
-                if constexpr (MODE == EPI_QKV) {   // KV append (ref:kv_cache.py:63-84)
-                    const int64_t off = qkv_cache ? ((int64_t)__ldg(e.row_slot + m) * e.H * e.cap + __ldg(e.row_pos + m)) * e.dh
-                                                  : (int64_t)m * e.d;
-                    qkv_base[off] = __float2bfloat16_rn(acc);
-                } else {
-                    epilogue<MODE, __nv_bfloat16>(e, m, n, N, acc);
-                }
+                if constexpr (MODE == EPI_QKV) qkv_base[ri.off] = __float2bfloat16_rn(acc);   // KV append (ref:kv_cache.py:63-84)
+                else epilogue<MODE, __nv_bfloat16>(e, m, n, N, acc);
             }
         }
-        (void)r_local;
         return nv;
     };
     // {sum, sum^2} over the warp's 32 columns for 4 rows at once (transpose-
@@ -580,9 +589,12 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
 #pragma unroll
                 for (int j0 = 0; j0 < 16; j0 += 4) {
                     float nv[4] = {0.f, 0.f, 0.f, 0.f};
+                    RowIn ri[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) ri[j] = pre(m0 + c0 + j0 + j, c0 + j0 + j < rows ? n : N);
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
-                        if (c0 + j0 + j < rows) nv[j] = put(c0 + j0 + j, m0 + c0 + j0 + j, n, v[j0 + j]);
+                        if (c0 + j0 + j < rows) nv[j] = put(m0 + c0 + j0 + j, n, v[j0 + j], ri[j]);
                     if (c0 + j0 < rows) stat4(c0 + j0, min(4, rows - c0 - j0), nv[0], nv[1], nv[2], nv[3]);
                 }
             }
@@ -619,17 +631,21 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
             const int nn = sub * BN + warp * 32 + lane, n = n0 + nn;
             int r = r0;
             for (; r + 4 <= r1; r += 4) {   // 4 rows x S partials in flight
+                RowIn ri[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) ri[u] = pre(m0 + r + u, n);
                 float acc[4];
                 dsmem_sum<4>(part_s + (uint32_t)((r * WR + nn) * 4), WR * 4, sp.S, acc);
                 float nv[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) nv[u] = put(r + u - r0, m0 + r + u, n, acc[u]);
+                for (int u = 0; u < 4; ++u) nv[u] = put(m0 + r + u, n, acc[u], ri[u]);
                 stat4(r - r0, 4, nv[0], nv[1], nv[2], nv[3]);
             }
             for (; r < r1; ++r) {
+                const RowIn ri = pre(m0 + r, n);
                 float acc;
                 dsmem_sum<1>(part_s + (uint32_t)((r * WR + nn) * 4), WR * 4, sp.S, &acc);
-                stat4(r - r0, 1, put(r - r0, m0 + r, n, acc), 0.f, 0.f, 0.f);
+                stat4(r - r0, 1, put(m0 + r, n, acc, ri), 0.f, 0.f, 0.f);
             }
         }
         flush_stats(r0, r1 - r0);
@@ -664,17 +680,21 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
             const int nn = sub * BN + warp * 32 + lane, n = n0 + nn;
             int r = r0;
             for (; r + 4 <= r1; r += 4) {   // 4 rows x S partials in flight
+                RowIn ri[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) ri[u] = pre(m0 + r + u, n);
                 float acc[4];
                 l2_sum<4>(blk + (int64_t)r * WR + nn, (int64_t)TT * WR, WR, sp.S, acc);
                 float nv[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) nv[u] = put(r + u - r0, m0 + r + u, n, acc[u]);
+                for (int u = 0; u < 4; ++u) nv[u] = put(m0 + r + u, n, acc[u], ri[u]);
                 stat4(r - r0, 4, nv[0], nv[1], nv[2], nv[3]);
             }
             for (; r < r1; ++r) {
+                const RowIn ri = pre(m0 + r, n);
                 float acc;
                 l2_sum<1>(blk + (int64_t)r * WR + nn, (int64_t)TT * WR, WR, sp.S, &acc);
-                stat4(r - r0, 1, put(r - r0, m0 + r, n, acc), 0.f, 0.f, 0.f);
+                stat4(r - r0, 1, put(m0 + r, n, acc, ri), 0.f, 0.f, 0.f);
             }
         }
         flush_stats(r0, r1 - r0);
