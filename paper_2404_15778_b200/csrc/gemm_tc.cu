@@ -336,10 +336,18 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
             float mean = 0.f, rstd = 0.f;
             if (m < M) {
                 float sm = 0.f, sq = 0.f;
-                for (int t = 0; t < xn.stat_tiles; ++t) {   // fixed tile order
-                    const float2 v = __ldcg(reinterpret_cast<const float2*>(xn.stats) + (int64_t)t * M + m);
-                    sm += v.x;
-                    sq += v.y;
+                for (int t0 = 0; t0 < xn.stat_tiles; t0 += 8) {   // 8 loads in flight, summed in tile order
+                    float2 v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (t0 + u < xn.stat_tiles)
+                            v[u] = __ldcg(reinterpret_cast<const float2*>(xn.stats) + (int64_t)(t0 + u) * M + m);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (t0 + u < xn.stat_tiles) {
+                            sm += v[u].x;
+                            sq += v[u].y;
+                        }
                 }
                 mean = sm / (float)K;
                 const float var = fmaxf(sq / (float)K - mean * mean, 0.f);
