@@ -206,6 +206,22 @@ __device__ __forceinline__ void l2_sum(const float* p0, int64_t split_stride, in
         }
 }
 
+#ifdef BASS_GEMM_PROBE
+// debug build only: globaltimer stamps of one GEMM shape's pipeline events
+// (first 16 CTAs of every launch with N == g_gp_n, K == g_gp_k; the last such
+// launch wins)
+__device__ unsigned long long* g_gp;
+__device__ int g_gp_n, g_gp_k;
+#define GPROBE(i)                                      \
+    do {                                               \
+        if (gp_on) g_gp[gp_cta * 16 + (i)] = gtimer(); \
+    } while (0)
+#else
+#define GPROBE(i) \
+    do {          \
+    } while (0)
+#endif
+
 // PACKED: W in the packed tile layout (1-D bulk copies); else W [N, K] via `tw`.
 // LNF: 0 plain; 1 (consumer) the LayerNorm preceding this GEMM is folded in
 // (see XNorm); 2 (residual producer) the epilogue also emits the next
@@ -218,6 +234,11 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
                                                              Split sp, Epi e, XNorm xn, TraceArg tr) {
     constexpr bool XN = LNF == 1;
     const unsigned long long t_start = tr.buf ? gtimer() : 0ull;
+#ifdef BASS_GEMM_PROBE
+    const int gp_cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const bool gp_on = g_gp && N == g_gp_n && sp.k_iters * BK == g_gp_k && gp_cta < 16;
+#endif
+    if (threadIdx.x == 0) GPROBE(0);
     using C = Cfg<TT, NB>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = su32(smem_raw);
@@ -289,6 +310,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
                 load_w(base + i * C::STAGE, full, it0 + i);
             }
             asm volatile("griddepcontrol.wait;" ::: "memory");
+            GPROBE(1);
             for (int i = 0; i < pre; ++i)
                 tma_2d(&tx, base + i * C::STAGE + C::W_BYTES, su32(&bars[i]), (it0 + i) * BK, m0);
             for (int i = pre; i < nit; ++i) {
@@ -308,6 +330,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
             for (int i = 0; i < nit; ++i) {
                 const int s = i % C::STAGES;
                 mbar_wait(su32(&bars[s]), (i / C::STAGES) & 1);
+                if (i == 0) GPROBE(2);
                 fence_after();
                 const uint32_t st = base + s * C::STAGE;
                 const uint64_t b = sdesc(st + C::W_BYTES);
@@ -322,6 +345,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
                 umma_commit(su32(&bars[C::STAGES + s]));
             }
             umma_commit(su32(&bars[2 * C::STAGES]));
+            GPROBE(3);
         }
         __syncwarp();
     } else if (XN && warp == 2) {
@@ -361,8 +385,10 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
 
     // ---- epilogue: TMEM lane = weight row n0 + sub*128 + 32*warp + lane; columns = tokens
     asm volatile("griddepcontrol.wait;" ::: "memory");   // previous kernel's writes visible
+    if (threadIdx.x == 64) GPROBE(4);
     if constexpr (XN) __syncthreads();                    // row mean / rstd (warp 2) visible
     mbar_wait(su32(&bars[2 * C::STAGES]), 0);
+    if (threadIdx.x == 64) GPROBE(5);
     fence_after();
     const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
     const int rows = min(TT, M - m0);
@@ -631,7 +657,9 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
                     if (c0 + j < rows) part[(c0 + j) * WR + nn] = v[j];
             }
         }
+        if (threadIdx.x == 64) GPROBE(6);
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (threadIdx.x == 64) GPROBE(7);
         const int r0 = split * rows / sp.S, r1 = (split + 1) * rows / sp.S;
         const uint32_t part_s = su32(part);
 #pragma unroll
@@ -656,9 +684,12 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
                 stat4(r - r0, 1, put(m0 + r, n, acc, ri), 0.f, 0.f, 0.f);
             }
         }
+        if (threadIdx.x == 64) GPROBE(8);
         flush_stats(r0, r1 - r0);
+        if (threadIdx.x == 64) GPROBE(9);
         // no CTA may leave (and free its shared memory) while others still read it
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (threadIdx.x == 64) GPROBE(10);
     } else {
         // split-K through L2: the S CTAs of this tile are one thread-block
         // cluster.  Each writes its fp32 partial tile (L2-resident scratch),
@@ -713,6 +744,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
     if (warp == 2)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS)
                      : "memory");
+    if (threadIdx.x == 64) GPROBE(11);
     if (tr.buf && threadIdx.x == 0) {   // trace record index: linear block id
         unsigned sm;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
@@ -726,6 +758,14 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
 }
 
 // ------------------------------------------------------------------ host
+#ifdef BASS_GEMM_PROBE
+void gemm_probe_set(void* p, int n, int k) {
+    BASS_CUDA(cudaMemcpyToSymbol(g_gp, &p, sizeof(p)));
+    BASS_CUDA(cudaMemcpyToSymbol(g_gp_n, &n, sizeof(n)));
+    BASS_CUDA(cudaMemcpyToSymbol(g_gp_k, &k, sizeof(k)));
+}
+#endif
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);

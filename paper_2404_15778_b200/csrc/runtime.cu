@@ -1121,6 +1121,26 @@ int bass_trace_read(bass_ctx* c, uint64_t* host, int64_t max_records, int64_t* n
     });
 }
 
+#ifdef BASS_GEMM_PROBE
+}
+namespace bass { namespace tc { void gemm_probe_set(void* p, int n, int k); } }
+extern "C" {
+// debug build: on = 1 arms the stamps for GEMMs of shape (n, k); on = 0
+// copies the last such launch's [16][16] globaltimer stamps to `out`
+int bass_gemm_probe(int on, int n, int k, unsigned long long* out) {
+    static unsigned long long* dp = nullptr;
+    if (on) {
+        if (!dp) cudaMalloc(&dp, 16 * 16 * 8);
+        cudaMemset(dp, 0, 16 * 16 * 8);
+        bass::tc::gemm_probe_set(dp, n, k);
+    } else if (dp) {
+        cudaDeviceSynchronize();
+        bass::tc::gemm_probe_set(nullptr, 0, 0);
+        cudaMemcpy(out, dp, 16 * 16 * 8, cudaMemcpyDeviceToHost);
+    }
+    return 0;
+}
+#endif
 #ifdef BASS_ATTN_PROBE
 }
 namespace bass { namespace ast { void attn_probe_set(void* p); } }
