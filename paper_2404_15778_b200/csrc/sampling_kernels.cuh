@@ -114,12 +114,30 @@ BASS_DEV void shape_row(const float* __restrict__ row, int V, double T, double t
         const int shift = 24 - 8 * pass;
         for (int b = tid; b < 256; b += nt) { sm.cnt[b] = 0; sm.mass[b] = 0.0; }
         __syncthreads();
-        for (int i = tid; i < V; i += nt) {
-            const uint32_t k = fkey(row[i]);
-            if (pass > 0 && (k >> (shift + 8)) != prefix) continue;
-            const int b = (k >> shift) & 255;
-            atomicAdd(&sm.cnt[b], 1);
-            atomicAdd(&sm.mass[b], e[i] / S);
+        // warp-aggregated: lanes hitting the same bucket are summed (lane
+        // order) and committed by one atomic per group — the few buckets that
+        // hold most logits would otherwise serialise thousands of fp64 atomics
+        const int lane = tid & 31;
+        for (int i0 = 0; i0 < V; i0 += nt) {   // uniform trip count: whole warps stay converged
+            const int i = i0 + tid;
+            int b = -1;
+            double m = 0.0;
+            if (i < V) {
+                const uint32_t k = fkey(row[i]);
+                if (pass == 0 || (k >> (shift + 8)) == prefix) {
+                    b = (k >> shift) & 255;
+                    m = e[i] / S;
+                }
+            }
+            const unsigned peers = __match_any_sync(0xffffffffu, b);
+            if (b >= 0) {
+                double g = 0.0;
+                for (unsigned mm = peers; mm; mm &= mm - 1) g += __shfl_sync(peers, m, __ffs(mm) - 1);
+                if (lane == __ffs(peers) - 1) {
+                    atomicAdd(&sm.cnt[b], __popc(peers));
+                    atomicAdd(&sm.mass[b], g);
+                }
+            }
         }
         __syncthreads();
         if (tid == 0) {
