@@ -1,0 +1,9 @@
+run() { (env $2 timeout 300 python bench.py --steps 3 --warmup 2 --no-cpu-baseline --kernel-events 0 > /tmp/b.log 2>&1); python -c "
+import json
+l=[x for x in open('/tmp/b.log') if x.startswith('{')][-1]; d=json.loads(l); print('$1', round(d['value'],1), round(d['per_seq_ms_per_token']['all'],4))" || tail -3 /tmp/b.log; }
+for i in 1 2; do
+run base X=1
+run mh2 BASS_SPLIT_OVERRIDE=50272x4608:2
+run dh2 BASS_SPLIT_OVERRIDE=50272x2048:2
+run mh3 BASS_SPLIT_OVERRIDE=50272x4608:3
+done
