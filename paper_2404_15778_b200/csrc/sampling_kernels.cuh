@@ -65,6 +65,7 @@ struct Shaped {
 struct ShapeSmem {
     int cnt[256];
     double mass[256];
+    double wmass[SM_THREADS / 32][256];   // per-warp bucket masses (summed in warp order)
     double dred[33];
     float fred[33];
     int ired[33];
@@ -112,12 +113,14 @@ BASS_DEV void shape_row(const float* __restrict__ row, int V, double T, double t
     int keep_all = 0;
     for (int pass = 0; pass < 4 && !keep_all; ++pass) {
         const int shift = 24 - 8 * pass;
-        for (int b = tid; b < 256; b += nt) { sm.cnt[b] = 0; sm.mass[b] = 0.0; }
+        for (int b = tid; b < 256; b += nt) sm.cnt[b] = 0;
+        for (int b = tid; b < (SM_THREADS / 32) * 256; b += nt) (&sm.wmass[0][0])[b] = 0.0;
         __syncthreads();
         // warp-aggregated: lanes hitting the same bucket are summed (lane
-        // order) and committed by one atomic per group — the few buckets that
-        // hold most logits would otherwise serialise thousands of fp64 atomics
-        const int lane = tid & 31;
+        // order) and the group's leader adds it to its warp's private
+        // histogram (no fp64 atomics; warps merged in fixed order below, so
+        // the masses are deterministic)
+        const int lane = tid & 31, wid = tid >> 5;
         for (int i0 = 0; i0 < V; i0 += nt) {   // uniform trip count: whole warps stay converged
             const int i = i0 + tid;
             int b = -1;
@@ -135,9 +138,16 @@ BASS_DEV void shape_row(const float* __restrict__ row, int V, double T, double t
                 for (unsigned mm = peers; mm; mm &= mm - 1) g += __shfl_sync(peers, m, __ffs(mm) - 1);
                 if (lane == __ffs(peers) - 1) {
                     atomicAdd(&sm.cnt[b], __popc(peers));
-                    atomicAdd(&sm.mass[b], g);
+                    sm.wmass[wid][b] += g;
                 }
             }
+        }
+        __syncthreads();
+        for (int b = tid; b < 256; b += nt) {
+            double mb = 0.0;
+#pragma unroll
+            for (int w = 0; w < SM_THREADS / 32; ++w) mb += sm.wmass[w][b];
+            sm.mass[b] = mb;
         }
         __syncthreads();
         if (tid == 0) {
