@@ -886,7 +886,8 @@ static void launch_mode(bass_model& m, int mode, bool packed, bool xn, const Lau
     if (xn) {   // LayerNorm folded in: the two projections that follow a LayerNorm
         if (mode == EPI_QKV) launch_k<TT, EPI_QKV, true, 1>(m, a, e);
         else if (mode == EPI_GELU) launch_k<TT, EPI_GELU, true, 1>(m, a, e);
-        else throw Error(BASS_ERR_STATE, "tcgen05 GEMM: folded LayerNorm only for QKV / FC");
+        else if (mode == EPI_STORE) launch_k<TT, EPI_STORE, true, 1>(m, a, e);   // head (final LayerNorm)
+        else throw Error(BASS_ERR_STATE, "tcgen05 GEMM: folded LayerNorm only for QKV / FC / head");
         return;
     }
     switch (mode) {

@@ -230,11 +230,27 @@ __global__ void ln_fold_kernel(const __nv_bfloat16* __restrict__ w, int N, int K
     }
 }
 
+// rows `lrows` of the folded-LN head input (bf16 X = x * g_f and the per
+// (tile, row) {sum, sum^2}) into compact [R] buffers
+__global__ void head_gather_kernel(const __nv_bfloat16* __restrict__ xb, const float2* __restrict__ st,
+                                   const int32_t* __restrict__ lrows, int M, int R, int d, int tiles,
+                                   __nv_bfloat16* __restrict__ xo, float2* __restrict__ so) {
+    pdl_trigger();
+    pdl_wait();
+    const int r = blockIdx.x, src = lrows[r];
+    const uint4* in = reinterpret_cast<const uint4*>(xb + (int64_t)src * d);
+    uint4* out = reinterpret_cast<uint4*>(xo + (int64_t)r * d);
+    for (int c = threadIdx.x; c < d / 8; c += blockDim.x) out[c] = in[c];
+    for (int t = threadIdx.x; t < tiles; t += blockDim.x) so[(int64_t)t * R + r] = st[(int64_t)t * M + src];
+}
+
 static void ln_fold_prepare(bass_model& m) {
     if (m.lnfold_valid) return;
     const int d = m.g.d_model, L = m.g.n_layer;
     const size_t per = (size_t)(2 * 3 * d + 2 * 4 * d);
-    float* base = (float*)m.lnfold.need(per * L * 4, m.ctx->stream);
+    const int V = m.g.vocab_size;
+    // per layer [3d c][3d e][4d c][4d e], then the final LayerNorm -> head [V c][V e]
+    float* base = (float*)m.lnfold.need((per * L + 2 * (size_t)V) * 4, m.ctx->stream);
     for (int l = 0; l < L; ++l) {
         float* p = base + per * l;
         const bass_layer& ly = m.layers[l];
@@ -243,6 +259,8 @@ static void ln_fold_prepare(bass_model& m) {
         ln_fold_kernel<<<(4 * d + 7) / 8, 256, 0, m.ctx->stream>>>((const __nv_bfloat16*)ly.wfc, 4 * d, d, ly.ln2_g,
                                                                     ly.ln2_b, p + 6 * d, p + 10 * d);
     }
+    ln_fold_kernel<<<(V + 7) / 8, 256, 0, m.ctx->stream>>>((const __nv_bfloat16*)m.head, V, d, m.lnf_g, m.lnf_b,
+                                                           base + per * L, base + per * L + V);
     BASS_CUDA(cudaGetLastError());
     m.lnfold_valid = true;
 }
@@ -611,10 +629,12 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
     const bool lnfuse = lnfuse_env && m.dtype == BASS_BF16 && m.packed && m.gemm_mode != BASS_GEMM_SIMT &&
                         tc_gemm_supported(m, d, d) && d % 8 == 0;
     const int stat_tiles = (d + 127) / 128;
+    static const bool headfold_env = !(getenv("BASS_HEADFOLD") && atoi(getenv("BASS_HEADFOLD")) == 0);
+    const bool headfold = headfold_env && tc_gemm_supported(m, V, d);
     float* lstats = nullptr;
     if (lnfuse) {
         ln_fold_prepare(m);
-        lstats = (float*)m.lnstats.need((size_t)stat_tiles * M * 2 * 4, st);
+        lstats = (float*)m.lnstats.need((size_t)stat_tiles * (M + R) * 2 * 4, st);   // + gathered head rows
     }
     if (m.dtype == BASS_BF16)
         BASS_CUDA(launch_pdl(embed_kernel<__nv_bfloat16>, dim3(M), dim3(256), 0, st,
@@ -647,10 +667,33 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
                 rp.stats = lstats;
                 rp.xb = (__nv_bfloat16*)h;
                 rp.xg = m.layers[li + 1].ln1_g;
+            } else if (R > 0 && headfold) {   // ... or of the head (final LayerNorm folded)
+                rp.stats = lstats;
+                rp.xb = (__nv_bfloat16*)h;
+                rp.xg = m.lnf_g;
             }
             gemm(m, EPI_RESID, f, L.wproj, M, d, 4 * d, rp, m.packed);
         }
-        if (R > 0) {
+        if (R > 0 && headfold) {
+            // every logit row goes through the same folded path (a row's bits
+            // never depend on whether the block also carried prompt rows)
+            bool ident = R == M;
+            for (int i = 0; ident && i < R; ++i) ident = b.logit_rows[i] == i;
+            const float* hf = (const float*)m.lnfold.p + per * g.n_layer;
+            const void* X = h;
+            const float* hst = lstats;
+            if (!ident) {
+                float* cst = lstats + (size_t)stat_tiles * M * 2;
+                BASS_CUDA(launch_pdl(head_gather_kernel, dim3(R), dim3(128), 0, st, (const __nv_bfloat16*)h,
+                                     (const float2*)lstats, lrows, M, R, d, stat_tiles, (__nv_bfloat16*)hs,
+                                     (float2*)cst));
+                check_launch(ctx);
+                X = hs;
+                hst = cst;
+            }
+            const TcNorm nh{hst, hf, hf + V, stat_tiles};
+            gemm(m, EPI_STORE, X, m.head, R, V, d, so, m.packed, &nh);
+        } else if (R > 0) {
             launch_layernorm_any(m, x, lrows, m.lnf_g, m.lnf_b, R, hs);
             gemm(m, EPI_STORE, hs, m.head, R, V, d, so, m.packed);
         }

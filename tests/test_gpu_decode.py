@@ -417,4 +417,4 @@ def test_timeline_trace_records_every_cta(B):
     assert (rec[:, 1] >= rec[:, 0]).all() and (rec[:, 0] > 0).all()
     assert (rec[:, 2] < 1024).all()
     classes = set((rec[:, 3] & 15).tolist())
-    assert {1, 2, 3} <= classes   # GEMM, attention, LayerNorm
+    assert {1, 2} <= classes   # GEMM, attention (the LayerNorms are folded into the GEMMs)
