@@ -399,6 +399,26 @@ def test_folded_layernorm_matches_unfused(tmp_path):
     assert float(err.max()) < 1e-2, float(err.max())
 
 
+def test_draft_self_speculation_accepts_every_proposal(B):
+    """Draft == main (same bf16 weights, separate caches), greedy, natural
+    acceptance: every proposal is the main model's own greedy token (rows are
+    bitwise batch-invariant), so every step accepts its whole draft.  Exercises
+    the greedy draft pick from the folded LM head's per-tile argmax partials
+    (a wrong pick would be rejected)."""
+    w = B.DeviceWeights.from_reference(_bf16_round(OR.init_weights(OR.Geometry(2, 4, 512, 128, 1500, 600), 71)),
+                                       "bf16")
+    rng = np.random.default_rng(12)
+    prompts = [rng.integers(0, 1500, n).tolist() for n in (33, 20, 57)]
+    main_m, draft_m = B.CudaModel(w, 3), B.CudaModel(w, 3)
+    eng = B.CudaEngine(main_m, draft_m)
+    req = B.GenerationRequest(prompts, 20, temperature=0.0, sequence_ids=[0, 1, 2])
+    res, _ = eng.run(req, B.FixedDraftController(4), speculative=True)[:2]
+    steps = list(res.steps)
+    assert len(steps) >= 2
+    for s in steps[:-1]:   # the last step may be clipped at max_new_tokens
+        assert all(a == s.draft_length for a in s.accepted), (s.step_index, s.accepted, s.draft_length)
+
+
 def test_timeline_trace_records_every_cta(B):
     """bass_trace_enable / bass_trace_read: one record per CTA of every traced
     launch, with ordered timestamps and valid SM ids."""
