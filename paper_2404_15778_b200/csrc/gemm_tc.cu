@@ -43,7 +43,8 @@ namespace tc {
 constexpr int BN = 128;          // weight rows per sub-tile (UMMA M)
 constexpr int BK = 64;           // k per stage (one 128-byte swizzle row of bf16)
 constexpr int UK = 16;           // k per tcgen05.mma for 16-bit inputs
-constexpr int THREADS = 128;
+constexpr int EH = 2;               // epilogue row halves: warps w and w + 4 share TMEM lane quarter w
+constexpr int THREADS = 128 * EH;   // 8 warps: 0 producer, 1 MMA, 2 TMEM alloc / folded-LN stats; all drain
 
 template <int TT, int NB>
 struct Cfg {
@@ -249,6 +250,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wq = warp & 3, half = warp >> 2;   // epilogue: TMEM lane quarter, row half
     // grid (token groups, splits, tiles): the token groups of one weight tile are
     // adjacent in launch order, so for large M (prefill) the tile is read from
     // HBM once and re-served from L2 to the other groups
@@ -390,15 +392,15 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
     mbar_wait(su32(&bars[2 * C::STAGES]), 0);
     if (threadIdx.x == 64) GPROBE(5);
     fence_after();
-    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+    const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
     const int rows = min(TT, M - m0);
     if constexpr (LNF == 0) {
     if (sp.S == 1) {
 #pragma unroll
         for (int sub = 0; sub < NB; ++sub) {
-            const int n = n0 + sub * BN + warp * 32 + lane;
+            const int n = n0 + sub * BN + wq * 32 + lane;
 #pragma unroll 1
-            for (int c0 = 0; c0 < TT; c0 += 16) {
+            for (int c0 = half * 16; c0 < TT; c0 += 16 * EH) {
                 if (c0 >= rows) break;
                 float v[16];
                 tmem_ld16(trow + sub * TT + c0, v);
@@ -420,9 +422,9 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
         float* part = reinterpret_cast<float*>(smem);
 #pragma unroll
         for (int sub = 0; sub < NB; ++sub) {
-            const int nn = sub * BN + warp * 32 + lane;
+            const int nn = sub * BN + wq * 32 + lane;
 #pragma unroll 1
-            for (int c0 = 0; c0 < TT; c0 += 16) {
+            for (int c0 = half * 16; c0 < TT; c0 += 16 * EH) {
                 if (c0 >= rows) break;
                 float v[16];
                 tmem_ld16(trow + sub * TT + c0, v);
@@ -433,19 +435,22 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
         }
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         const int r0 = split * rows / sp.S, r1 = (split + 1) * rows / sp.S;
+        // the two warp halves take [r0, rmid) and [rmid, r1) (4-row aligned)
+        const int rmid = r0 + min(r1 - r0, ((r1 - r0 + 7) / 8) * 4);
+        const int rb = half == 0 ? r0 : rmid, re = half == 0 ? rmid : r1;
         const uint32_t part_s = su32(part);
 #pragma unroll
         for (int sub = 0; sub < NB; ++sub) {
-            const int nn = sub * BN + warp * 32 + lane, n = n0 + nn;
+            const int nn = sub * BN + wq * 32 + lane, n = n0 + nn;
             if (n < N) {
-                int r = r0;
-                for (; r + 4 <= r1; r += 4) {   // 4 rows x S partials in flight
+                int r = rb;
+                for (; r + 4 <= re; r += 4) {   // 4 rows x S partials in flight
                     float acc[4];
                     dsmem_sum<4>(part_s + (uint32_t)((r * WR + nn) * 4), WR * 4, sp.S, acc);
 #pragma unroll
                     for (int u = 0; u < 4; ++u) epilogue<MODE, __nv_bfloat16>(e, m0 + r + u, n, N, acc[u]);
                 }
-                for (; r < r1; ++r) {
+                for (; r < re; ++r) {
                     float acc;
                     dsmem_sum<1>(part_s + (uint32_t)((r * WR + nn) * 4), WR * 4, sp.S, &acc);
                     epilogue<MODE, __nv_bfloat16>(e, m0 + r, n, N, acc);
@@ -463,9 +468,9 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
         float* blk = sp.ws + (int64_t)(tile * gridDim.x + group) * sp.S * TT * WR;
 #pragma unroll
         for (int sub = 0; sub < NB; ++sub) {
-            const int nn = sub * BN + warp * 32 + lane;
+            const int nn = sub * BN + wq * 32 + lane;
 #pragma unroll 1
-            for (int c0 = 0; c0 < TT; c0 += 16) {
+            for (int c0 = half * 16; c0 < TT; c0 += 16 * EH) {
                 if (c0 >= rows) break;
                 float v[16];
                 tmem_ld16(trow + sub * TT + c0, v);
@@ -477,18 +482,21 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
         __threadfence();
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         const int r0 = split * rows / sp.S, r1 = (split + 1) * rows / sp.S;
+        // the two warp halves take [r0, rmid) and [rmid, r1) (4-row aligned)
+        const int rmid = r0 + min(r1 - r0, ((r1 - r0 + 7) / 8) * 4);
+        const int rb = half == 0 ? r0 : rmid, re = half == 0 ? rmid : r1;
 #pragma unroll
         for (int sub = 0; sub < NB; ++sub) {
-            const int nn = sub * BN + warp * 32 + lane, n = n0 + nn;
+            const int nn = sub * BN + wq * 32 + lane, n = n0 + nn;
             if (n < N) {
-                int r = r0;
-                for (; r + 4 <= r1; r += 4) {   // 4 rows x S partials in flight
+                int r = rb;
+                for (; r + 4 <= re; r += 4) {   // 4 rows x S partials in flight
                     float acc[4];
                     l2_sum<4>(blk + (int64_t)r * WR + nn, (int64_t)TT * WR, WR, sp.S, acc);
 #pragma unroll
                     for (int u = 0; u < 4; ++u) epilogue<MODE, __nv_bfloat16>(e, m0 + r + u, n, N, acc[u]);
                 }
-                for (; r < r1; ++r) {
+                for (; r < re; ++r) {
                     float acc;
                     l2_sum<1>(blk + (int64_t)r * WR + nn, (int64_t)TT * WR, WR, sp.S, &acc);
                     epilogue<MODE, __nv_bfloat16>(e, m0 + r, n, N, acc);
@@ -505,7 +513,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
     const float* s_mean = reinterpret_cast<const float*>(tmem_slot + 4);
     const float* s_rstd = s_mean + TT;
     // per-thread column constants (NB == 1: one weight row n per thread)
-    const int n_t = n0 + warp * 32 + lane;
+    const int n_t = n0 + wq * 32 + lane;
     float g_n = 0.f, c_n = 0.f, e_n = 0.f;
     if (n_t < N) {
         if constexpr (stats) g_n = __ldg(e.xg + n_t);
@@ -596,7 +604,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
             a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
             const int idx = (lane >> 2) & 7, row = idx >> 1;
             if ((lane & 3) == 0 && row < count) {
-                float* dst = reinterpret_cast<float*>(&red[(r_local0 + row) * 4 + warp]);
+                float* dst = reinterpret_cast<float*>(&red[(r_local0 + row) * 4 + wq]);
                 dst[idx & 1] = a[0];
             }
         }
@@ -614,9 +622,9 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
         red = reinterpret_cast<float2*>(smem);
 #pragma unroll
         for (int sub = 0; sub < NB; ++sub) {
-            const int n = n0 + sub * BN + warp * 32 + lane;
+            const int n = n0 + sub * BN + wq * 32 + lane;
 #pragma unroll 1
-            for (int c0 = 0; c0 < TT; c0 += 16) {
+            for (int c0 = half * 16; c0 < TT; c0 += 16 * EH) {
                 if (c0 >= rows) break;
                 float v[16];
                 tmem_ld16(trow + sub * TT + c0, v);
@@ -646,9 +654,9 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
         red = reinterpret_cast<float2*>(smem + (size_t)rows * WR * 4);
 #pragma unroll
         for (int sub = 0; sub < NB; ++sub) {
-            const int nn = sub * BN + warp * 32 + lane;
+            const int nn = sub * BN + wq * 32 + lane;
 #pragma unroll 1
-            for (int c0 = 0; c0 < TT; c0 += 16) {
+            for (int c0 = half * 16; c0 < TT; c0 += 16 * EH) {
                 if (c0 >= rows) break;
                 float v[16];
                 tmem_ld16(trow + sub * TT + c0, v);
@@ -661,12 +669,15 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         if (threadIdx.x == 64) GPROBE(7);
         const int r0 = split * rows / sp.S, r1 = (split + 1) * rows / sp.S;
+        // the two warp halves take [r0, rmid) and [rmid, r1) (4-row aligned)
+        const int rmid = r0 + min(r1 - r0, ((r1 - r0 + 7) / 8) * 4);
+        const int rb = half == 0 ? r0 : rmid, re = half == 0 ? rmid : r1;
         const uint32_t part_s = su32(part);
 #pragma unroll
         for (int sub = 0; sub < NB; ++sub) {
-            const int nn = sub * BN + warp * 32 + lane, n = n0 + nn;
-            int r = r0;
-            for (; r + 4 <= r1; r += 4) {   // 4 rows x S partials in flight
+            const int nn = sub * BN + wq * 32 + lane, n = n0 + nn;
+            int r = rb;
+            for (; r + 4 <= re; r += 4) {   // 4 rows x S partials in flight
                 RowIn ri[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) ri[u] = pre(m0 + r + u, n);
@@ -677,7 +688,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
                 for (int u = 0; u < 4; ++u) nv[u] = put(m0 + r + u, n, acc[u], ri[u]);
                 stat4(r - r0, 4, nv[0], nv[1], nv[2], nv[3]);
             }
-            for (; r < r1; ++r) {
+            for (; r < re; ++r) {
                 const RowIn ri = pre(m0 + r, n);
                 float acc;
                 dsmem_sum<1>(part_s + (uint32_t)((r * WR + nn) * 4), WR * 4, sp.S, &acc);
@@ -700,9 +711,9 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
         red = reinterpret_cast<float2*>(smem);
 #pragma unroll
         for (int sub = 0; sub < NB; ++sub) {
-            const int nn = sub * BN + warp * 32 + lane;
+            const int nn = sub * BN + wq * 32 + lane;
 #pragma unroll 1
-            for (int c0 = 0; c0 < TT; c0 += 16) {
+            for (int c0 = half * 16; c0 < TT; c0 += 16 * EH) {
                 if (c0 >= rows) break;
                 float v[16];
                 tmem_ld16(trow + sub * TT + c0, v);
@@ -714,11 +725,14 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
         __threadfence();
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         const int r0 = split * rows / sp.S, r1 = (split + 1) * rows / sp.S;
+        // the two warp halves take [r0, rmid) and [rmid, r1) (4-row aligned)
+        const int rmid = r0 + min(r1 - r0, ((r1 - r0 + 7) / 8) * 4);
+        const int rb = half == 0 ? r0 : rmid, re = half == 0 ? rmid : r1;
 #pragma unroll
         for (int sub = 0; sub < NB; ++sub) {
-            const int nn = sub * BN + warp * 32 + lane, n = n0 + nn;
-            int r = r0;
-            for (; r + 4 <= r1; r += 4) {   // 4 rows x S partials in flight
+            const int nn = sub * BN + wq * 32 + lane, n = n0 + nn;
+            int r = rb;
+            for (; r + 4 <= re; r += 4) {   // 4 rows x S partials in flight
                 RowIn ri[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) ri[u] = pre(m0 + r + u, n);
@@ -729,7 +743,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
                 for (int u = 0; u < 4; ++u) nv[u] = put(m0 + r + u, n, acc[u], ri[u]);
                 stat4(r - r0, 4, nv[0], nv[1], nv[2], nv[3]);
             }
-            for (; r < r1; ++r) {
+            for (; r < re; ++r) {
                 const RowIn ri = pre(m0 + r, n);
                 float acc;
                 l2_sum<1>(blk + (int64_t)r * WR + nn, (int64_t)TT * WR, WR, sp.S, &acc);
