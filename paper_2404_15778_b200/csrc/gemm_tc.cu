@@ -43,7 +43,7 @@ namespace tc {
 constexpr int BN = 128;          // weight rows per sub-tile (UMMA M)
 constexpr int BK = 64;           // k per stage (one 128-byte swizzle row of bf16)
 constexpr int UK = 16;           // k per tcgen05.mma for 16-bit inputs
-constexpr int EH = 2;               // epilogue row halves: warps w and w + 4 share TMEM lane quarter w
+constexpr int EH = 2;               // epilogue row groups: warps w, w + 4 share TMEM lane quarter w (EH = 3 with 80 registers measured slower)
 constexpr int THREADS = 128 * EH;   // 8 warps: 0 producer, 1 MMA, 2 TMEM alloc / folded-LN stats; all drain
 
 template <int TT, int NB>
@@ -229,7 +229,7 @@ __device__ int g_gp_n, g_gp_k;
 // LayerNorm's row sums and X = bf16(x * g_next).  Compile-time, so the plain
 // kernels carry none of it.
 template <int TT, int MODE, int NB, bool PACKED, int LNF>
-__global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tw,
+__global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tw,
                                                              const __grid_constant__ CUtensorMap tx,
                                                              const __nv_bfloat16* __restrict__ wpk, int M, int N,
                                                              Split sp, Epi e, XNorm xn, TraceArg tr) {
@@ -435,9 +435,9 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
         }
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         const int r0 = split * rows / sp.S, r1 = (split + 1) * rows / sp.S;
-        // the two warp halves take [r0, rmid) and [rmid, r1) (4-row aligned)
-        const int rmid = r0 + min(r1 - r0, ((r1 - r0 + 7) / 8) * 4);
-        const int rb = half == 0 ? r0 : rmid, re = half == 0 ? rmid : r1;
+        // the EH warp groups take consecutive 4-row-aligned slices of [r0, r1)
+        const int rper = ((r1 - r0 + 4 * EH - 1) / (4 * EH)) * 4;
+        const int rb = r0 + min(r1 - r0, half * rper), re = r0 + min(r1 - r0, (half + 1) * rper);
         const uint32_t part_s = su32(part);
 #pragma unroll
         for (int sub = 0; sub < NB; ++sub) {
@@ -482,9 +482,9 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
         __threadfence();
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         const int r0 = split * rows / sp.S, r1 = (split + 1) * rows / sp.S;
-        // the two warp halves take [r0, rmid) and [rmid, r1) (4-row aligned)
-        const int rmid = r0 + min(r1 - r0, ((r1 - r0 + 7) / 8) * 4);
-        const int rb = half == 0 ? r0 : rmid, re = half == 0 ? rmid : r1;
+        // the EH warp groups take consecutive 4-row-aligned slices of [r0, r1)
+        const int rper = ((r1 - r0 + 4 * EH - 1) / (4 * EH)) * 4;
+        const int rb = r0 + min(r1 - r0, half * rper), re = r0 + min(r1 - r0, (half + 1) * rper);
 #pragma unroll
         for (int sub = 0; sub < NB; ++sub) {
             const int nn = sub * BN + wq * 32 + lane, n = n0 + nn;
@@ -669,9 +669,9 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         if (threadIdx.x == 64) GPROBE(7);
         const int r0 = split * rows / sp.S, r1 = (split + 1) * rows / sp.S;
-        // the two warp halves take [r0, rmid) and [rmid, r1) (4-row aligned)
-        const int rmid = r0 + min(r1 - r0, ((r1 - r0 + 7) / 8) * 4);
-        const int rb = half == 0 ? r0 : rmid, re = half == 0 ? rmid : r1;
+        // the EH warp groups take consecutive 4-row-aligned slices of [r0, r1)
+        const int rper = ((r1 - r0 + 4 * EH - 1) / (4 * EH)) * 4;
+        const int rb = r0 + min(r1 - r0, half * rper), re = r0 + min(r1 - r0, (half + 1) * rper);
         const uint32_t part_s = su32(part);
 #pragma unroll
         for (int sub = 0; sub < NB; ++sub) {
@@ -725,9 +725,9 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
         __threadfence();
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         const int r0 = split * rows / sp.S, r1 = (split + 1) * rows / sp.S;
-        // the two warp halves take [r0, rmid) and [rmid, r1) (4-row aligned)
-        const int rmid = r0 + min(r1 - r0, ((r1 - r0 + 7) / 8) * 4);
-        const int rb = half == 0 ? r0 : rmid, re = half == 0 ? rmid : r1;
+        // the EH warp groups take consecutive 4-row-aligned slices of [r0, r1)
+        const int rper = ((r1 - r0 + 4 * EH - 1) / (4 * EH)) * 4;
+        const int rb = r0 + min(r1 - r0, half * rper), re = r0 + min(r1 - r0, (half + 1) * rper);
 #pragma unroll
         for (int sub = 0; sub < NB; ++sub) {
             const int nn = sub * BN + wq * 32 + lane, n = n0 + nn;
