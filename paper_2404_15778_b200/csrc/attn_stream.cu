@@ -106,6 +106,23 @@ __device__ __forceinline__ void ld16_nowait(uint32_t taddr, float* v) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void ld8_nowait(uint32_t taddr, float* v) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+// CQ (8 / 16 / 32 / 64) consecutive columns
+template <int CQ>
+__device__ __forceinline__ void ldq_nowait(uint32_t taddr, float* v) {
+    if constexpr (CQ == 8) ld8_nowait(taddr, v);
+    else {
+#pragma unroll
+        for (int j0 = 0; j0 < CQ; j0 += 16) ld16_nowait(taddr + j0, v + j0);
+    }
+}
 __device__ __forceinline__ void ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void st16(uint32_t taddr, const float* v) {
     asm volatile(
@@ -119,15 +136,22 @@ __device__ __forceinline__ void st16(uint32_t taddr, const float* v) {
         "r"(__float_as_uint(v[15]))
         : "memory");
 }
+__device__ __forceinline__ void st8(uint32_t taddr, const float* v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+                 "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+                 "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+                 "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
+                 : "memory");
+}
 __device__ __forceinline__ void st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-// named barrier 1 over the four softmax warps
-__device__ __forceinline__ void sm_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
-__device__ __forceinline__ bool sm_vote_any(bool p) {
+// named barrier 1 + grp over the four warps of one softmax group
+__device__ __forceinline__ void sm_bar(int grp) { asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory"); }
+__device__ __forceinline__ bool sm_vote_any(bool p, int grp) {
     uint32_t r;
     asm volatile(
-        "{\n .reg .pred a, b;\n setp.ne.u32 a, %1, 0;\n bar.red.or.pred b, 1, 128, a;\n selp.u32 %0, 1, 0, b;\n}"
+        "{\n .reg .pred a, b;\n setp.ne.u32 a, %1, 0;\n bar.red.or.pred b, %2, 128, a;\n selp.u32 %0, 1, 0, b;\n}"
         : "=r"(r)
-        : "r"((uint32_t)p)
+        : "r"((uint32_t)p), "r"(1 + grp)
         : "memory");
     return r != 0;
 }
@@ -142,7 +166,8 @@ __device__ __forceinline__ float fast_exp2(float x) {
 // Intra-warp: transpose-reduce (lane L ends holding columns L*NQ/32 + i);
 // then the four warps' partials are combined in warp order by NQ threads.
 template <int NQ, bool MAX>
-__device__ __forceinline__ void col_reduce(float (&v)[NQ], float* red, float* fin, int wq, int lane, int tid) {
+__device__ __forceinline__ void col_reduce(float (&v)[NQ], float* red, float* fin, int wq, int lane, int tid,
+                                           int grp) {
     float w[NQ];
 #pragma unroll
     for (int i = 0; i < NQ; ++i) w[i] = v[i];
@@ -173,12 +198,12 @@ __device__ __forceinline__ void col_reduce(float (&v)[NQ], float* red, float* fi
 #pragma unroll
         for (int i = 0; i < PER; ++i) red[wq * NQ + (lane * NQ) / 32 + i] = w[i];
     }
-    sm_bar();
+    sm_bar(grp);
     if (tid < NQ) {
         const float a = red[tid], b = red[NQ + tid], c = red[2 * NQ + tid], d = red[3 * NQ + tid];
         fin[tid] = MAX ? fmaxf(fmaxf(a, b), fmaxf(c, d)) : (a + b) + (c + d);
     }
-    sm_bar();
+    sm_bar(grp);
 }
 
 // One work entry per (sequence, query tile, split), expanded over heads in the
@@ -244,8 +269,13 @@ struct Cfg {
     static constexpr int TMEM_COLS = 4 * NQ < 32 ? 32 : 4 * NQ;   // S0 S1 O0 O1
 };
 
+// softmax / epilogue groups of 4 warps: two (splitting the query columns)
+// where the registers allow, one for NQ = 64
+__host__ __device__ constexpr int softmax_groups(int nq) { return nq <= 32 ? 2 : 1; }
+__host__ __device__ constexpr int attn_threads(int nq) { return 64 + 128 * softmax_groups(nq); }
+
 template <int NQ>
-__global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
+__global__ void __launch_bounds__(attn_threads(NQ), 1) attn_stream_kernel(
     const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
     const __grid_constant__ CUtensorMap tv, Seqs seqs, const Work* __restrict__ work, int n_items, int H, int cap,
     float* __restrict__ part_o, float* __restrict__ part_ml, int max_splits, __nv_bfloat16* __restrict__ out,
@@ -253,6 +283,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
     const unsigned long long t_start = tr.buf ? gtimer() : 0ull;
     using Cf = Cfg<NQ>;
     constexpr int ST = Cf::STAGES;
+    constexpr int SG = softmax_groups(NQ), CQ = NQ / SG;
     if (threadIdx.x == 0) APROBE(0);
     extern __shared__ uint8_t smem_raw[];
     pdl_trigger();
@@ -284,9 +315,9 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
         for (int i = 0; i < Cf::NBAR; ++i) mbar_init(su32(&bars[i]), 1);
         // software arrivals: one per softmax warp
         for (int i = 0; i < 2; ++i) {
-            mbar_init(su32(&s_free[i]), 4);
-            mbar_init(su32(&p_full[i]), 4);
-            mbar_init(su32(&o_free[i]), 4);
+            mbar_init(su32(&s_free[i]), 4 * SG);
+            mbar_init(su32(&p_full[i]), 4 * SG);
+            mbar_init(su32(&o_free[i]), 4 * SG);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -420,11 +451,18 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
         }
         __syncwarp();
     } else {
-        // ---------------- softmax / epilogue (warps 2-5)
+        // ---------------- softmax / epilogue (SG groups of 4 warps from warp 2)
+        // group grp owns query columns [grp*CQ, (grp+1)*CQ) of the tile: all
+        // per-column rules are column-local, so splitting columns over groups
+        // changes no decision, only who computes it
         pdl_wait();
+        const int grp = (warp - 2) >> 2;
         const int wq = warp & 3;                 // TMEM lane quarter this warp may access
         const int key = wq * 32 + lane;          // key within the chunk (S^T lane) = head dim (O^T lane)
-        const int tid = threadIdx.x - 64;        // 0..127
+        const int tid = threadIdx.x - 64 - grp * 128;   // 0..127 within the group
+        const int c_off = grp * CQ;
+        float* red_g = red + grp * 4 * CQ;       // this group's [4][CQ] partials
+        float* fin_g = fin + c_off;
         const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
         const float C = 1.4426950408889634f / sqrtf((float)DH);   // log2(e) / sqrt(dh)
         // P^T row of this key: NQ bf16 (MN-major B operand), 16-byte chunks swizzled
@@ -437,21 +475,20 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
         while (items.next(wk, h)) {
             const int qn = wk.qn, off = wk.off, q0row = wk.q0row;
             const int L = off + qn, s0 = wk.split * SPLIT, ob = n & 1;
-            const int ncol = min(NQ, qn - wk.t0);   // valid query columns of the tile (uniform)
-            const int dlim = off + wk.t0;           // column j sees keys kp <= dlim + j
-            float l_t[NQ];
+            // valid query columns of this group (uniform; may be 0)
+            const int ncol = max(0, min(NQ, qn - wk.t0) - c_off);
+            const int dlim = off + wk.t0 + c_off;   // local column j sees keys kp <= dlim + j
+            float l_t[CQ];
 #pragma unroll
-            for (int j = 0; j < NQ; ++j) l_t[j] = 0.f;
+            for (int j = 0; j < CQ; ++j) l_t[j] = 0.f;
             for (int c = 0; c < wk.nch; ++c, ++g) {
                 const int sb = g & 1;
                 const bool first = c == 0;
                 mbar_wait(su32(&s_full[sb]), (g >> 1) & 1);
-                if (g < 4 && tid == 0) APROBE(12 + g);
+                if (g < 4 && threadIdx.x == 64) APROBE(12 + g);
                 fence_after();
-                float x[NQ];
-#pragma unroll
-                for (int j0 = 0; j0 < NQ; j0 += 16)
-                    if (j0 < ncol) ld16_nowait(tmem + lane_off + sb * NQ + j0, x + j0);
+                float x[CQ];
+                if (ncol > 0) ldq_nowait<CQ>(tmem + lane_off + sb * NQ + c_off, x);
                 ld_wait();
                 fence_before();
                 __syncwarp();
@@ -459,51 +496,61 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
                 const int cbase = s0 + c * CH, kp = cbase + key;
                 if (cbase + CH - 1 > dlim) {   // chunk crosses the causal diagonal / the end (uniform)
 #pragma unroll
-                    for (int j = 0; j < NQ; ++j)
+                    for (int j = 0; j < CQ; ++j)
                         if (!(kp <= dlim + j && kp < L)) x[j] = -INFINITY;
                 }
                 bool reduce = first;
                 if (!first) {
                     bool over = false;
 #pragma unroll
-                    for (int j = 0; j < NQ; ++j)
-                        if (j < ncol) over |= x[j] > thr[j];
-                    reduce = sm_vote_any(over);
+                    for (int j = 0; j < CQ; ++j)
+                        if (j < ncol) over |= x[j] > thr[c_off + j];
+                    reduce = sm_vote_any(over, grp);
                 }
                 if (reduce) {
                     // exact chunk max; a column's reference moves only when its own
                     // scores leave the window (first chunk: set unconditionally)
-                    col_reduce<NQ, true>(x, red, fin, wq, lane, tid);
+                    col_reduce<CQ, true>(x, red_g, fin_g, wq, lane, tid, grp);
                     bool resc = false;
-                    if (tid < NQ) {
-                        const float cm = fin[tid] * C, mo = first ? -INFINITY : mref[tid];
+                    if (tid < CQ) {
+                        const int cc = c_off + tid;
+                        const float cm = fin_g[tid] * C, mo = first ? -INFINITY : mref[cc];
                         float a = 1.f;
                         if (first || cm > mo + TH) {
                             a = mo == -INFINITY ? 0.f : fast_exp2(mo - cm);
                             resc = !first;
-                            mref[tid] = cm;
-                            thr[tid] = (cm + TH) / C;
+                            mref[cc] = cm;
+                            thr[cc] = (cm + TH) / C;
                         }
-                        alph[tid] = a;
+                        alph[cc] = a;
                     }
-                    const bool any_rescale = sm_vote_any(resc);   // also publishes mref / thr / alph
+                    const bool any_rescale = sm_vote_any(resc, grp);   // also publishes mref / thr / alph
                     if (!first) {
 #pragma unroll
-                        for (int j = 0; j < NQ; ++j) l_t[j] *= alph[j];
+                        for (int j = 0; j < CQ; ++j) l_t[j] *= alph[c_off + j];
                     }
                     if (any_rescale) {
-                        // O^T holds chunks < c: wait for the previous PV, rescale its columns
+                        // O^T holds chunks < c: wait for the previous PV, rescale this group's columns
                         mbar_wait(su32(&p_free[(g - 1) & 1]), ((g - 1) >> 1) & 1);
                         fence_after();
-                        const uint32_t to = tmem + lane_off + 2 * NQ + ob * NQ;
-#pragma unroll
-                        for (int j0 = 0; j0 < NQ; j0 += 16) {
-                            float o[16];
-                            ld16_nowait(to + j0, o);
+                        const uint32_t to = tmem + lane_off + 2 * NQ + ob * NQ + c_off;
+                        if constexpr (CQ == 8) {
+                            float o[8];
+                            ld8_nowait(to, o);
                             ld_wait();
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) o[j] *= alph[j0 + j];
-                            st16(to + j0, o);
+                            for (int j = 0; j < 8; ++j) o[j] *= alph[c_off + j];
+                            st8(to, o);
+                        } else {
+#pragma unroll
+                            for (int j0 = 0; j0 < CQ; j0 += 16) {
+                                float o[16];
+                                ld16_nowait(to + j0, o);
+                                ld_wait();
+#pragma unroll
+                                for (int j = 0; j < 16; ++j) o[j] *= alph[c_off + j0 + j];
+                                st16(to + j0, o);
+                            }
                         }
                         st_wait();
                         fence_before();
@@ -513,12 +560,12 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
                 if (g >= 2) mbar_wait(su32(&p_free[sb]), ((g >> 1) - 1) & 1);
                 const uint32_t pb = base + Cf::OFF_P + sb * Cf::P_BUF + prow;
 #pragma unroll
-                for (int j0 = 0; j0 < NQ; j0 += 8) {
+                for (int j0 = 0; j0 < CQ; j0 += 8) {
                     if (j0 >= ncol) break;   // columns past the tile's rows: never read back
                     uint32_t pk[4];
 #pragma unroll
                     for (int u = 0; u < 8; u += 2) {
-                        const float4 m4 = *reinterpret_cast<const float4*>(mref + j0 + (u & 4));
+                        const float4 m4 = *reinterpret_cast<const float4*>(mref + c_off + j0 + (u & 4));
                         const float ma = (u & 2) ? m4.z : m4.x, mb = (u & 2) ? m4.w : m4.y;
                         const float p0 = fast_exp2(fmaf(x[j0 + u], C, -ma));
                         const float p1 = fast_exp2(fmaf(x[j0 + u + 1], C, -mb));
@@ -527,7 +574,7 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
                         __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
                         pk[u >> 1] = *reinterpret_cast<uint32_t*>(&b2);
                     }
-                    const uint32_t dst = pb + ((((uint32_t)j0 >> 3) ^ pswz) << 4);
+                    const uint32_t dst = pb + (((((uint32_t)(c_off + j0)) >> 3) ^ pswz) << 4);
                     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(pk[0]), "r"(pk[1]),
                                  "r"(pk[2]), "r"(pk[3])
                                  : "memory");
@@ -535,39 +582,38 @@ __global__ void __launch_bounds__(THREADS, 1) attn_stream_kernel(
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // P -> tensor core
                 __syncwarp();
                 if (lane == 0) mbar_arrive(su32(&p_full[sb]));
-                if (g < 4 && tid == 0) APROBE(16 + g);
+                if (g < 4 && threadIdx.x == 64) APROBE(16 + g);
             }
             // ---- epilogue: l per column (fixed-order block sum), O^T lane = head dim
-            col_reduce<NQ, false>(l_t, red, fin, wq, lane, tid);
-            if (n < 2 && tid == 0) APROBE(20 + n);
+            col_reduce<CQ, false>(l_t, red_g, fin_g, wq, lane, tid, grp);
+            if (n < 2 && threadIdx.x == 64) APROBE(20 + n);
             mbar_wait(su32(&o_full[ob]), (n >> 1) & 1);
-            if (n < 2 && tid == 0) APROBE(22 + n);
+            if (n < 2 && threadIdx.x == 64) APROBE(22 + n);
             fence_after();
-            float o[NQ];
-#pragma unroll
-            for (int j0 = 0; j0 < NQ; j0 += 16) ld16_nowait(tmem + lane_off + 2 * NQ + ob * NQ + j0, o + j0);
+            float o[CQ];
+            if (ncol > 0) ldq_nowait<CQ>(tmem + lane_off + 2 * NQ + ob * NQ + c_off, o);
             ld_wait();
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(su32(&o_free[ob]));
 #pragma unroll
-            for (int j = 0; j < NQ; ++j) {
-                const int t = wk.t0 + j;
-                if (t >= qn || off + t < s0) continue;   // padded row / row does not see this split
+            for (int j = 0; j < CQ; ++j) {
+                const int t = wk.t0 + c_off + j;
+                if (j >= ncol || off + t < s0) continue;   // padded row / row does not see this split
                 const int row = q0row + t;
-                const float l = fin[j];
+                const float l = fin_g[j];
                 if (off + t < SPLIT) {   // whole history in split 0: normalised output
                     out[((int64_t)row * H + h) * DH + key] = __float2bfloat16_rn(o[j] / l);
                 } else {
                     const int64_t idx = ((int64_t)row * H + h) * max_splits + wk.split;
                     part_o[idx * DH + key] = o[j];
                     if (key == 0) {
-                        part_ml[idx * 2] = mref[j] * 0.6931471805599453f;   // natural-log units for the combine
+                        part_ml[idx * 2] = mref[c_off + j] * 0.6931471805599453f;   // natural-log units for the combine
                         part_ml[idx * 2 + 1] = l;
                     }
                 }
             }
-            if (n < 2 && tid == 0) APROBE(24 + n);
+            if (n < 2 && threadIdx.x == 64) APROBE(24 + n);
             ++n;
         }
     }
@@ -628,7 +674,7 @@ static void launch(bass_ctx* ctx, const AttnPlan& p, const CUtensorMap& tk, cons
     }
     const int n_items = nw * p.H;
     const int grid = std::max(1, std::min(n_items, ctx->sm_count));
-    BASS_CUDA(launch_pdl(attn_stream_kernel<NQ>, dim3(grid), dim3(THREADS), (size_t)Cf::SMEM, ctx->stream, p.tq, tk,
+    BASS_CUDA(launch_pdl(attn_stream_kernel<NQ>, dim3(grid), dim3(attn_threads(NQ)), (size_t)Cf::SMEM, ctx->stream, p.tq, tk,
                          tv, seqs, wp, n_items, p.H, p.cap, po, pml, p.mc, out, ctx->trace(grid, BASS_TR_ATTN)));
 }
 
