@@ -115,12 +115,14 @@ __device__ __forceinline__ void ld8_nowait(uint32_t taddr, float* v) {
     for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 // CQ (8 / 16 / 32 / 64) consecutive columns
+// (16-column chunks at or past `ncol` valid columns are not loaded)
 template <int CQ>
-__device__ __forceinline__ void ldq_nowait(uint32_t taddr, float* v) {
+__device__ __forceinline__ void ldq_nowait(uint32_t taddr, float* v, int ncol) {
     if constexpr (CQ == 8) ld8_nowait(taddr, v);
     else {
 #pragma unroll
-        for (int j0 = 0; j0 < CQ; j0 += 16) ld16_nowait(taddr + j0, v + j0);
+        for (int j0 = 0; j0 < CQ; j0 += 16)
+            if (j0 < ncol) ld16_nowait(taddr + j0, v + j0);
     }
 }
 __device__ __forceinline__ void ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
@@ -456,7 +458,7 @@ __global__ void __launch_bounds__(attn_threads(NQ), 1) attn_stream_kernel(
         // per-column rules are column-local, so splitting columns over groups
         // changes no decision, only who computes it
         pdl_wait();
-        const int grp = (warp - 2) >> 2;
+        const int grp = SG == 1 ? 0 : (warp - 2) >> 2;
         const int wq = warp & 3;                 // TMEM lane quarter this warp may access
         const int key = wq * 32 + lane;          // key within the chunk (S^T lane) = head dim (O^T lane)
         const int tid = threadIdx.x - 64 - grp * 128;   // 0..127 within the group
@@ -488,7 +490,7 @@ __global__ void __launch_bounds__(attn_threads(NQ), 1) attn_stream_kernel(
                 if (g < 4 && threadIdx.x == 64) APROBE(12 + g);
                 fence_after();
                 float x[CQ];
-                if (ncol > 0) ldq_nowait<CQ>(tmem + lane_off + sb * NQ + c_off, x);
+                if (ncol > 0) ldq_nowait<CQ>(tmem + lane_off + sb * NQ + c_off, x, ncol);
                 ld_wait();
                 fence_before();
                 __syncwarp();
@@ -591,7 +593,7 @@ __global__ void __launch_bounds__(attn_threads(NQ), 1) attn_stream_kernel(
             if (n < 2 && threadIdx.x == 64) APROBE(22 + n);
             fence_after();
             float o[CQ];
-            if (ncol > 0) ldq_nowait<CQ>(tmem + lane_off + 2 * NQ + ob * NQ + c_off, o);
+            if (ncol > 0) ldq_nowait<CQ>(tmem + lane_off + 2 * NQ + ob * NQ + c_off, o, CQ);
             ld_wait();
             fence_before();
             __syncwarp();
