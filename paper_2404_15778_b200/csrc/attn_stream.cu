@@ -252,11 +252,13 @@ __device__ unsigned long long* g_attn_probe;
     } while (0)
 #endif
 
-template <int NQ>
+// ST: K/V ring stages.  NQ = 16 has two builds: 2 stages for short
+// histories (decode / verify: items of 1-3 chunks, measured faster end to
+// end) and 3 for long ones (the launch picks by the longest history);
+// NQ = 64 is smem bound at 2.
+template <int NQ, int ST = (NQ == 32 ? 3 : 2)>
 struct Cfg {
-    // NQ = 16 (decode / verify up to 15 drafts): 2 stages measured 0.7 %
-    // faster end to end than 3 (items have 1-3 chunks); NQ = 64: smem bound
-    static constexpr int STAGES = NQ == 32 ? 3 : 2;
+    static constexpr int STAGES = ST;
     static constexpr int KV_TILE = CH * 128;      // 128 rows x 64 bf16 (one 128B-swizzle sub-tile)
     static constexpr int STAGE = 4 * KV_TILE;     // K0 K1 V0 V1
     static constexpr int R_TILE = NQ * 128;       // NQ rows x 64 bf16: one sub-tile of Q or P
@@ -276,14 +278,14 @@ struct Cfg {
 __host__ __device__ constexpr int softmax_groups(int nq) { return nq <= 64 ? 2 : 1; }
 __host__ __device__ constexpr int attn_threads(int nq) { return 64 + 128 * softmax_groups(nq); }
 
-template <int NQ>
+template <int NQ, int STG>
 __global__ void __launch_bounds__(attn_threads(NQ), 1) attn_stream_kernel(
     const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
     const __grid_constant__ CUtensorMap tv, Seqs seqs, const Work* __restrict__ work, int n_items, int H, int cap,
     float* __restrict__ part_o, float* __restrict__ part_ml, int max_splits, __nv_bfloat16* __restrict__ out,
     TraceArg tr) {
     const unsigned long long t_start = tr.buf ? gtimer() : 0ull;
-    using Cf = Cfg<NQ>;
+    using Cf = Cfg<NQ, STG>;
     constexpr int ST = Cf::STAGES;
     constexpr int SG = softmax_groups(NQ), CQ = NQ / SG;
     if (threadIdx.x == 0) APROBE(0);
@@ -665,18 +667,26 @@ static const CUtensorMap& kv_map(const void* ptr, int64_t rows) {
     return it->second;
 }
 
-template <int NQ>
+template <int NQ, int STG = Cfg<NQ>::STAGES>
 static void launch(bass_ctx* ctx, const AttnPlan& p, const CUtensorMap& tk, const CUtensorMap& tv, const Seqs& seqs,
                    const Work* wp, int nw, float* po, float* pml, __nv_bfloat16* out) {
-    using Cf = Cfg<NQ>;
+    if constexpr (NQ == 16 && STG == 2) {
+        // long histories stream better with a third K/V stage
+        if (p.max_len > 768) {
+            launch<16, 3>(ctx, p, tk, tv, seqs, wp, nw, po, pml, out);
+            return;
+        }
+    }
+    using Cf = Cfg<NQ, STG>;
     static bool attr = false;
     if (!attr) {
-        BASS_CUDA(cudaFuncSetAttribute(attn_stream_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
+        BASS_CUDA(cudaFuncSetAttribute(attn_stream_kernel<NQ, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Cf::SMEM));
         attr = true;
     }
     const int n_items = nw * p.H;
     const int grid = std::max(1, std::min(n_items, ctx->sm_count));
-    BASS_CUDA(launch_pdl(attn_stream_kernel<NQ>, dim3(grid), dim3(attn_threads(NQ)), (size_t)Cf::SMEM, ctx->stream, p.tq, tk,
+    BASS_CUDA(launch_pdl(attn_stream_kernel<NQ, STG>, dim3(grid), dim3(attn_threads(NQ)), (size_t)Cf::SMEM, ctx->stream, p.tq, tk,
                          tv, seqs, wp, n_items, p.H, p.cap, po, pml, p.mc, out, ctx->trace(grid, BASS_TR_ATTN)));
 }
 
@@ -762,6 +772,7 @@ void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, in
     plan.tq = map2d(q, M, (int64_t)H * DH, (int64_t)H * DH, NQ);
     plan.NQ = NQ;
     plan.pad_len = strategy == BASS_PAD ? max_L : 0;
+    plan.max_len = max_L;
     plan.strategy = strategy;
     plan.H = H;
     plan.cap = cap;
