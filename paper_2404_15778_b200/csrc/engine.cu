@@ -26,7 +26,7 @@ struct bass_engine {
     int strategy = BASS_RAGGED;
     static constexpr int kPstride = kMaxEmit;
     int32_t* proposals = nullptr;     // [n_slots][kPstride]
-    DevBuf vlog, dlog, vamax, vlse, accf, corr, bonus, scratch, slotbuf, stepbuf, align_tok, arena, pick;
+    DevBuf vlog, dlog, vamax, vlse, accf, corr, bonus, scratch, slotbuf, stepbuf, align_tok, arena, pick, shaped;
     SlotStep* step_host = nullptr;    // pinned
     int32_t* small_host = nullptr;    // pinned staging for tiny per-step arrays
 };
@@ -149,7 +149,7 @@ int bass_engine_destroy(bass_engine* e) {
     cudaFreeHost(e->step_host);
     cudaFreeHost(e->small_host);
     for (DevBuf* b : {&e->vlog, &e->dlog, &e->vamax, &e->vlse, &e->accf, &e->corr, &e->bonus, &e->scratch,
-                      &e->slotbuf, &e->stepbuf, &e->align_tok, &e->arena, &e->pick})
+                      &e->slotbuf, &e->stepbuf, &e->align_tok, &e->arena, &e->pick, &e->shaped})
         b->release();
     delete e;
     return BASS_OK;
@@ -358,7 +358,10 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                 VerifyArgs va{nA, l, V, r->temperature, r->top_p, r->seed, d_slot, d_sid, d_com,
                               e->proposals, bass_engine::kPstride, vlog, dlog, scratch, accf, corr, btok};
                 ProfScope prof(c, BASS_PROF_SAMPLE, (double)R * V * 8);
-                verify_sampled_kernel<<<dim3(l + 1, nA), SM_THREADS, 0, st>>>(va);
+                Shaped* shp = (Shaped*)e->shaped.need((size_t)nA * (l + 1) * 2 * sizeof(Shaped), st);
+                verify_shape_kernel<<<dim3(l + 1, nA, 2), SM_THREADS, 0, st>>>(va, shp);
+                launched(c);
+                verify_accept_kernel<<<dim3(l + 1, nA), SM_THREADS, 0, st>>>(va, shp);
                 launched(c);
             }
             StepArgs sa{nA, l, V, d_slot, d_com, d_gen, e->proposals, bass_engine::kPstride, vlog, vamax, vlse,

@@ -414,6 +414,10 @@ static __global__ void __launch_bounds__(SM_THREADS) shape_sample_kernel(const f
     if (threadIdx.x == 0) tok[blockIdx.x] = t;
 }
 
+// accept / resample given both rows' shaping (see accept_block)
+BASS_DEV int accept_shaped(const float* qrow, const float* prow, int V, const double* eq, const double* ep,
+                           const Shaped& sq, const Shaped& sp, int tok, Pcg64& g, ShapeSmem& sm);
+
 // accept / resample for one (q row, p row, token, VERIFY generator);
 // returns corrected token or -1 when accepted; -2 on zero draft probability.
 BASS_DEV int accept_block(const float* qrow, const float* prow, int V, double T, double top_p,
@@ -423,6 +427,11 @@ BASS_DEV int accept_block(const float* qrow, const float* prow, int V, double T,
     __syncthreads();
     shape_row(prow, V, T, top_p, ep, sm);
     const Shaped sp = sm.sh;
+    return accept_shaped(qrow, prow, V, eq, ep, sq, sp, tok, g, sm);
+}
+
+BASS_DEV int accept_shaped(const float* qrow, const float* prow, int V, const double* eq, const double* ep,
+                           const Shaped& sq, const Shaped& sp, int tok, Pcg64& g, ShapeSmem& sm) {
     const double px = sh_prob(sp, prow, ep, tok);
     const double qx = sh_prob(sq, qrow, eq, tok);
     if (px <= 0.0) return -2;
@@ -596,6 +605,54 @@ static __global__ void __launch_bounds__(SM_THREADS) verify_sampled_kernel(Verif
     }
     Pcg64 g = pcg64_from_key(a.seed, uint64_t(sid), 1u, uint64_t(pos));
     const int c = accept_block(q, p, a.V, a.T, a.top_p, eq, ep, tok, g, sm);
+    if (threadIdx.x == 0) {
+        a.acc_flag[i * (l + 1) + j] = c == -1;
+        a.corr[i * (l + 1) + j] = c;
+        if (j == l) a.bonus_tok[i] = tok;
+    }
+}
+
+// Verify, split in two launches so the 2 (l+1) nA row shapings run on as
+// many CTAs: (1) shape every main row q (z = 0) and draft row p (z = 1),
+// keeping e in the scratch and the Shaped summary in `sh`; (2) per (j, i):
+// bonus draw (j = l) and accept / resample — the same arithmetic, RNG
+// streams and draws as verify_sampled_kernel.
+static __global__ void __launch_bounds__(SM_THREADS) verify_shape_kernel(VerifyArgs a, Shaped* __restrict__ sh) {
+    __shared__ ShapeSmem sm;
+    pdl_trigger();
+    pdl_wait();
+    const int j = blockIdx.x, i = blockIdx.y, z = blockIdx.z, l = a.l;
+    const int64_t r = (int64_t)i * (l + 1) + j;
+    const float* row = z == 0 ? a.vlog + r * a.V : a.dlog + (int64_t)(j * a.nA + i) * a.V;
+    double* e = a.scratch + r * 2 * a.V + (z == 0 ? 0 : a.V);
+    shape_row(row, a.V, a.T, a.top_p, e, sm);
+    if (threadIdx.x == 0) sh[r * 2 + z] = sm.sh;
+}
+
+static __global__ void __launch_bounds__(SM_THREADS) verify_accept_kernel(VerifyArgs a,
+                                                                          const Shaped* __restrict__ sh) {
+    __shared__ ShapeSmem sm;
+    pdl_trigger();
+    pdl_wait();
+    const int j = blockIdx.x, i = blockIdx.y, l = a.l;
+    const int slot = a.slot[i], sid = a.sid[slot], pos = a.committed[i] + j;
+    const int64_t r = (int64_t)i * (l + 1) + j;
+    const float* q = a.vlog + r * a.V;
+    const float* p = a.dlog + (int64_t)(j * a.nA + i) * a.V;
+    const double* eq = a.scratch + r * 2 * a.V;
+    const double* ep = eq + a.V;
+    const Shaped sq = sh[r * 2], sp = sh[r * 2 + 1];
+    int tok;
+    if (j < l) {
+        tok = a.proposals[slot * a.pstride + j];
+    } else {
+        Pcg64 gd = pcg64_from_key(a.seed, uint64_t(sid), 0u, uint64_t(pos));
+        const double ub = pcg64_double(gd);
+        tok = inverse_cdf_block(a.V, ub, [&](int k) { return sh_prob(sp, p, ep, k); }, sm);
+        __syncthreads();
+    }
+    Pcg64 g = pcg64_from_key(a.seed, uint64_t(sid), 1u, uint64_t(pos));
+    const int c = accept_shaped(q, p, a.V, eq, ep, sq, sp, tok, g, sm);
     if (threadIdx.x == 0) {
         a.acc_flag[i * (l + 1) + j] = c == -1;
         a.corr[i * (l + 1) + j] = c;
