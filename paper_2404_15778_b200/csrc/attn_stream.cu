@@ -275,7 +275,7 @@ struct Cfg {
 
 // softmax / epilogue groups of 4 warps: two (splitting the query columns)
 // where the registers allow, one for NQ = 64
-__host__ __device__ constexpr int softmax_groups(int nq) { return nq == 64 ? 4 : 2; }
+__host__ __device__ constexpr int softmax_groups(int nq) { return nq >= 32 ? 4 : 2; }
 __host__ __device__ constexpr int attn_threads(int nq) { return 64 + 128 * softmax_groups(nq); }
 
 template <int NQ, int STG>
