@@ -217,7 +217,10 @@ def forward_ragged(w: dict, cache: RaggedCache, slots, blocks,
         ids = np.asarray(blk, dtype=np.int64)
         if ids.min() < 0 or ids.max() >= g.vocab_size:
             raise ValueError(f"sequence {s}: token id outside vocab")
-        xs.append(w["tok_emb"][ids] + w["pos_emb"][np.arange(off, off + len(blk))])
+        # float64 residual stream even when the tables are stored on a
+        # narrower grid (bf16-rounded float32 parity weights)
+        xs.append(np.asarray(w["tok_emb"][ids], dtype=np.float64)
+                  + w["pos_emb"][np.arange(off, off + len(blk))])
     attend = attend_pad if strategy == "pad" else attend_split
     for li, lay in enumerate(w["layers"]):
         qs = []

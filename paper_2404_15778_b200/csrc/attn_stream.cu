@@ -678,12 +678,11 @@ static void launch(bass_ctx* ctx, const AttnPlan& p, const CUtensorMap& tk, cons
         }
     }
     using Cf = Cfg<NQ, STG>;
-    static bool attr = false;
-    if (!attr) {
+    static unsigned attr = 0;
+    once_per_device(attr, [] {
         BASS_CUDA(cudaFuncSetAttribute(attn_stream_kernel<NQ, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        Cf::SMEM));
-        attr = true;
-    }
+    });
     const int n_items = nw * p.H;
     const int grid = std::max(1, std::min(n_items, ctx->sm_count));
     BASS_CUDA(launch_pdl(attn_stream_kernel<NQ, STG>, dim3(grid), dim3(attn_threads(NQ)), (size_t)Cf::SMEM, ctx->stream, p.tq, tk,
@@ -693,6 +692,8 @@ static void launch(bass_ctx* ctx, const AttnPlan& p, const CUtensorMap& tk, cons
 }  // namespace ast
 
 int stream_split_len() { return ast::SPLIT; }
+
+bool tc_attention_supported(int dtype, int dh) { return dtype == BASS_BF16 && dh == ast::DH; }
 
 // Plan: work items (seq, q tile, split, chunks seen) — RAGGED/SPLIT exact,
 // PAD over the padded [max q] x [max L] grid (padded keys streamed, masked).
@@ -778,7 +779,6 @@ void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, in
     plan.cap = cap;
     plan.n_slots = n_slots;
     plan.mc = (cap + SPLIT - 1) / SPLIT;   // splits per row (partial buffer stride)
-    plan.fused = false;
     plan.stream = true;
     plan.needs_combine = multi;
     plan.first = std::move(first);

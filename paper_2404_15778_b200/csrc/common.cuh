@@ -47,6 +47,19 @@ BASS_DEV void trace_end(const TraceArg& tr, unsigned long long t0) {
     }
 }
 
+// cudaFuncSetAttribute is per device: run `f` once per (call site, device).
+// `mask` is the call site's static bit set of devices already configured.
+template <typename F>
+inline void once_per_device(unsigned& mask, F&& f) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned bit = 1u << (dev & 31);
+    if (!(mask & bit)) {
+        f();
+        mask |= bit;
+    }
+}
+
 // Launch with programmatic stream serialization (PDL).
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -58,8 +71,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    static const bool pdl = !(getenv("BASS_PDL") && atoi(getenv("BASS_PDL")) == 0);   // BASS_PDL=0: debug
-    at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);

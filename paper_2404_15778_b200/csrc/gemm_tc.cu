@@ -156,9 +156,10 @@ struct Split {
 // written by the previous residual epilogue, and the row mean / rstd from
 // the per-(tile, row) sums that epilogue emitted (`stats`, `stat_tiles`).
 struct XNorm {
-    const float* stats;    // [stat_tiles][M] {sum, sum of squares}
+    const float* stats;    // [stat_tiles][M] {sum, sum of squares} of c = x - K (K: the producer's row shift)
     const float* c;        // [N] sum_k g_k W[n, k]
     const float* e;        // [N] sum_k b_k W[n, k]
+    float* kmean;          // [M] row shift K on entry; the tile-0 / split-0 CTA leaves K + mean(c) = mean(x)
     int stat_tiles;
 };
 
@@ -375,12 +376,27 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
                             sq += v[u].y;
                         }
                 }
+                    // sums are of c = x - K (K = the producer's row shift ~ mean):
+                // `mean` is mean(c) = mean(x) - K, var(x) = E[c^2] - mean(c)^2
                 mean = sm / (float)K;
                 const float var = fmaxf(sq / (float)K - mean * mean, 0.f);
                 rstd = 1.0f / sqrtf(var + 1e-5f);
             }
             s_mean[r] = mean;
             s_rstd[r] = rstd;
+            // the row's exact mean for the next residual producer's shift (one
+            // writer per row; it is the only CTA of this launch touching kmean)
+            if (xn.kmean && tile == 0 && split == 0 && m < M) xn.kmean[m] = __ldcg(xn.kmean + m) + mean;
+        }
+    } else if (LNF == 2 && warp == 2) {
+        // ---- residual producer (warp 2, idle during the main loop): each row's
+        // shift K = the mean of the stream this GEMM adds into (left in kmean by
+        // the LayerNorm consumer before it); the epilogue centres on it
+        float* s_shift = reinterpret_cast<float*>(tmem_slot + 4);   // [TT]
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        for (int r = lane; r < TT; r += 32) {
+            const int m = m0 + r;
+            s_shift[r] = m < M ? __ldcg(e.shift + m) : 0.f;
         }
     }
     __syncwarp();
@@ -388,7 +404,7 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
     // ---- epilogue: TMEM lane = weight row n0 + sub*128 + 32*warp + lane; columns = tokens
     asm volatile("griddepcontrol.wait;" ::: "memory");   // previous kernel's writes visible
     if (threadIdx.x == 64) GPROBE(4);
-    if constexpr (XN) __syncthreads();                    // row mean / rstd (warp 2) visible
+    if constexpr (LNF != 0) __syncthreads();              // row mean / rstd or shift (warp 2) visible
     mbar_wait(su32(&bars[2 * C::STAGES]), 0);
     if (threadIdx.x == 64) GPROBE(5);
     fence_after();
@@ -559,9 +575,11 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
         float nv = 0.f;
         if (n < N) {
             if constexpr (stats) {
-                nv = ri.x + acc;
-                e.x[(int64_t)m * N + n] = nv;
-                // X of the next GEMM (its LayerNorm folded): bf16(x * g_next)
+                const float xnew = ri.x + acc;
+                e.x[(int64_t)m * N + n] = xnew;
+                // X of the next GEMM (its LayerNorm folded): bf16((x - K) * g_next);
+                // the statistics are of the centred value too
+                nv = xnew - s_mean[m - m0];
                 e.xb[(int64_t)m * N + n] = __float2bfloat16_rn(nv * g_n);
             } else {
                 if constexpr (XN) {
@@ -822,32 +840,23 @@ static State& state(bass_model& m) {
     return *static_cast<State*>(m.tc_state);
 }
 
-// Split count from (N, K) only — never from M — so a row's reduction order
-// (and hence its bits) does not depend on how many rows share the launch.
-// The table holds the benchmark's projection shapes (profiles/r1_gemm_*);
-// elsewhere: the largest split (<= 8, >= 4 k-blocks per CTA) that keeps the
-// 128-row tiles within ~1.75 CTAs per SM.
+// Split count from (N, K) and the SM count only — never from M — so a row's
+// reduction order (and hence its bits) does not depend on how many rows share
+// the launch.  Rule (fit to the in-chain sweeps of profiles/r1_gemm_nb_split_sweep.txt,
+// profiles/r1_split_chain_final.txt): the largest S <= 8 that divides the k
+// blocks evenly, leaves >= 4 k blocks per CTA and keeps the 128-row tiles x S
+// within 1.75 CTAs per SM; S = 2 may fill the two-CTA-per-SM wave (<= 2 per SM)
+// when each CTA still streams >= 32 k blocks.  At every C2 shape this gives the
+// measured optimum (qkv 2, o 6, fc 2, proj 6, head 1; draft 4 / 8 / 4 / 8 / 1).
 static int choose_splits(int sm_count, int N, int K) {
-    static const struct { int N, K, S; } tuned[] = {
-        {13824, 4608, 2}, {4608, 4608, 6}, {18432, 4608, 2}, {4608, 18432, 6}, {50272, 4608, 1},
-        {6144, 2048, 4},  {2048, 2048, 8}, {8192, 2048, 4},  {2048, 8192, 8},  {50272, 2048, 1}};
-    if (const char* ov = getenv("BASS_SPLIT_OVERRIDE")) {   // tuning only: "NxK:S,NxK:S"
-        int n_, k_, s_, used = 0;
-        for (const char* q = ov; sscanf(q, "%dx%d:%d%n", &n_, &k_, &s_, &used) == 3; q += used + (q[used] == ',')) {
-            if (n_ == N && k_ == K) return s_;
-            if (!q[used]) break;
-        }
-    }
-    if (sm_count == 148 && !getenv("BASS_NO_SPLIT_TABLE"))
-        for (const auto& t : tuned)
-            if (t.N == N && t.K == K) return t.S;
     const int n_tiles = (N + BN - 1) / BN, k_iters = K / BK;
-    const int slots = sm_count * 7 / 4;
-    static const int cap_s = getenv("BASS_MAX_SPLIT") ? atoi(getenv("BASS_MAX_SPLIT")) : 8;
-    int best_s = 1;
-    for (int s = 2; s <= cap_s; ++s)
-        if (n_tiles * s <= slots && k_iters / s >= 4) best_s = s;
-    return best_s;
+    int best = 1;
+    for (int s = 2; s <= MAX_S; ++s) {
+        if (k_iters % s != 0 || k_iters / s < 4) continue;
+        const int ctas = n_tiles * s;
+        if (ctas * 4 <= sm_count * 7 || (s == 2 && ctas <= 2 * sm_count && k_iters / s >= 32)) best = s;
+    }
+    return best;
 }
 
 struct LaunchArgs {
@@ -863,12 +872,11 @@ template <int TT, int MODE, bool PACKED, int LNF>
 static void launch_k(bass_model& m, const LaunchArgs& a, const Epi& e) {
     constexpr int NB = 1;   // (NB = 2 measured slower at every benchmark shape: profiles/r1_gemm_nb_split_sweep.txt)
     using C = Cfg<TT, NB>;
-    static bool attr = false;
-    if (!attr) {
+    static unsigned attr = 0;
+    once_per_device(attr, [] {
         BASS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<TT, MODE, NB, PACKED, LNF>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-        attr = true;
-    }
+    });
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((a.M + TT - 1) / TT, a.sp.S, (a.N + NB * BN - 1) / (NB * BN));
     cfg.blockDim = dim3(THREADS);
@@ -876,8 +884,7 @@ static void launch_k(bass_model& m, const LaunchArgs& a, const Epi& e) {
     cfg.stream = m.ctx->stream;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    static const bool pdl = !(getenv("BASS_PDL") && atoi(getenv("BASS_PDL")) == 0);
-    at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
     at[1].id = cudaLaunchAttributeClusterDimension;   // split-K CTAs of a tile = one cluster
     at[1].val.clusterDim.x = 1;
     at[1].val.clusterDim.y = a.sp.S;
@@ -951,7 +958,7 @@ void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N
         wm = &it->second;
     }
     XNorm xn{};
-    if (norm) xn = XNorm{norm->stats, norm->c, norm->e, norm->stat_tiles};   // X = bf16(x * g) (caller)
+    if (norm) xn = XNorm{norm->stats, norm->c, norm->e, norm->kmean, norm->stat_tiles};   // X = bf16(x * g) (caller)
     auto xkey = std::make_tuple(X, M, K, TT);
     auto xit = S.xmaps.find(xkey);
     if (xit == S.xmaps.end()) xit = S.xmaps.emplace(xkey, make_map(X, M, K, TT)).first;
@@ -959,11 +966,10 @@ void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N
     auto sk = std::make_pair(N, K);
     auto si = S.splits.find(sk);
     if (si == S.splits.end()) si = S.splits.emplace(sk, choose_splits(m.ctx->sm_count, N, K)).first;
-    static const int wevict = getenv("BASS_W_EVICT") ? atoi(getenv("BASS_W_EVICT")) : 1;
     // one token group: every weight byte is read once (prefill re-reads it per group from L2)
-    Split sp{si->second, K / BK, nullptr, (wevict && packed && M <= TT) ? 1 : 0};
-    if (const char* fs = getenv("BASS_FORCE_SPLIT")) sp.S = atoi(fs);   // tuning only
-    sp.S = std::max(1, std::min(MAX_S, sp.S));   // reduction loops and cluster size hold <= 8
+    Split sp{si->second, K / BK, nullptr, (packed && M <= TT) ? 1 : 0};
+    // reduction loops and cluster size hold <= 8; every split owns >= 1 k block
+    sp.S = std::max(1, std::min(std::min(MAX_S, sp.S), sp.k_iters));
     if (sp.S > 1) {
         const size_t blocks = (size_t)((N + NB * BN - 1) / (NB * BN)) * ((M + TT - 1) / TT);
         sp.ws = (float*)S.ws.need(blocks * sp.S * TT * NB * BN * 4, m.ctx->stream);

@@ -28,13 +28,17 @@ struct Seqs {                    // one entry per sequence in the block
 
 // ------------------------------------------------------------- embedding
 // x[r] = tok_emb[id] + pos_emb[pos]   (ref:model.py:203-209)
+// `stats` (optional, bf16 folded-LayerNorm path): the row's exact mean K ->
+// shift[r] (the row-mean array `kmean` of forward()), {sum (x - K), sum (x - K)^2} -> stats[r] (one 'tile' covering the
+// whole row, fixed-order sums) and X = bf16((x - K) * xg) -> xb for the
+// layer-0 QKV GEMM (see forward(): centring keeps a large row mean from
+// swallowing the deviations).
 template <typename TW>
-// `stats` (optional): {sum, sum of squares} of the row for a LayerNorm fused
-// into the next GEMM (one 'tile' covering the whole row, fixed-order sums).
 __global__ void embed_kernel(const TW* __restrict__ tok_emb, const TW* __restrict__ pos_emb,
                              Rows rows, const int32_t* __restrict__ proposals, int pstride,
                              int d, float* __restrict__ x, float* __restrict__ stats,
-                             __nv_bfloat16* __restrict__ xb, const float* __restrict__ xg) {
+                             float* __restrict__ shift, __nv_bfloat16* __restrict__ xb,
+                             const float* __restrict__ xg) {
     __shared__ float red[2][33];
     pdl_trigger();
     pdl_wait();
@@ -44,10 +48,10 @@ __global__ void embed_kernel(const TW* __restrict__ tok_emb, const TW* __restric
     const int p = rows.pos[r];
     float s1 = 0.f, s2 = 0.f;
     if constexpr (std::is_same<TW, __nv_bfloat16>::value) {
-        if ((d & 7) == 0) {   // 16-byte rows: every load of the row issued before the first use
-            constexpr int NV = 4;   // d <= 8 * NV * blockDim
+        constexpr int NV = 4;   // d <= 8 * NV * blockDim: the row stays in registers
+        if ((d & 7) == 0 && (d >> 3) <= NV * (int)blockDim.x) {
             const int n8 = d >> 3;
-            uint4 te[NV], pe[NV];
+            uint4 te[NV], pe[NV];   // every load of the row issued before the first use
 #pragma unroll
             for (int u = 0; u < NV; ++u) {
                 const int c8 = threadIdx.x + u * blockDim.x;
@@ -56,48 +60,70 @@ __global__ void embed_kernel(const TW* __restrict__ tok_emb, const TW* __restric
                     pe[u] = __ldg(reinterpret_cast<const uint4*>(pos_emb + (int64_t)p * d) + c8);
                 }
             }
+            float v[NV][8];
 #pragma unroll
             for (int u = 0; u < NV; ++u) {
                 const int c8 = threadIdx.x + u * blockDim.x;
                 if (c8 >= n8) continue;
                 const __nv_bfloat16* tb = reinterpret_cast<const __nv_bfloat16*>(&te[u]);
                 const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(&pe[u]);
-                float v[8];
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    v[k] = __bfloat162float(tb[k]) + __bfloat162float(pb[k]);
-                    s1 += v[k];
-                    s2 += v[k] * v[k];
+                    v[u][k] = __bfloat162float(tb[k]) + __bfloat162float(pb[k]);
+                    s1 += v[u][k];
                 }
                 float4* xo = reinterpret_cast<float4*>(x + (int64_t)r * d) + 2 * c8;
-                xo[0] = make_float4(v[0], v[1], v[2], v[3]);
-                xo[1] = make_float4(v[4], v[5], v[6], v[7]);
-                if (xb) {
-                    const float4 g0 = __ldg(reinterpret_cast<const float4*>(xg) + 2 * c8);
-                    const float4 g1 = __ldg(reinterpret_cast<const float4*>(xg) + 2 * c8 + 1);
-                    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-                    uint4 ob;
-                    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&ob);
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) o[k] = __float2bfloat16_rn(v[k] * gg[k]);
-                    reinterpret_cast<uint4*>(xb + (int64_t)r * d)[c8] = ob;
-                }
+                xo[0] = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
+                xo[1] = make_float4(v[u][4], v[u][5], v[u][6], v[u][7]);
             }
-            if (n8 <= NV * (int)blockDim.x) goto stats_out;
-            s1 = s2 = 0.f;   // row too long for the register path: generic loop below
+            if (!stats) return;
+            const float K = block_sum(s1, red[0]) / (float)d;
+            s1 = 0.f;
+#pragma unroll
+            for (int u = 0; u < NV; ++u) {
+                const int c8 = threadIdx.x + u * blockDim.x;
+                if (c8 >= n8) continue;
+                const float4 g0 = __ldg(reinterpret_cast<const float4*>(xg) + 2 * c8);
+                const float4 g1 = __ldg(reinterpret_cast<const float4*>(xg) + 2 * c8 + 1);
+                const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+                uint4 ob;
+                __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&ob);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const float c = v[u][k] - K;
+                    s1 += c;
+                    s2 += c * c;
+                    o[k] = __float2bfloat16_rn(c * gg[k]);
+                }
+                reinterpret_cast<uint4*>(xb + (int64_t)r * d)[c8] = ob;
+            }
+            const float a = block_sum(s1, red[0]), b = block_sum(s2, red[1]);
+            if (threadIdx.x == 0) {
+                reinterpret_cast<float2*>(stats)[r] = make_float2(a, b);
+                shift[r] = K;
+            }
+            return;
         }
     }
+    // generic rows (fp32 tables, or rows too long for the register path)
     for (int c = threadIdx.x; c < d; c += blockDim.x) {
         const float v = ld(tok_emb, (int64_t)id * d + c) + ld(pos_emb, (int64_t)p * d + c);
         x[(int64_t)r * d + c] = v;
-        if (xb) xb[(int64_t)r * d + c] = __float2bfloat16_rn(v * xg[c]);
         s1 += v;
-        s2 += v * v;
     }
-stats_out:
-    if (stats) {
-        const float a = block_sum(s1, red[0]), b = block_sum(s2, red[1]);
-        if (threadIdx.x == 0) reinterpret_cast<float2*>(stats)[r] = make_float2(a, b);
+    if (!stats) return;
+    const float K = block_sum(s1, red[0]) / (float)d;
+    s1 = 0.f;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {   // this thread's own writes: no barrier needed
+        const float cv = x[(int64_t)r * d + c] - K;
+        xb[(int64_t)r * d + c] = __float2bfloat16_rn(cv * xg[c]);
+        s1 += cv;
+        s2 += cv * cv;
+    }
+    const float a = block_sum(s1, red[0]), b = block_sum(s2, red[1]);
+    if (threadIdx.x == 0) {
+        reinterpret_cast<float2*>(stats)[r] = make_float2(a, b);
+        shift[r] = K;
     }
 }
 
@@ -166,8 +192,10 @@ enum EpiMode { EPI_QKV = 0, EPI_RESID = 1, EPI_GELU = 2, EPI_STORE = 3 };
 
 struct Epi {
     float* x;            // EPI_RESID: x[m, n] += acc (fp32 residual stream)
-    float* stats;        // EPI_RESID (tcgen05 path, optional): per (128-column tile, row) {sum x, sum x^2} of the new x
-    __nv_bfloat16* xb;   //   ... with it: bf16(x_new * xg) = X of the next GEMM (its LayerNorm folded)
+    float* stats;        // EPI_RESID (tcgen05 path, optional): per (128-column tile, row) {sum c, sum c^2},
+                         //   c = x_new - K with the row shift K = shift[row] (the mean of x before the add)
+    const float* shift;
+    __nv_bfloat16* xb;   //   ... with it: bf16(c * xg) = X of the next GEMM (its LayerNorm folded)
     const float* xg;     //   the next LayerNorm's gain
     void* out;           // EPI_QKV: q [M, d] (act); EPI_GELU: [M, N] (act); EPI_STORE: [M, N] fp32
     void* kc;            // EPI_QKV: this layer's K cache [slot][H][cap][dh] (act dtype)

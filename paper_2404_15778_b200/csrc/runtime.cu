@@ -301,13 +301,6 @@ void gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, i
 #undef BASS_GEMM_CASE
 }
 
-// Default: the persistent streaming kernel (attn_stream.cu);
-// BASS_ATTN_MODE=chunk selects the earlier one-CTA-per-tile kernel (attn_tc.cu)
-static bool attn_stream_mode() {
-    static const bool chunk = getenv("BASS_ATTN_MODE") && std::string(getenv("BASS_ATTN_MODE")) == "chunk";
-    return !chunk;
-}
-
 template <typename TA, int DH>
 static void launch_attention_t(bass_ctx* ctx, int strategy, const void* q, const void* kc, const void* vc,
                                const Seqs& seqs_dev, const std::vector<int32_t>& qn,
@@ -316,38 +309,26 @@ static void launch_attention_t(bass_ctx* ctx, int strategy, const void* q, const
                                void* out) {
     const int n_seq = (int)qn.size();
     if constexpr (std::is_same<TA, __nv_bfloat16>::value && DH == 128) {
-        if (tc_attention_supported(BASS_BF16, DH)) {   // TMA + tcgen05 path (attn_tc.cu)
-            const int mc = (cap + 127) / 128;
-            float* part_o = (float*)po.need((size_t)M * H * mc * DH * 4, ctx->stream);
-            float* part_ml = (float*)pml.need((size_t)M * H * mc * 2 * 4, ctx->stream);
+        if (tc_attention_supported(BASS_BF16, DH)) {   // persistent TMA + tcgen05 kernel (attn_stream.cu)
             double abytes = 0.0, aflops = 0.0;
             for (int i = 0; i < n_seq; ++i) {
                 abytes += (2.0 * H * (off[i] + qn[i]) * DH + 2.0 * H * qn[i] * DH) * sizeof(TA);
                 aflops += 4.0 * H * DH * qn[i] * (off[i] + 0.5 * (qn[i] + 1));
             }
             ProfScope prof(ctx, BASS_PROF_ATTN, abytes, aflops);
-            if (attn_stream_mode()) {
-                AttnPlan plan;
-                std::vector<int32_t> ident(n_seq);
-                for (int i = 0; i < n_seq; ++i) ident[i] = i;   // standalone: sequence i uses K/V entry i
-                stream_attention_plan(ctx, strategy, q, M, n_slots, ident, qn, off, H, cap, work_buf, plan);
-                float* so = (float*)po.need((size_t)M * H * plan.mc * DH * 4, ctx->stream);
-                float* sml = (float*)pml.need((size_t)M * H * plan.mc * 2 * 4, ctx->stream);
-                stream_attention_run(ctx, plan, kc, vc, seqs_dev, so, sml, out);
-                if (plan.needs_combine) {
-                    BASS_CUDA(launch_pdl(attn_combine_kernel<TA, DH>, dim3(M, H), dim3(DH), 0, ctx->stream,
-                                         (const float*)so, (const float*)sml, row_pos_dev, H, plan.mc,
-                                         stream_split_len(), (TA*)out, 1));
-                    check_launch(ctx);
-                }
-                return;
+            AttnPlan plan;
+            std::vector<int32_t> ident(n_seq);
+            for (int i = 0; i < n_seq; ++i) ident[i] = i;   // standalone: sequence i uses K/V entry i
+            stream_attention_plan(ctx, strategy, q, M, n_slots, ident, qn, off, H, cap, work_buf, plan);
+            float* so = (float*)po.need((size_t)M * H * plan.mc * DH * 4, ctx->stream);
+            float* sml = (float*)pml.need((size_t)M * H * plan.mc * 2 * 4, ctx->stream);
+            stream_attention_run(ctx, plan, kc, vc, seqs_dev, so, sml, out);
+            if (plan.needs_combine) {
+                BASS_CUDA(launch_pdl(attn_combine_kernel<TA, DH>, dim3(M, H), dim3(DH), 0, ctx->stream,
+                                     (const float*)so, (const float*)sml, row_pos_dev, H, plan.mc,
+                                     stream_split_len(), (TA*)out, 1));
+                check_launch(ctx);
             }
-            int nq = 0;
-            tc_attention(ctx, strategy, q, M, kc, vc, n_slots, seqs_dev, qn, off, H, cap, work_buf, part_o, part_ml,
-                         mc, &nq);
-            BASS_CUDA(launch_pdl(attn_combine_kernel<TA, DH>, dim3(M, H), dim3(DH), 0, ctx->stream,
-                                 (const float*)part_o, (const float*)part_ml, row_pos_dev, H, mc, 128, (TA*)out, 0));
-            check_launch(ctx);
             return;
         }
     }
@@ -355,12 +336,11 @@ static void launch_attention_t(bass_ctx* ctx, int strategy, const void* q, const
     float* part_o = (float*)po.need((size_t)M * H * max_chunks * DH * 4, ctx->stream);
     float* part_ml = (float*)pml.need((size_t)M * H * max_chunks * 2 * 4, ctx->stream);
     const size_t smem = (size_t)(DH * (AT_SUB + 1) + AT_SUB * DH + AT_QT * DH) * 4;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static unsigned attr = 0;
+    once_per_device(attr, [&] {
         BASS_CUDA(cudaFuncSetAttribute(attn_partial_kernel<TA, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
-        attr_set = true;
-    }
+    });
     int max_qn = 0, max_L = 0;
     for (int i = 0; i < n_seq; ++i) {
         max_qn = std::max(max_qn, qn[i]);
@@ -447,7 +427,7 @@ static void append_meta(const Batch& b, std::vector<int32_t>& hm) {
 
 // the forward's attention runs the stream kernel (its work list can be pre-staged)
 static bool uses_stream_attention(const bass_model& m) {
-    return m.dtype == BASS_BF16 && tc_attention_supported(BASS_BF16, m.g.d_head) && attn_stream_mode();
+    return m.dtype == BASS_BF16 && tc_attention_supported(BASS_BF16, m.g.d_head);
 }
 
 PreMetaOff forward_premeta(const bass_model& m, const Batch& b, int strategy, const std::vector<int32_t>& safe,
@@ -494,18 +474,15 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
     void* q = m.q.need((size_t)M * d * es, st);
     void* cx = m.ctxb.need((size_t)M * d * es, st);
     void* f = m.f.need((size_t)M * 4 * d * es, st);
-    static DevBuf work_buf;   // per-process attention work list (tiny)
+    DevBuf& work_buf = m.attn_work;
 
     // tcgen05 attention: one plan (work list, Q map) for all layers of this forward
     AttnPlan plan;
     double attn_bytes = 0.0, attn_flops = 0.0;
     float *pa_o = nullptr, *pa_ml = nullptr;
     if (m.dtype == BASS_BF16 && tc_attention_supported(BASS_BF16, dh)) {
-        if (attn_stream_mode())
-            stream_attention_plan(ctx, strategy, q, M, kv.n_slots, b.slot, b.qn, b.off, H, kv.cap, work_buf, plan,
-                                  pre ? pre->work : nullptr);
-        else
-            tc_attention_plan(ctx, strategy, q, M, kv.n_slots, b.qn, b.off, H, kv.cap, work_buf, plan);
+        stream_attention_plan(ctx, strategy, q, M, kv.n_slots, b.slot, b.qn, b.off, H, kv.cap, work_buf, plan,
+                              pre ? pre->work : nullptr);
         pa_o = (float*)m.part_o.need((size_t)M * H * plan.mc * dh * 4, st);
         pa_ml = (float*)m.part_ml.need((size_t)M * H * plan.mc * 2 * 4, st);
         for (int i = 0; i < n_seq; ++i) {
@@ -518,22 +495,12 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
     auto run_attention = [&](int li, void* kc, void* vc) {
         if (plan.valid) {
             ProfScope prof(ctx, BASS_PROF_ATTN, attn_bytes, attn_flops);
-            if (plan.stream) {
-                stream_attention_run(ctx, plan, kc, vc, seqs, pa_o, pa_ml, cx);
-                if (plan.needs_combine) {
-                    BASS_CUDA(launch_pdl(attn_combine_kernel<__nv_bfloat16, 128>, dim3(M, H), dim3(128), 0, st,
-                                         (const float*)pa_o, (const float*)pa_ml, rows.pos, H, plan.mc,
-                                         stream_split_len(), (__nv_bfloat16*)cx, 1));
-                    check_launch(ctx);
-                }
-            } else {
-                tc_attention_run(ctx, plan, kc, vc, seqs, pa_o, pa_ml, cx);
-                if (!plan.fused) {
-                    BASS_CUDA(launch_pdl(attn_combine_kernel<__nv_bfloat16, 128>, dim3(M, H), dim3(128), 0, st,
-                                         (const float*)pa_o, (const float*)pa_ml, rows.pos, H, plan.mc, 128,
-                                         (__nv_bfloat16*)cx, 0));
-                    check_launch(ctx);
-                }
+            stream_attention_run(ctx, plan, kc, vc, seqs, pa_o, pa_ml, cx);
+            if (plan.needs_combine) {
+                BASS_CUDA(launch_pdl(attn_combine_kernel<__nv_bfloat16, 128>, dim3(M, H), dim3(128), 0, st,
+                                     (const float*)pa_o, (const float*)pa_ml, rows.pos, H, plan.mc,
+                                     stream_split_len(), (__nv_bfloat16*)cx, 1));
+                check_launch(ctx);
             }
         } else {
             launch_attention(ctx, m.dtype, dh, strategy, q, kc, vc, seqs, b.qn, b.off, rows.pos, M, H, kv.cap,
@@ -561,117 +528,66 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
     so.out = logits_out;
     void* hs = R > 0 ? m.hs.need((size_t)R * d * es, st) : nullptr;
 
-    if (mega_supported(m)) {
-        // layer megakernels: [LN1, QKV]_0, attn_0, [O, LN2, FC, proj, LN1, QKV]_1, attn_1, ...,
-        // [O, LN2, FC, proj, LN_f, head]
-        auto ln = [&](const float* g_, const float* b_, const int32_t* gather, void* out, int rows_) {
-            MegaPhase p;
-            p.gemm = false;
-            p.x = x; p.gather = gather; p.g = g_; p.b = b_; p.out = out; p.rows = rows_; p.d = d;
-            return p;
-        };
-        auto mm = [&](const void* X, const void* W, int mode, int Mr, int N, int K, const Epi& e) {
-            MegaPhase p;
-            p.X = X; p.W = W; p.mode = mode; p.M = Mr; p.N = N; p.K = K; p.e = e;
-            return p;
-        };
-        std::vector<MegaLaunch> launches(g.n_layer + 1);
-        std::vector<double> lbytes(g.n_layer + 1, 0.0);
-        auto add = [&](int l, const MegaPhase& p) {
-            launches[l].phases.push_back(p);
-            launches[l].M_tile = M;
-            lbytes[l] += p.gemm ? gemm_bytes(m, p.mode, p.M, p.N, p.K) : (double)p.rows * d * (4.0 + es);
-        };
-        add(0, ln(m.layers[0].ln1_g, m.layers[0].ln1_b, nullptr, h, M));
-        add(0, mm(h, m.layers[0].wqkv, EPI_QKV, M, 3 * d, d, qkv_epi(0)));
-        for (int li = 0; li < g.n_layer; ++li) {
-            const bass_layer& L = m.layers[li];
-            add(li + 1, mm(cx, L.wo, EPI_RESID, M, d, d, r));
-            add(li + 1, ln(L.ln2_g, L.ln2_b, nullptr, h, M));
-            add(li + 1, mm(h, L.wfc, EPI_GELU, M, 4 * d, d, ge));
-            add(li + 1, mm(f, L.wproj, EPI_RESID, M, d, 4 * d, r));
-            if (li + 1 < g.n_layer) {
-                add(li + 1, ln(m.layers[li + 1].ln1_g, m.layers[li + 1].ln1_b, nullptr, h, M));
-                add(li + 1, mm(h, m.layers[li + 1].wqkv, EPI_QKV, M, 3 * d, d, qkv_epi(li + 1)));
-            } else if (R > 0) {
-                add(li + 1, ln(m.lnf_g, m.lnf_b, lrows, hs, R));
-                add(li + 1, mm(hs, m.head, EPI_STORE, R, V, d, so));
-            }
-        }
-        mega_prepare(m, launches);   // one descriptor upload, before the forward's first kernel
-        if (m.dtype == BASS_BF16)
-            BASS_CUDA(launch_pdl(embed_kernel<__nv_bfloat16>, dim3(M), dim3(256), 0, st,
-                                 (const __nv_bfloat16*)m.tok_emb, (const __nv_bfloat16*)m.pos_emb, rows, proposals,
-                                 pstride, d, x, (float*)nullptr, (__nv_bfloat16*)nullptr, (const float*)nullptr));
-        else
-            BASS_CUDA(launch_pdl(embed_kernel<float>, dim3(M), dim3(128), 0, st, (const float*)m.tok_emb,
-                                 (const float*)m.pos_emb, rows, proposals, pstride, d, x, (float*)nullptr,
-                                 (__nv_bfloat16*)nullptr, (const float*)nullptr));
-        check_launch(ctx);
-        {
-            ProfScope prof(ctx, BASS_PROF_GEMM, lbytes[0]);
-            mega_launch(m, 0);
-        }
-        for (int li = 0; li < g.n_layer; ++li) {
-            run_attention(li, kc_of(li), vc_of(li));
-            ProfScope prof(ctx, BASS_PROF_GEMM, lbytes[li + 1]);
-            mega_launch(m, li + 1);
-        }
-        return;
-    }
-
     // LayerNorms folded into the QKV / FC GEMMs (bf16 tcgen05 path):
-    //   LN(x) W^T = rstd * ((x * g) W^T - mean * c) + e,  c = W g, e = W b.
-    // The embedding and the residual GEMMs write X = bf16(x * g_next) and
-    // per-(128-column tile, row) {sum, sum^2}; the next GEMM applies rstd /
-    // mean in its epilogue — no LayerNorm kernels between projections.
-    static const bool lnfuse_env = !(getenv("BASS_LNFUSE") && atoi(getenv("BASS_LNFUSE")) == 0);
-    const bool lnfuse = lnfuse_env && m.dtype == BASS_BF16 && m.packed && m.gemm_mode != BASS_GEMM_SIMT &&
+    //   LN(x) W^T = rstd * (((x - K) * g) W^T - (mean - K) * c) + e,  c = W g, e = W b,
+    // for any per-row shift K.  The embedding and the residual GEMMs write
+    // X = bf16((x - K) * g_next) and per-(128-column tile, row) sums of
+    // (x - K) and (x - K)^2 with K ~ the row mean, so neither the bf16 operand
+    // nor the variance loses the row's deviations when |mean| >> std; the
+    // next GEMM applies rstd and (mean - K) in its epilogue — no LayerNorm
+    // kernels between projections.  K: the embedding writes each row's exact
+    // mean to `kmean`; every LayerNorm consumer (QKV, FC) turns it into the
+    // exact mean of the stream it normalised (K + mean(x - K)), which is the
+    // shift the following residual GEMM centres on (the mean of the stream it
+    // adds into).
+    const bool lnfuse = m.dtype == BASS_BF16 && m.packed && m.gemm_mode != BASS_GEMM_SIMT &&
                         tc_gemm_supported(m, d, d) && d % 8 == 0;
     const int stat_tiles = (d + 127) / 128;
-    static const bool headfold_env = !(getenv("BASS_HEADFOLD") && atoi(getenv("BASS_HEADFOLD")) == 0);
-    const bool headfold = headfold_env && tc_gemm_supported(m, V, d);
-    float* lstats = nullptr;
+    const bool headfold = tc_gemm_supported(m, V, d);
+    float *lstats = nullptr, *kmean = nullptr;
     if (lnfuse) {
         ln_fold_prepare(m);
-        lstats = (float*)m.lnstats.need((size_t)stat_tiles * (M + R) * 2 * 4, st);   // + gathered head rows
+        const size_t slot = (size_t)stat_tiles * (M + R) * 2;   // + gathered head rows
+        lstats = (float*)m.lnstats.need((slot + (size_t)M) * 4, st);
+        kmean = lstats + slot;
     }
     if (m.dtype == BASS_BF16)
         BASS_CUDA(launch_pdl(embed_kernel<__nv_bfloat16>, dim3(M), dim3(256), 0, st,
                              (const __nv_bfloat16*)m.tok_emb, (const __nv_bfloat16*)m.pos_emb, rows, proposals,
-                             pstride, d, x, lstats, lnfuse ? (__nv_bfloat16*)h : (__nv_bfloat16*)nullptr,
+                             pstride, d, x, lstats, kmean, lnfuse ? (__nv_bfloat16*)h : (__nv_bfloat16*)nullptr,
                              (const float*)m.layers[0].ln1_g));
     else
         BASS_CUDA(launch_pdl(embed_kernel<float>, dim3(M), dim3(128), 0, st, (const float*)m.tok_emb,
                              (const float*)m.pos_emb, rows, proposals, pstride, d, x, (float*)nullptr,
-                             (__nv_bfloat16*)nullptr, (const float*)nullptr));
+                             (float*)nullptr, (__nv_bfloat16*)nullptr, (const float*)nullptr));
     check_launch(ctx);
     if (lnfuse) {
         const size_t per = (size_t)(2 * 3 * d + 2 * 4 * d);
         const float* fold = (const float*)m.lnfold.p;
+        // residual producer: x += acc, statistics of x - K (K = kmean), X of the next GEMM
+        auto resid_epi = [&](const float* g_next) {
+            Epi e = r;
+            e.stats = lstats;
+            e.shift = kmean;
+            e.xb = (__nv_bfloat16*)h;
+            e.xg = g_next;
+            return e;
+        };
         for (int li = 0; li < g.n_layer; ++li) {
             const bass_layer& L = m.layers[li];
             const float* fl = fold + per * li;
-            const TcNorm n1{lstats, fl, fl + 3 * d, li == 0 ? 1 : stat_tiles};
+            const TcNorm n1{lstats, fl, fl + 3 * d, kmean, li == 0 ? 1 : stat_tiles};   // embedding: one whole-row tile
             gemm(m, EPI_QKV, h, L.wqkv, M, 3 * d, d, qkv_epi(li), m.packed, &n1);
             run_attention(li, kc_of(li), vc_of(li));
-            Epi ro = r;               // x += ctx Wo^T; X of FC = bf16(x * ln2_g)
-            ro.stats = lstats;
-            ro.xb = (__nv_bfloat16*)h;
-            ro.xg = L.ln2_g;
-            gemm(m, EPI_RESID, cx, L.wo, M, d, d, ro, m.packed);
-            const TcNorm n2{lstats, fl + 6 * d, fl + 10 * d, stat_tiles};
+            // x += ctx Wo^T; X of FC = bf16((x - K) * ln2_g)
+            gemm(m, EPI_RESID, cx, L.wo, M, d, d, resid_epi(L.ln2_g), m.packed);
+            const TcNorm n2{lstats, fl + 6 * d, fl + 10 * d, kmean, stat_tiles};
             gemm(m, EPI_GELU, h, L.wfc, M, 4 * d, d, ge, m.packed, &n2);
-            Epi rp = r;               // x += f Wproj^T; X of the next QKV = bf16(x * ln1_g)
-            if (li + 1 < g.n_layer) {
-                rp.stats = lstats;
-                rp.xb = (__nv_bfloat16*)h;
-                rp.xg = m.layers[li + 1].ln1_g;
-            } else if (R > 0 && headfold) {   // ... or of the head (final LayerNorm folded)
-                rp.stats = lstats;
-                rp.xb = (__nv_bfloat16*)h;
-                rp.xg = m.lnf_g;
-            }
+            // x += f Wproj^T; X of the next QKV (or of the head: final LayerNorm
+            // folded) = bf16((x - K) * g)
+            Epi rp = r;
+            if (li + 1 < g.n_layer) rp = resid_epi(m.layers[li + 1].ln1_g);
+            else if (R > 0 && headfold) rp = resid_epi(m.lnf_g);
             gemm(m, EPI_RESID, f, L.wproj, M, d, 4 * d, rp, m.packed);
         }
         if (R > 0 && headfold) {
@@ -691,7 +607,7 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
                 X = hs;
                 hst = cst;
             }
-            const TcNorm nh{hst, hf, hf + V, stat_tiles};
+            const TcNorm nh{hst, hf, hf + V, nullptr, stat_tiles};
             gemm(m, EPI_STORE, X, m.head, R, V, d, so, m.packed, &nh);
         } else if (R > 0) {
             launch_layernorm_any(m, x, lrows, m.lnf_g, m.lnf_b, R, hs);
@@ -757,6 +673,7 @@ int bass_ctx_destroy(bass_ctx* c) {
     cudaStreamSynchronize(c->stream);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     if (c->staging.base) cudaFreeHost(c->staging.base);
+    for (DevBuf* b : {&c->scr_meta, &c->scr_work, &c->scr_po, &c->scr_pml}) b->release();
     delete c;
     return BASS_OK;
 }
@@ -827,7 +744,7 @@ int bass_model_create(bass_ctx* c, const bass_geometry* g, int dtype, bass_model
         m->esize = dtype == BASS_BF16 ? 2 : 4;
         const int64_t d = g->d_model, V = g->vocab_size, S = g->max_seq_len, L = g->n_layer;
         // bf16 GEMM weights live in the packed tile layout (rows padded to 128)
-        m->packed = dtype == BASS_BF16 && d % 64 == 0 && !(getenv("BASS_PACK") && atoi(getenv("BASS_PACK")) == 0);
+        m->packed = dtype == BASS_BF16 && d % 64 == 0;
         auto rows = [&](int64_t N) { return m->packed ? packed_rows(N) : N; };
         const int64_t per_layer = (rows(3 * d) + rows(d) + rows(4 * d)) * d + rows(d) * 4 * d;
         const int64_t total = V * d + S * d + L * per_layer + rows(V) * d;
@@ -875,11 +792,10 @@ int bass_model_destroy(bass_model* m) {
     cudaSetDevice(m->ctx->device);
     cudaStreamSynchronize(m->ctx->stream);
     tc_release(*m);
-    mega_release(*m);
     cudaFree(m->wblob);
     cudaFree(m->fblob);
     for (DevBuf* b : {&m->x, &m->h, &m->q, &m->ctxb, &m->f, &m->hs, &m->meta, &m->part_o, &m->part_ml,
-                      &m->logits_tmp, &m->lnstats, &m->lnfold})
+                      &m->logits_tmp, &m->lnstats, &m->lnfold, &m->attn_work})
         b->release();
     delete m;
     return BASS_OK;
@@ -1127,7 +1043,7 @@ int bass_attention(bass_ctx* c, int strategy, int dtype, int n_seq, int n_head, 
             for (int t = 0; t < qn[i]; ++t) row_pos.push_back(off[i] + t);
         }
         const int M = cu_q[n_seq];
-        static DevBuf meta, work, po, pml;
+        DevBuf &meta = c->scr_meta, &work = c->scr_work, &po = c->scr_po, &pml = c->scr_pml;
         int32_t* dm = (int32_t*)meta.need((4 * (size_t)n_seq + M) * 4, c->stream);
         std::vector<int32_t> hm;
         for (auto* v_ : {&slot, &q0, &qn, &off}) hm.insert(hm.end(), v_->begin(), v_->end());
@@ -1219,7 +1135,7 @@ int bass_attention_bench(bass_ctx* c, int strategy, int n_seq, int n_head, const
             for (int t = 0; t < qn[i]; ++t) row_pos.push_back(off[i] + t);
         }
         const int M = cu_q[n_seq], H = n_head;
-        static DevBuf meta, work, po, pml;
+        DevBuf &meta = c->scr_meta, &work = c->scr_work, &po = c->scr_po, &pml = c->scr_pml;
         int32_t* dm = (int32_t*)meta.need((4 * (size_t)n_seq + M) * 4, c->stream);
         std::vector<int32_t> hm;
         for (auto* v_ : {&slot, &q0, &qn, &off}) hm.insert(hm.end(), v_->begin(), v_->end());

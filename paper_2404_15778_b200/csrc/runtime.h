@@ -64,6 +64,7 @@ struct bass_ctx {
     int64_t launches = 0;
     int64_t h2d_bytes = 0, d2h_bytes = 0;
     bass::Staging staging;
+    bass::DevBuf scr_meta, scr_work, scr_po, scr_pml;   // standalone attention entry points
     // profiling
     bool profile = false;
     struct Pending { int cls; cudaEvent_t a, b; double bytes, flops; };
@@ -86,7 +87,7 @@ struct bass_ctx {
     }
 };
 // trace tags (kernel classes)
-enum { BASS_TR_GEMM = 1, BASS_TR_ATTN = 2, BASS_TR_NORM = 3, BASS_TR_COMBINE = 4, BASS_TR_MEGA = 5 };
+enum { BASS_TR_GEMM = 1, BASS_TR_ATTN = 2, BASS_TR_NORM = 3, BASS_TR_COMBINE = 4 };
 
 namespace bass {
 // RAII timer around one launch (no-op unless ctx->profile)
@@ -136,7 +137,7 @@ struct bass_model {
     bass::DevBuf lnfold;             // per layer: c, e of LN1 -> QKV and LN2 -> FC (c = W g, e = W b)
     bool lnfold_valid = false;       // recomputed after any weight / LN parameter change
     void* tc_state = nullptr;        // tcgen05 split-K GEMM descriptors (gemm_tc.cu)
-    void* mega_state = nullptr;      // layer megakernel descriptors / workspace (layer_mega.cu)
+    bass::DevBuf attn_work;          // stream-attention work list of the current forward
 };
 
 struct bass_kv {
@@ -205,6 +206,7 @@ struct TcNorm {
     const float* stats;
     const float* c;
     const float* e;
+    float* kmean;      // row means (see forward()), updated by the consumer
     int stat_tiles;
 };
 void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K,
@@ -213,36 +215,10 @@ void tc_release(bass_model& m);
 // pack n_mat contiguous [N, K] bf16 matrices into the packed layout (dst: n_mat * packed_rows(N) * K)
 void pack_weights(cudaStream_t st, const void* src, void* dst, int N, int K, int n_mat);
 
-// layer megakernel (layer_mega.cu): GEMM (packed weights, fused epilogue) and
-// LayerNorm phases of one launch, separated by grid barriers
-struct MegaPhase {
-    bool gemm = true;
-    // GEMM: Y[M, N] = X[M, K] W^T -> epilogue `mode`
-    const void* X = nullptr;
-    const void* W = nullptr;
-    int mode = 0, M = 0, N = 0, K = 0;
-    Epi e{};
-    // LayerNorm: out[r] = LN(x[gather ? gather[r] : r]) (bf16), r < rows
-    const float* x = nullptr;
-    const int32_t* gather = nullptr;
-    const float* g = nullptr;
-    const float* b = nullptr;
-    void* out = nullptr;
-    int rows = 0, d = 0;
-};
-struct MegaLaunch {
-    std::vector<MegaPhase> phases;
-    int M_tile = 0;   // largest row count of the launch (token tile)
-};
-bool mega_supported(const bass_model& m);
-void mega_prepare(bass_model& m, const std::vector<MegaLaunch>& launches);
-void mega_launch(bass_model& m, int idx);
-void mega_release(bass_model& m);
-
-// tcgen05 attention (attn_tc.cu).  A plan (work list + Q tensor map) is
+// tcgen05 attention (attn_stream.cu).  A plan (work list + Q tensor map) is
 // built once per forward and reused by every layer.
 struct AttnPlan {
-    bool valid = false, fused = false;   // fused: CTA walks all chunks, writes ctx directly
+    bool valid = false;
     bool stream = false;                 // streaming flash-decoding kernel (attn_stream.cu)
     bool needs_combine = false;          // some row spans more than one 1024-key split
     int max_len = 0;                     // longest history + block (stream kernel: stage count choice)
@@ -251,11 +227,6 @@ struct AttnPlan {
     void* work = nullptr;
     CUtensorMap tq;
 };
-void tc_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, int n_slots, const std::vector<int32_t>& qn,
-                       const std::vector<int32_t>& off, int H, int cap, DevBuf& work_buf, AttnPlan& plan,
-                       bool allow_fused = true);
-void tc_attention_run(bass_ctx* ctx, const AttnPlan& plan, const void* kc, const void* vc, const Seqs& seqs_dev,
-                      float* part_o, float* part_ml, void* out);
 bool tc_attention_supported(int dtype, int dh);
 // streaming tcgen05 attention (attn_stream.cu): the default bf16 d_head=128 path
 int stream_split_len();
@@ -269,8 +240,4 @@ void stream_attention_work(int strategy, const std::vector<int32_t>& slot, const
                            std::vector<int32_t>& w);
 void stream_attention_run(bass_ctx* ctx, const AttnPlan& plan, const void* kc, const void* vc, const Seqs& seqs_dev,
                           float* part_o, float* part_ml, void* out);
-void tc_attention(bass_ctx* ctx, int strategy, const void* q, int M, const void* kc, const void* vc, int n_slots,
-                  const Seqs& seqs_dev, const std::vector<int32_t>& qn, const std::vector<int32_t>& off, int H, int cap,
-                  DevBuf& work_buf, float* part_o, float* part_ml, int max_chunks, int* nq_out);
-
 }  // namespace bass
