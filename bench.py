@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -115,48 +116,148 @@ def dist_env():
     return rank, world, local
 
 
+# ----------------------------------------------------------- trace analysis
+TRACE_CLASSES = {1: "gemm", 2: "attn", 3: "norm", 4: "combine"}
+
+
+def _union_ms(iv):
+    """Total length (ms) of the union of [start, end] ns intervals."""
+    if not len(iv):
+        return 0.0
+    o = np.argsort(iv[:, 0], kind="stable")
+    s0, e0 = iv[o, 0], iv[o, 1]
+    ce = np.maximum.accumulate(e0)
+    new_blk = np.r_[True, s0[1:] > ce[:-1]]
+    starts = s0[new_blk]
+    ends = ce[np.r_[np.flatnonzero(new_blk)[1:] - 1, len(ce) - 1]]
+    return float((ends - starts).sum()) / 1e6
+
+
+def trace_summary(rec):
+    """Per kernel class: union time, launches, median launch span, from the
+    {t0, t1, smid, tag} records of bass_trace_read (tag = class | seq << 4)."""
+    rec = rec[rec[:, 0] > 0]
+    cls = rec[:, 3] & 15
+    seq = rec[:, 3] >> 4
+    out = {"classes": {}}
+    for c, name in TRACE_CLASSES.items():
+        r, sq = rec[cls == c], seq[cls == c]
+        if not len(r):
+            continue
+        o = np.argsort(sq, kind="stable")
+        r, sq = r[o], sq[o]
+        cut = np.flatnonzero(np.diff(sq)) + 1
+        spans = [(x[:, 1].max() - x[:, 0].min()) / 1e3 for x in np.split(r, cut)]
+        out["classes"][name] = {"union_ms": _union_ms(r[:, :2]), "launches": len(spans),
+                                "median_span_us": float(np.median(spans)), "ctas": int(len(r))}
+    out["untraced_ms"] = None
+    if len(rec):
+        busy = _union_ms(rec[:, :2])
+        out["untraced_ms"] = (rec[:, 1].max() - rec[:, 0].min()) / 1e6 - busy   # no traced CTA resident (sampling, embed, host gaps)
+    return out
+
+
+# ------------------------------------------------- acceptance-harness schedule
+_M64 = (1 << 64) - 1
+
+
+def _splitmix64(x):
+    x = (x + 0x9E3779B97F4A7C15) & _M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & _M64
+    return x ^ (x >> 31)
+
+
+def harness_schedule(batch, prompt, new, align, align_seed=99, sids=None, params=(7, 2, 10, 32)):
+    """Per-step draft lengths of a greedy generation under the keyed
+    acceptance override (csrc/sampling_kernels.cuh aligned_override: the
+    proposal at absolute position p is the main model's greedy token iff
+    u(seed, sid, p) < align) driven by Algorithm 1 (ref:draft_control.py:49-69),
+    with the engine's bonus / length rules (ref:engine.py:276-349).  No model
+    is needed: it reproduces the GPU run's steps and draft lengths exactly
+    (up to hash tokens that happen to equal the greedy token, p ~ 1/V).
+    align < 0 (natural acceptance of a random-init draft ~ 0): nothing is
+    accepted.  Returns (list of l per step, tokens per sequence)."""
+    l0, incre, mod, limit = params
+    sids = list(range(batch)) if sids is None else sids
+    C, gen, done = [prompt] * batch, [0] * batch, [False] * batch
+    l, s, ls = l0, 0, []
+    while not all(done):
+        accs = []
+        for i in range(batch):
+            if done[i]:
+                continue
+            x = 0
+            while align >= 0 and x < l:
+                h = _splitmix64(align_seed ^ _splitmix64((sids[i] * 0x100000001B3 + C[i] + x) & _M64))
+                if (h >> 11) * 2.0 ** -53 >= align:
+                    break
+                x += 1
+            rem = new - gen[i]
+            n = min(x + (1 if x < l or rem > l else 0), rem)
+            gen[i] += n
+            C[i] += n
+            done[i] = gen[i] >= new
+            accs.append(x)
+        ls.append(l)
+        if max(accs) == l:
+            l, s = min(l + incre, limit), 0
+        else:
+            l, s = max([1, l - math.ceil(l / mod) - s] + accs), 1
+    return ls, new
+
+
 # ------------------------------------------------------------ CPU reference
-def cpu_reference(cfg, k_mean, tokens_per_step, batch):
+def cpu_reference(cfg, step_lengths, tokens_per_seq, batch):
     """Time the oracle port (numpy fp64, all host threads) on a bounded
-    sample: one full-width layer + head of main (verify block) and draft
-    (single-token block) at the benchmark's context; extrapolate one step."""
-    from oracle.cpu_timing import time_spec_step
+    sample — one full-width layer (+ head) of each piece a generation is made
+    of (ref:model.py:211-245 per-sequence cost structure) — and compose one
+    generation from the per-step draft-length schedule:
+    T = T_prefill + sum_steps (t_verify + l_step * t_draft_token).
+    An extrapolated estimate (kind "port"), not a timed full run."""
+    from oracle.cpu_timing import time_generation_pieces
     from oracle.ragged import Geometry
     gm, gd = Geometry(*cfg["main"]), Geometry(*cfg["draft"])
     ctx_len = cfg["prompt"] + cfg["new"] // 2
-    k = max(1, int(round(k_mean)))
+    k = max(1, int(round(statistics.mean(step_lengths))))
     t0 = time.perf_counter()
-    r = time_spec_step(gm, gd, batch, ctx_len, k)
+    p = time_generation_pieces(gm, gd, batch, cfg["prompt"], ctx_len, k)
     wall = time.perf_counter() - t0
-    tps = batch * tokens_per_step / r["t_step_s"]
+    t_gen = p["prefill_main"] + p["prefill_draft"] + sum(p["verify"] + l * p["draft_token"] for l in step_lengths)
+    tps = batch * tokens_per_seq / t_gen
     return {"value": tps, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
-            "sample": (f"oracle numpy fp64: 1 main layer (verify {batch}x{k + 1} rows, ctx {ctx_len}) "
-                       f"+ head, 1 draft layer (1 row) + head at full width, extrapolated to "
-                       f"{gm.n_layer}+{k}x{gd.n_layer} layers/step at the GPU run's "
-                       f"{tokens_per_step:.2f} tokens/step/seq; sample wall {wall:.1f}s"),
-            "t_step_s": r["t_step_s"], "per_seq_ms_per_token": 1000 * r["t_step_s"] / tokens_per_step}
+            "sample": (f"extrapolated: oracle numpy fp64, one full-width layer + head per piece (verify "
+                       f"{batch}x{k + 1} rows at ctx {ctx_len}; one draft token; step-1 prompt blocks) x layer "
+                       f"count, composed over a {len(step_lengths)}-step schedule (mean draft length "
+                       f"{statistics.mean(step_lengths):.2f}, {tokens_per_seq * batch / len(step_lengths) / batch:.2f} "
+                       f"tokens/step/seq); sample wall {wall:.1f}s"),
+            "t_gen_s": t_gen, "pieces_s": p,
+            "per_seq_ms_per_token": 1000 * t_gen / tokens_per_seq}
 
 
 def run_reference_arm(args, cfg):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    # acceptance regime of the GPU arm's harness: alignment a -> expected
-    # tokens/step with k = Alg.1's steady state; use the closed form
-    # (ref perf.py:149-159) at the default l0 = 7 for a bounded run
-    a, k = max(args.align, 0.0), 7   # natural acceptance of a random-init draft ~ 0
-    tps_step = (1 - a ** (k + 1)) / (1 - a) if a < 1 else k + 1.0
+    # the GPU arm's acceptance regime, replayed exactly: greedy configs use the
+    # keyed override at --align (draft lengths and tokens/step identical to the
+    # GPU run); sampled configs the natural acceptance of a random-init draft
+    ls, per_seq = harness_schedule(cfg["batch"], cfg["prompt"], cfg["new"],
+                                   args.align if cfg["temperature"] == 0.0 else -1.0)
     # each step is one bounded sample (~10-30 s of host work); no warm-up
     # is needed for the CPU port, W is accepted for the interface only
-    vals = [cpu_reference(cfg, k, tps_step, cfg["batch"]) for _ in range(max(1, args.steps))]
+    vals = [cpu_reference(cfg, ls, per_seq, cfg["batch"]) for _ in range(max(1, args.steps))]
     v = statistics.median([x["value"] for x in vals])
     line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": statistics.median([x["t_step_s"] for x in vals]) * 1e3,
+            "warmup": args.warmup, "ms_per_step": statistics.median([x["t_gen_s"] for x in vals]) * 1e3,
+            "ms_per_step_kind": "extrapolated (one generation composed from per-layer samples)",
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": cfg["workload"], "batch_per_gpu": cfg["batch"],
                        "prompt_len": cfg["prompt"], "max_new_tokens": cfg["new"],
-                       "align": args.align},
+                       "align": args.align, "steps_per_generation": len(ls),
+                       "mean_draft_len": statistics.mean(ls)},
+            "per_seq_ms_per_token": statistics.median(x["per_seq_ms_per_token"] for x in vals),
             "cpu_baseline": {k_: vals[-1][k_] for k_ in ("kind", "cores", "sample")} | {"value": v,
                                                                                      "unit": "tokens/s"},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -180,8 +281,10 @@ def main():
     ap.add_argument("--profile-only", action="store_true", help="one profiled generation (ncu)")
     ap.add_argument("--save-traj", default=None, help="save the greedy trajectory (.npy)")
     ap.add_argument("--load-traj", default=None, help="reuse a saved trajectory (ncu runs)")
-    ap.add_argument("--kernel-events", type=int, default=1,
-                    help="per-kernel CUDA-event timing inside the timed region (0: off)")
+    ap.add_argument("--kernel-events", type=int, default=0,
+                    help="extra generation with per-kernel CUDA events (diagnostics; breaks PDL overlap)")
+    ap.add_argument("--trace", type=int, default=1, help="traced generation for the in-chain roofline (0: off)")
+    ap.add_argument("--trace-records", type=int, default=6 << 20)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.align is None:
@@ -269,6 +372,7 @@ def main():
 
     launches0 = ctx.launches
     h2d0, d2h0 = ctx.transfer_bytes()
+    algo0 = ctx.algo_read()
     results = []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     # pass A (headline): K generations, no instrumentation
@@ -283,23 +387,33 @@ def main():
         t_host1 = time.perf_counter()
     launches = ctx.launches - launches0
     h2d1, d2h1 = ctx.transfer_bytes()
+    algo1 = ctx.algo_read()
     dev_s = ev0.elapsed_time(ev1) / 1e3
     host_s = t_host1 - t_host0
-    # pass B (roofline): the same generations with per-kernel CUDA events on
-    # the libbass stream (events break PDL overlap, so they are kept out of A)
+    # pass T (roofline): one more generation with the per-CTA timeline trace
+    # on (a globaltimer read at CTA start and one 32-byte record at its end;
+    # the PDL chain is untouched).  A kernel class's in-chain time is the
+    # union of its CTAs' [start, end] intervals: overlapping launches
+    # (the next GEMM's weight prefetch during its predecessor) are counted
+    # once, so it can never exceed the generation's device time.
+    trace = None
+    if args.trace:
+        ctx.trace(args.trace_records)
+        evt0, evt1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        evt0.record(stream)
+        generate()
+        evt1.record(stream)
+        torch.cuda.synchronize()
+        trace = trace_summary(ctx.trace_read(args.trace_records))
+        trace["generation_ms"] = evt0.elapsed_time(evt1)
+        ctx.trace(0)
+    # optional pass B: per-launch CUDA events (break PDL overlap; diagnostics only)
     prof = None
-    dev_b_s = None
     if args.kernel_events:
         ctx.profile(True)
-        evb0, evb1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        evb0.record(stream)
-        for _ in range(max(1, min(args.steps, 2))):
-            generate()
-        evb1.record(stream)
+        generate()
         torch.cuda.synchronize()
-        dev_b_s = evb0.elapsed_time(evb1) / 1e3
         prof = ctx.profile_read()
-        prof["_generations"] = max(1, min(args.steps, 2))
         ctx.profile(False)
 
     tokens = sum(sum(len(t) for t in r[0].tokens) for r in results)
@@ -327,17 +441,26 @@ def main():
                   if rd_warm is not None else None)
 
     hbm, tfl, peak_kind = peaks()
-    empty = {"launches": 0, "ms": 0.0, "bytes": 0.0, "flops": 0.0}
-    g = prof["gemm"] if prof else empty
-    gemm_gbs = g["bytes"] / (g["ms"] / 1e3) / 1e9 if g["ms"] else 0.0
-    a = prof["attention"] if prof else empty
-    attn_gbs = a["bytes"] / (a["ms"] / 1e3) / 1e9 if a["ms"] else 0.0
-    gens_b = prof["_generations"] if prof else 1
-    # pass-B device time (the instrumented generations themselves): the
-    # event-timed kernel shares are fractions of it; the in-chain rate scales
-    # the same share onto the un-instrumented pass-A time
-    step_b_ms = dev_b_s * 1e3 if dev_b_s else dev_s / args.steps * 1e3 * gens_b
-    step_a_ms = dev_s / args.steps * 1e3 * gens_b
+    step_ms = dev_s / args.steps * 1e3
+    # algorithmic work per generation (SURVEY 8(d) per-launch formulas, summed
+    # over every launch of the timed generations)
+    algo = {k: {f: (algo1[k][f] - algo0[k][f]) / args.steps for f in ("launches", "bytes", "flops")}
+            for k in algo1}
+    all_bytes = sum(v["bytes"] for v in algo.values())
+
+    def roof(cls, tcls, kernel):
+        g = algo[cls]
+        out = {"bound": "hbm", "kernel": kernel, "peak": hbm, "unit": "GB/s", "peak_kind": peak_kind,
+               "bytes_per_generation": g["bytes"], "launches_per_generation": g["launches"]}
+        if trace and trace["classes"].get(tcls):
+            t = trace["classes"][tcls]
+            ach = g["bytes"] / (t["union_ms"] / 1e3) / 1e9
+            out.update({"achieved": ach, "frac": ach / hbm, "in_chain_ms_per_generation": t["union_ms"],
+                        "share_of_generation": t["union_ms"] / trace["generation_ms"],
+                        "median_launch_span_us": t["median_span_us"],
+                        "tflops": g["flops"] / (t["union_ms"] / 1e3) / 1e12})
+        return out
+
     traffic = None
     tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     traffic_src = None
@@ -347,7 +470,12 @@ def main():
             traffic, traffic_src = tj.get("dram_bytes_per_launch"), tj.get("shape")
         except Exception:
             traffic = None
-    step_ms = dev_s / args.steps * 1e3
+    roofline = roof("gemm", "gemm", "gemm_tc_kernel (tcgen05 weight streaming)")
+    roofline.update({"traffic": traffic, "traffic_launch": traffic_src,
+                     "step_frac": all_bytes / (step_ms / 1e3) / 1e9 / hbm,
+                     "method": "achieved = algorithmic GEMM bytes per generation / in-chain GEMM time (union of "
+                               "the GEMM CTAs' globaltimer intervals in a traced generation); step_frac = all "
+                               "algorithmic bytes per generation / ms_per_step / peak"})
     line = {
         "metric": METRIC,
         "value": tokens / dev_s,
@@ -376,29 +504,19 @@ def main():
                 "h2d_bytes_per_step": (h2d1 - h2d0) // max(args.steps, 1),
                 "d2h_bytes_per_step": (d2h1 - d2h0) // max(args.steps, 1)},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "kernel": "gemm_tc_kernel (tcgen05 weight streaming)",
-                     "achieved": gemm_gbs, "peak": hbm, "unit": "GB/s", "frac": gemm_gbs / hbm,
-                     "traffic": traffic, "traffic_launch": traffic_src, "peak_kind": peak_kind,
-                     "launches_per_generation": g["launches"] / gens_b,
-                     "share_of_step": g["ms"] / step_b_ms if step_b_ms else None,
-                     "achieved_in_chain": (g["bytes"] / (g["ms"] / step_b_ms * step_a_ms / 1e3) / 1e9
-                                           if g["ms"] and step_b_ms else None),
-                     "note": "achieved: CUDA-event time per launch from an instrumented repeat of the "
-                             "timed generations (events between kernels disable PDL overlap); share_of_step "
-                             "is of that repeat's device time; achieved_in_chain applies the share to the "
-                             "un-instrumented (PDL-overlapped) timed run"},
-        "attention_roofline": {"kernel": "attn_stream_kernel (+ split combine)", "achieved": attn_gbs, "peak": hbm,
-                               "unit": "GB/s", "frac": attn_gbs / hbm,
-                               "launches_per_generation": a["launches"] / gens_b,
-                               "share_of_step": a["ms"] / step_b_ms if step_b_ms else None,
-                               "achieved_in_chain": (a["bytes"] / (a["ms"] / step_b_ms * step_a_ms / 1e3) / 1e9
-                                                     if a["ms"] and step_b_ms else None)},
-        "kernel_time_ms_per_generation": ({k: v["ms"] / gens_b for k, v in prof.items()
-                                           if not k.startswith("_")} if prof else None),
+        "roofline": roofline,
+        "attention_roofline": roof("attention", "attn", "attn_stream_kernel (persistent TMA + tcgen05)"),
+        "algorithmic_bytes_per_generation": {k: v["bytes"] for k, v in algo.items()},
+        "trace": ({"generation_ms": trace["generation_ms"], "untraced_ms": trace["untraced_ms"],
+                   "classes": trace["classes"]} if trace else None),
+        "kernel_event_ms_per_generation": ({k: v["ms"] for k, v in prof.items()} if prof else None),
         "clocks": clocks.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_reference(cfg, statistics.mean(dl), tok_per_step, b)
+        # the GPU run's own per-step draft lengths (first timed generation)
+        cb = cpu_reference(cfg, [s_.draft_length for s_ in results[0][0].steps],
+                           sum(len(t) for t in results[0][0].tokens) / b, b)
+        line["cpu_baseline"] = {k_: cb[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

@@ -71,6 +71,11 @@ int         bass_ctx_transfer_bytes(const bass_ctx* ctx, int64_t* h2d, int64_t* 
 int         bass_ctx_profile(bass_ctx* ctx, int enable);
 int         bass_ctx_profile_read(bass_ctx* ctx, int cls, int64_t* launches,
                                   double* ms, double* bytes, double* flops);
+/* cumulative algorithmic work of every launch of a class since the context
+ * was created (no events, no overhead): launches, bytes, flops.  The bench's
+ * roofline divides these by the traced in-chain kernel time. */
+int         bass_ctx_algo_read(bass_ctx* ctx, int cls, int64_t* launches,
+                               double* bytes, double* flops);
 
 /* Model weights live in device memory owned by the model.
  * Replaces ModelWeights/init_model (ref:model.py:87-132). */

@@ -9,6 +9,12 @@ width with the reference's own per-sequence cost structure
 
   T_step = L_main * t_layer(main, verify block) + t_head(main, verify rows)
          + k * (L_draft * t_layer(draft, 1-row block) + t_head(draft, 1 row))
+
+`time_generation_pieces` adds the first step's prompt blocks (the reference
+prefills inside step 1's ragged block, ref:engine.py:248, 268), so a whole
+generation's time is composed from an exact per-step draft-length schedule:
+
+  T_gen = T_prefill + sum_steps [t_verify + l_step * t_draft_token]
 """
 
 from __future__ import annotations
@@ -80,4 +86,33 @@ def time_spec_step(main: Geometry, draft: Geometry, batch: int, ctx_len: int, k:
     t_step = main.n_layer * out["main"]["t_layer_s"] + out["main"]["t_head_s"] + \
         k * (draft.n_layer * out["draft"]["t_layer_s"] + out["draft"]["t_head_s"])
     out["t_step_s"] = t_step
+    return out
+
+
+def time_generation_pieces(main: Geometry, draft: Geometry, batch: int, prompt: int, ctx_len: int,
+                           k: int, seed: int = 0) -> dict:
+    """Host-core times of the pieces a generation is made of (full width, one
+    layer each, extrapolated by layer count): the verify forward of a
+    (k+1)-row block per sequence at context `ctx_len`, one draft token (1-row
+    block), and the prompt blocks of step 1 (main: prompt + k rows, draft:
+    prompt rows) from an empty cache."""
+    rng = np.random.default_rng(seed)
+    out = {}
+    for name, g, rows, ctx in (("verify", main, k + 1, ctx_len), ("draft_token", draft, 1, ctx_len),
+                               ("prefill_main", main, prompt + k, 0), ("prefill_draft", draft, prompt, 0)):
+        lay = _layer(rng, g.d_model)
+        head = _rand(rng, (g.d_model, g.vocab_size))
+        cache = RaggedCache(1, batch, g.n_head, g.d_head)
+        if ctx:
+            for s_ in range(batch):
+                kv = rng.standard_normal((g.n_head, ctx, g.d_head))
+                cache.append(s_, 0, kv, kv)
+        xs = [rng.standard_normal((rows, g.d_model)) for _ in range(batch)]
+        t_l = _time_layer(g, lay, xs, cache, list(range(batch)), [ctx] * batch)
+        # logits of the rows the step consumes: all k+1 verify rows, one per
+        # draft forward (the last prompt row)
+        t_h = _time_head(head, [x[-(k + 1):] if name == "prefill_main" else x[-1:] if name != "verify" else x
+                                for x in xs])
+        out[name] = g.n_layer * t_l + t_h
+        del lay, head, cache, xs
     return out

@@ -64,6 +64,7 @@ SIGNATURES = {
     "bass_ctx_transfer_bytes": (C.c_int, [vp, i64p, i64p]),
     "bass_ctx_profile": (C.c_int, [vp, C.c_int]),
     "bass_ctx_profile_read": (C.c_int, [vp, C.c_int, i64p, f64p, f64p, f64p]),
+    "bass_ctx_algo_read": (C.c_int, [vp, C.c_int, i64p, f64p, f64p]),
     "bass_model_create": (C.c_int, [vp, C.POINTER(Geometry), C.c_int, C.POINTER(vp)]),
     "bass_model_destroy": (C.c_int, [vp]),
     "bass_model_set_weight": (C.c_int, [vp, C.c_int, C.c_int, f32p, C.c_int64]),

@@ -723,6 +723,15 @@ int bass_ctx_profile_read(bass_ctx* c, int cls, int64_t* launches, double* ms, d
     });
 }
 
+int bass_ctx_algo_read(bass_ctx* c, int cls, int64_t* launches, double* bytes, double* flops) {
+    return guarded(c, [&] {
+        BASS_REQUIRE(cls >= 0 && cls < BASS_PROF_N, "unknown profile class");
+        *launches = c->algo_n[cls];
+        *bytes = c->algo_bytes[cls];
+        *flops = c->algo_flops[cls];
+    });
+}
+
 // ---------------------------------------------------------------- model
 int bass_model_create(bass_ctx* c, const bass_geometry* g, int dtype, bass_model** out) {
     *out = nullptr;

@@ -72,6 +72,9 @@ struct bass_ctx {
     std::vector<cudaEvent_t> pool;
     double prof_ms[BASS_PROF_N] = {}, prof_bytes[BASS_PROF_N] = {}, prof_flops[BASS_PROF_N] = {};
     int64_t prof_n[BASS_PROF_N] = {};
+    // algorithmic work of every launch (counted without events)
+    double algo_bytes[BASS_PROF_N] = {}, algo_flops[BASS_PROF_N] = {};
+    int64_t algo_n[BASS_PROF_N] = {};
     cudaEvent_t ev();
     void resolve();
     void sync();
@@ -90,7 +93,8 @@ struct bass_ctx {
 enum { BASS_TR_GEMM = 1, BASS_TR_ATTN = 2, BASS_TR_NORM = 3, BASS_TR_COMBINE = 4 };
 
 namespace bass {
-// RAII timer around one launch (no-op unless ctx->profile)
+// Algorithmic-work accounting around one launch (always on: launch count,
+// bytes, flops per kernel class) plus a CUDA-event timer when ctx->profile.
 struct ProfScope {
     bass_ctx* c;
     int cls;
@@ -98,6 +102,9 @@ struct ProfScope {
     cudaEvent_t a = nullptr;
     ProfScope(bass_ctx* c_, int cls_, double bytes_, double flops_ = 0)
         : c(c_), cls(cls_), bytes(bytes_), flops(flops_) {
+        c->algo_n[cls] += 1;
+        c->algo_bytes[cls] += bytes_;
+        c->algo_flops[cls] += flops_;
         if (c->profile) {
             a = c->ev();
             cudaEventRecord(a, c->stream);

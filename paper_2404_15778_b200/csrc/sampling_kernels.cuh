@@ -13,7 +13,6 @@
 namespace bass {
 
 constexpr int SM_THREADS = 512;
-constexpr int kMaxEmit = 64;   // >= draft limit + 1
 
 // thread-local argmax over a row (16-byte loads, 4 in flight), first index on ties
 BASS_DEV ArgMax row_argmax_local(const float* __restrict__ row, int V) {
@@ -282,7 +281,7 @@ static __global__ void __launch_bounds__(SM_THREADS) row_stats_kernel(const floa
 
 struct DraftPick {               // per active sequence of a draft step
     const int32_t* slot;         // [nA]
-    const int32_t* sid;          // sequence ids (by slot)
+    const int64_t* sid;          // sequence ids (by slot)
     const int32_t* pos;          // absolute position of the proposal (by seq)
     int32_t* proposals;          // [slot][pstride]
     int pstride, j;
@@ -478,11 +477,19 @@ static __global__ void rng_kernel(int n, uint64_t seed, const int64_t* sid, cons
 
 // ------------------------------------------------------ engine step logic
 
-struct SlotStep {                 // device -> host, one per active sequence
+// device -> host, one record per active sequence: a SlotStep header, then
+// `estride` emitted token ids (int32, padded to 8 bytes), then `estride`
+// logprobs (double); estride = draft limit + 1 (the most a step can emit)
+struct SlotStep {
     int32_t accepted, n_emit, reason, err;   // reason: -1 running, 0 eos, 1 length
-    int32_t tok[kMaxEmit];
-    double lp[kMaxEmit];
 };
+__host__ __device__ inline size_t slot_rec_bytes(int estride) {
+    return sizeof(SlotStep) + (((size_t)estride * 4 + 7) & ~(size_t)7) + (size_t)estride * 8;
+}
+__host__ __device__ inline int32_t* slot_rec_tok(void* rec) { return reinterpret_cast<int32_t*>((char*)rec + sizeof(SlotStep)); }
+__host__ __device__ inline double* slot_rec_lp(void* rec, int estride) {
+    return reinterpret_cast<double*>((char*)rec + sizeof(SlotStep) + (((size_t)estride * 4 + 7) & ~(size_t)7));
+}
 
 struct StepArgs {
     int nA, l, V;
@@ -500,7 +507,8 @@ struct StepArgs {
     const int32_t* corr;          // [nA*(l+1)]
     const int32_t* bonus_tok;     // [nA]
     int greedy;
-    SlotStep* out;
+    char* out;                    // [nA] records of slot_rec_bytes(estride)
+    int estride;
 };
 
 // accepted prefix + correction / bonus + EOS/length finalize + logprobs
@@ -511,7 +519,8 @@ static __global__ void finalize_kernel(StepArgs a) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.nA) return;
     const int slot = a.slot[i], l = a.l, rb = i * (l + 1);
-    int em[kMaxEmit];
+    char* rec = a.out + (size_t)i * slot_rec_bytes(a.estride);
+    int32_t* em = slot_rec_tok(rec);   // emitted tokens, built in place (<= l + 1)
     int x = 0, n = 0, err = 0;
     for (int j = 0; j < l; ++j) {
         const int t = a.proposals[slot * a.pstride + j];
@@ -551,15 +560,13 @@ static __global__ void finalize_kernel(StepArgs a) {
     }
     if (n > remaining) { n = remaining; reason = 1; }
     else if (n == remaining && reason < 0) reason = 1;
-    SlotStep& o = a.out[i];
+    SlotStep& o = *reinterpret_cast<SlotStep*>(rec);
     o.accepted = x;
     o.n_emit = n;
     o.reason = reason;
     o.err = err;
-    for (int j = 0; j < n; ++j) {
-        o.tok[j] = em[j];
-        o.lp[j] = double(a.vlog[(int64_t)(rb + j) * a.V + em[j]]) - a.vlse[rb + j];
-    }
+    double* lp = slot_rec_lp(rec, a.estride);
+    for (int j = 0; j < n; ++j) lp[j] = double(a.vlog[(int64_t)(rb + j) * a.V + em[j]]) - a.vlse[rb + j];
 }
 
 // sampled verify: one CTA per (sequence, position j <= l).  j < l tests the
@@ -570,7 +577,7 @@ struct VerifyArgs {
     double T, top_p;
     uint64_t seed;
     const int32_t* slot;
-    const int32_t* sid;           // by slot
+    const int64_t* sid;           // by slot
     const int32_t* committed;     // [nA]
     const int32_t* proposals;
     int pstride;
@@ -587,7 +594,8 @@ static __global__ void __launch_bounds__(SM_THREADS) verify_sampled_kernel(Verif
     pdl_trigger();
     pdl_wait();
     const int j = blockIdx.x, i = blockIdx.y, l = a.l;
-    const int slot = a.slot[i], sid = a.sid[slot], pos = a.committed[i] + j;
+    const int slot = a.slot[i], pos = a.committed[i] + j;
+    const int64_t sid = a.sid[slot];
     const float* q = a.vlog + (int64_t)(i * (l + 1) + j) * a.V;
     const float* p = a.dlog + (int64_t)(j * a.nA + i) * a.V;
     double* eq = a.scratch + (int64_t)(i * (l + 1) + j) * 2 * a.V;
@@ -635,7 +643,8 @@ static __global__ void __launch_bounds__(SM_THREADS) verify_accept_kernel(Verify
     pdl_trigger();
     pdl_wait();
     const int j = blockIdx.x, i = blockIdx.y, l = a.l;
-    const int slot = a.slot[i], sid = a.sid[slot], pos = a.committed[i] + j;
+    const int slot = a.slot[i], pos = a.committed[i] + j;
+    const int64_t sid = a.sid[slot];
     const int64_t r = (int64_t)i * (l + 1) + j;
     const float* q = a.vlog + r * a.V;
     const float* p = a.dlog + (int64_t)(j * a.nA + i) * a.V;
@@ -665,7 +674,7 @@ static __global__ void __launch_bounds__(SM_THREADS) verify_accept_kernel(Verify
 // forward's token indirection.
 struct RegularArgs {
     const int32_t* slot;
-    const int32_t* sid;           // by slot
+    const int64_t* sid;           // by slot
     const int32_t* pos;           // [nA] absolute position of the new token
     int32_t* proposals;
     int pstride;

@@ -94,6 +94,28 @@ class CudaContext:
         """Start (and reset) / stop per-kernel-class CUDA-event timing."""
         self.check(self.lib.bass_ctx_profile(self.handle, 1 if enable else 0))
 
+    def algo_read(self) -> dict:
+        """Cumulative algorithmic work per kernel class (launches, bytes, flops)."""
+        out = {}
+        for i, name in enumerate(self.PROFILE_CLASSES):
+            n, by, fl = C.c_int64(), C.c_double(), C.c_double()
+            self.check(self.lib.bass_ctx_algo_read(self.handle, i, C.byref(n), C.byref(by), C.byref(fl)))
+            out[name] = {"launches": n.value, "bytes": by.value, "flops": fl.value}
+        return out
+
+    def trace(self, records: int):
+        """Enable (records > 0, capacity) / disable (0) the per-CTA timeline trace."""
+        self.check(self.lib.bass_trace_enable(self.handle, int(records)))
+
+    def trace_read(self, max_records: int):
+        """Records {t0, t1, smid, tag} (globaltimer ns) of the traced launches
+        since enable, as an int64 [n, 4] array; resets the trace."""
+        buf = np.zeros(int(max_records) * 4, np.uint64)
+        n = C.c_int64()
+        self.check(self.lib.bass_trace_read(self.handle, buf.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                            int(max_records), C.byref(n)))
+        return buf[: 4 * n.value].reshape(-1, 4).astype(np.int64)
+
     def profile_read(self) -> dict:
         out = {}
         for i, name in enumerate(self.PROFILE_CLASSES):

@@ -368,3 +368,43 @@ def test_timeline_trace_records_every_cta(B):
     assert (rec[:, 2] < 1024).all()
     classes = set((rec[:, 3] & 15).tolist())
     assert {1, 2} <= classes   # GEMM, attention (the LayerNorms are folded into the GEMMs)
+
+
+def test_sequence_ids_beyond_int32_and_long_drafts_match_oracle(B):
+    """Contract fidelity (ref:engine.py:36-61 accepts any non-negative id;
+    ref:draft_control.py:17-29 any limit >= 1): sequence ids above 2^32 key
+    the per-sequence RNG exactly like the reference, and a fixed draft of 70
+    tokens (beyond any fixed emit buffer) runs; sampled, fp32 parity mode,
+    tokens / logprobs / step counters equal to the oracle engine."""
+    g = OR.Geometry(1, 4, 64, 16, 96, 512)
+    tw = B.DeviceWeights.from_reference(OR.init_weights(TINY, 1234), "fp32")
+    dwt = OR.init_weights(g, 99)
+    dw = B.DeviceWeights.from_reference(dwt, "fp32")
+    prompts = [[3, 5, 7, 9], [11, 2], [40, 41, 42]]
+    sids = [2 ** 40 + 3, 5, 2 ** 62 + 17]
+    ref = OE.run_speculative(OE.OracleModel(OR.init_weights(TINY, 1234), 3), OE.OracleModel(dwt, 3),
+                             OE.Request(prompts, 90, temperature=0.9, top_p=0.95, seed=77, sequence_ids=sids),
+                             oracle.FixedLength(70))
+    req = B.GenerationRequest(prompts, 90, temperature=0.9, top_p=0.95, seed=77, sequence_ids=sids)
+    got = B.decode_speculative(B.CudaModel(tw, 3, capacity=256), B.CudaModel(dw, 3, capacity=256), req,
+                               B.FixedDraftController(70))
+    assert got.tokens == ref.tokens
+    for a, b in zip(got.logprobs, ref.logprobs):
+        assert np.allclose(a, b, rtol=0, atol=2e-4)
+    assert got.main_forward_calls == ref.main_calls and got.draft_forward_calls == ref.draft_calls
+
+
+def test_align_override_requires_greedy_and_errors_roll_back(B):
+    """The keyed acceptance override (bench harness) is rejected for sampled
+    decoding before any work, and the providers stay usable."""
+    from paper_2404_15778_b200 import engine as E
+    tw = B.DeviceWeights.from_reference(OR.init_weights(TINY, 1234), "fp32")
+    main, draft = B.CudaModel(tw, 2), B.CudaModel(tw, 2)
+    eng = E.CudaEngine(main, draft)
+    req = B.GenerationRequest([[1, 2, 3], [4, 5]], 8, temperature=0.5)
+    with pytest.raises(ValueError, match="greedy"):
+        eng.run(req, B.FixedDraftController(3), speculative=True, align=0.5,
+                align_tokens=np.zeros((2, 8), np.int32))
+    assert main.lengths() == [0, 0] and draft.lengths() == [0, 0]
+    res = B.decode_speculative(main, draft, req, B.FixedDraftController(3))
+    assert all(len(t) == 8 for t in res.tokens)
