@@ -87,6 +87,10 @@ int bass_model_destroy(bass_model* m);
  * output-major on device.  n must equal the tensor's element count. */
 int bass_model_set_weight(bass_model* m, int tensor, int layer,
                           const float* host, int64_t n);
+/* the inverse: one tensor back to host fp32 in the reference layout (the
+ * device values, e.g. bf16-rounded) — checkpoint save (ref:checkpoint.py:65-79) */
+int bass_model_get_weight(const bass_model* m, int tensor, int layer,
+                          float* host, int64_t n);
 /* device-side N(0, std) init for benchmark-scale models (ref init is
  * N(0,0.02) on the fp32 grid, ref:model.py:106-132); LN gains 1, biases 0 */
 int bass_model_init_random(bass_model* m, uint64_t seed, float std);

@@ -68,6 +68,7 @@ SIGNATURES = {
     "bass_model_create": (C.c_int, [vp, C.POINTER(Geometry), C.c_int, C.POINTER(vp)]),
     "bass_model_destroy": (C.c_int, [vp]),
     "bass_model_set_weight": (C.c_int, [vp, C.c_int, C.c_int, f32p, C.c_int64]),
+    "bass_model_get_weight": (C.c_int, [vp, C.c_int, C.c_int, f32p, C.c_int64]),
     "bass_model_init_random": (C.c_int, [vp, C.c_uint64, C.c_float]),
     "bass_model_set_gemm": (C.c_int, [vp, C.c_int]),
     "bass_model_weight_bytes": (C.c_int64, [vp]),

@@ -144,6 +144,31 @@ __global__ void transpose_convert(const float* __restrict__ src, int K, int N, T
     }
 }
 
+// inverse of transpose_convert: device output-major rows -> reference [K, N] fp32
+template <typename T>
+__global__ void transpose_gather(const T* __restrict__ src, int K, int N, float* __restrict__ dst,
+                                 int64_t src_ld, int64_t row_off, bool packed) {
+    __shared__ float tile[32][33];
+    const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int n = n0 + i, k = k0 + threadIdx.x;
+        tile[threadIdx.x][i] = (n < N && k < K)
+                                   ? ld(src, packed ? packed_index(row_off + n, k, src_ld) : (row_off + n) * src_ld + k)
+                                   : 0.f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int k = k0 + i, n = n0 + threadIdx.x;
+        if (k < K && n < N) dst[(int64_t)k * N + n] = tile[i][threadIdx.x];
+    }
+}
+
+template <typename T>
+__global__ void to_f32(const T* __restrict__ src, int64_t n, float* __restrict__ dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = ld(src, i);
+}
+
 __global__ void pack_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst, int N, int K,
                             int64_t src_stride, int64_t dst_stride, int n_mat) {
     const int64_t per = (int64_t)N * K;
@@ -868,6 +893,64 @@ int bass_model_set_weight(bass_model* m, int tensor, int layer, const float* hos
             case BASS_W_LNF_G: put_f32(m->lnf_g); break;
             case BASS_W_LNF_B: put_f32(m->lnf_b); break;
             case BASS_W_HEAD: put_matrix(d, V, m->head, 0); break;
+        }
+        BASS_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+// read one tensor back in the reference layout (inverse of bass_model_set_weight)
+int bass_model_get_weight(const bass_model* mc, int tensor, int layer, float* host, int64_t n) {
+    bass_model* m = const_cast<bass_model*>(mc);
+    return guarded(m->ctx, [&] {
+        const bass_geometry& g = m->g;
+        const int64_t d = g.d_model, V = g.vocab_size, S = g.max_seq_len;
+        BASS_REQUIRE(tensor >= BASS_W_TOK_EMB && tensor <= BASS_W_HEAD, "unknown tensor id");
+        const bool per_layer = tensor >= BASS_W_LN1_G && tensor <= BASS_W_PROJ;
+        BASS_REQUIRE(!per_layer || (layer >= 0 && layer < g.n_layer), "layer index out of range");
+        cudaStream_t st = m->ctx->stream;
+        float* tmp = nullptr;
+        auto get_matrix = [&](int64_t K, int64_t N, const void* src, int64_t row_off) {
+            BASS_REQUIRE(n == K * N, "geometry: element count does not match the tensor");
+            BASS_CUDA(cudaMallocAsync((void**)&tmp, K * N * 4, st));
+            dim3 grid((N + 31) / 32, (K + 31) / 32), blk(32, 8);
+            if (m->dtype == BASS_BF16)
+                transpose_gather<<<grid, blk, 0, st>>>((const __nv_bfloat16*)src, (int)K, (int)N, tmp, K, row_off,
+                                                       m->packed);
+            else
+                transpose_gather<<<grid, blk, 0, st>>>((const float*)src, (int)K, (int)N, tmp, K, row_off, false);
+        };
+        auto get_rows = [&](int64_t count, const void* src) {
+            BASS_REQUIRE(n == count, "geometry: element count does not match the tensor");
+            BASS_CUDA(cudaMallocAsync((void**)&tmp, count * 4, st));
+            if (m->dtype == BASS_BF16) to_f32<<<256, 256, 0, st>>>((const __nv_bfloat16*)src, count, tmp);
+            else to_f32<<<256, 256, 0, st>>>((const float*)src, count, tmp);
+        };
+        auto get_f32 = [&](const float* src) {
+            BASS_REQUIRE(n == d, "geometry: LN parameter must have d_model elements");
+            BASS_CUDA(cudaMemcpyAsync(host, src, d * 4, cudaMemcpyDeviceToHost, st));
+        };
+        const bass_layer* L = per_layer ? &m->layers[layer] : nullptr;
+        switch (tensor) {
+            case BASS_W_TOK_EMB: get_rows(V * d, m->tok_emb); break;
+            case BASS_W_POS_EMB: get_rows(S * d, m->pos_emb); break;
+            case BASS_W_LN1_G: get_f32(L->ln1_g); break;
+            case BASS_W_LN1_B: get_f32(L->ln1_b); break;
+            case BASS_W_LN2_G: get_f32(L->ln2_g); break;
+            case BASS_W_LN2_B: get_f32(L->ln2_b); break;
+            case BASS_W_WQ: get_matrix(d, d, L->wqkv, 0); break;
+            case BASS_W_WK: get_matrix(d, d, L->wqkv, d); break;
+            case BASS_W_WV: get_matrix(d, d, L->wqkv, 2 * d); break;
+            case BASS_W_WO: get_matrix(d, d, L->wo, 0); break;
+            case BASS_W_FC: get_matrix(d, 4 * d, L->wfc, 0); break;
+            case BASS_W_PROJ: get_matrix(4 * d, d, L->wproj, 0); break;
+            case BASS_W_LNF_G: get_f32(m->lnf_g); break;
+            case BASS_W_LNF_B: get_f32(m->lnf_b); break;
+            case BASS_W_HEAD: get_matrix(d, V, m->head, 0); break;
+        }
+        BASS_CUDA(cudaGetLastError());
+        if (tmp) {
+            BASS_CUDA(cudaMemcpyAsync(host, tmp, n * 4, cudaMemcpyDeviceToHost, st));
+            BASS_CUDA(cudaFreeAsync(tmp, st));
         }
         BASS_CUDA(cudaStreamSynchronize(st));
     });

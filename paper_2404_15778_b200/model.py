@@ -179,6 +179,20 @@ class DeviceWeights:
         self.ctx.check(self.ctx.lib.bass_model_set_weight(self.handle, tensor, layer,
                                                           L.ptr(a, C.c_float), a.size))
 
+    _SHAPES = {L.W_TOK_EMB: lambda c: (c.vocab_size, c.d_model), L.W_POS_EMB: lambda c: (c.max_seq_len, c.d_model),
+               L.W_HEAD: lambda c: (c.d_model, c.vocab_size), L.W_WQ: lambda c: (c.d_model, c.d_model),
+               L.W_WK: lambda c: (c.d_model, c.d_model), L.W_WV: lambda c: (c.d_model, c.d_model),
+               L.W_WO: lambda c: (c.d_model, c.d_model), L.W_FC: lambda c: (c.d_model, 4 * c.d_model),
+               L.W_PROJ: lambda c: (4 * c.d_model, c.d_model)}
+
+    def get(self, tensor: int, layer: int = 0) -> np.ndarray:
+        """One tensor back in the reference layout (float32 values as stored)."""
+        shape = self._SHAPES.get(tensor, lambda c: (c.d_model,))(self.config)
+        out = np.empty(shape, dtype=np.float32)
+        self.ctx.check(self.ctx.lib.bass_model_get_weight(self.handle, tensor, layer, L.ptr(out, C.c_float),
+                                                          out.size))
+        return out
+
     @classmethod
     def from_reference(cls, weights, dtype="bf16", ctx=None) -> "DeviceWeights":
         """Upload a reference `ModelWeights` (or the oracle's dict) to the device."""
@@ -190,6 +204,36 @@ class DeviceWeights:
         for i, lay in enumerate(layers):
             for name, tid in _LAYER_IDS.items():
                 dw._put(tid, i, lay[name])
+        return dw
+
+    @classmethod
+    def init_model(cls, config: ModelConfig, seed: int, dtype="bf16", ctx=None) -> "DeviceWeights":
+        """The reference's `init_model(config, seed)` (ref:model.py:106-132),
+        value for value: one `default_rng(seed)` stream, N(0, 0.02) drawn on
+        the float32 grid in the reference's order (token_emb, pos_emb, per
+        layer wq wk wv wo w_fc w_proj, head), LN gains 1 / biases 0.  numpy's
+        normal draws are chunk-invariant, so each tensor is drawn, uploaded
+        (converted to `dtype` on the device) and dropped in turn — the fp64
+        model is never materialised (65 GB at the 7.8B shape)."""
+        dw = cls(config, dtype, ctx)
+        rng = np.random.default_rng(seed)
+        d, v, s, ff = config.d_model, config.vocab_size, config.max_seq_len, config.d_ff
+
+        def draw(shape):
+            return rng.normal(0.0, 0.02, size=shape).astype(np.float32)
+
+        dw._put(L.W_TOK_EMB, 0, draw((v, d)))
+        dw._put(L.W_POS_EMB, 0, draw((s, d)))
+        one, zero = np.ones(d, np.float32), np.zeros(d, np.float32)
+        for li in range(config.n_layer):
+            for tid, shape in ((L.W_WQ, (d, d)), (L.W_WK, (d, d)), (L.W_WV, (d, d)), (L.W_WO, (d, d)),
+                               (L.W_FC, (d, ff)), (L.W_PROJ, (ff, d))):
+                dw._put(tid, li, draw(shape))
+            for tid, val in ((L.W_LN1_G, one), (L.W_LN1_B, zero), (L.W_LN2_G, one), (L.W_LN2_B, zero)):
+                dw._put(tid, li, val)
+        dw._put(L.W_LNF_G, 0, one)
+        dw._put(L.W_LNF_B, 0, zero)
+        dw._put(L.W_HEAD, 0, draw((d, v)))
         return dw
 
     @classmethod
