@@ -51,6 +51,12 @@ CONFIGS = {
                batch=8, prompt=128, new=128, temperature=0.2, top_p=0.95,
                workload="OPT-13B-shape main + OPT-125M-shape draft, batch 8/GPU, bf16, sampled "
                         "T=0.2 top_p=0.95"),
+    # BASELINE configs[4]: 64 global sequences sharded over the ranks (strong
+    # scaling: total work fixed), ~256-token contexts
+    "c5": dict(main=(30, 36, 4608, 128, 50272, 2048), draft=(4, 16, 2048, 128, 50272, 2048),
+               batch=64, global_batch=64, prompt=128, new=128, temperature=0.0, top_p=1.0,
+               workload="7.8B-class main + 310M-class draft, 64 sequences sharded over the GPUs (replica per "
+                        "GPU), bf16, greedy, dynamic draft length"),
     "small": dict(main=(4, 8, 512, 64, 4096, 1024), draft=(1, 8, 512, 64, 4096, 1024),
                   batch=8, prompt=64, new=64, temperature=0.0, top_p=1.0,
                   workload="small smoke config"),
@@ -220,14 +226,18 @@ def cpu_reference(cfg, step_lengths, tokens_per_seq, batch):
     gm, gd = Geometry(*cfg["main"]), Geometry(*cfg["draft"])
     ctx_len = cfg["prompt"] + cfg["new"] // 2
     k = max(1, int(round(statistics.mean(step_lengths))))
+    # the reference runs its dense layers per sequence (ref:model.py:211-245),
+    # so a piece's time is linear in the batch: sample at most 8 sequences
+    sb = min(batch, 8)
     t0 = time.perf_counter()
-    p = time_generation_pieces(gm, gd, batch, cfg["prompt"], ctx_len, k)
+    p = {n: t * batch / sb for n, t in time_generation_pieces(gm, gd, sb, cfg["prompt"], ctx_len, k).items()}
     wall = time.perf_counter() - t0
     t_gen = p["prefill_main"] + p["prefill_draft"] + sum(p["verify"] + l * p["draft_token"] for l in step_lengths)
     tps = batch * tokens_per_seq / t_gen
     return {"value": tps, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
             "sample": (f"extrapolated: oracle numpy fp64, one full-width layer + head per piece (verify "
-                       f"{batch}x{k + 1} rows at ctx {ctx_len}; one draft token; step-1 prompt blocks) x layer "
+                       f"{sb}x{k + 1} rows at ctx {ctx_len}, x{batch / sb:g} sequences; one draft token; "
+                       f"step-1 prompt blocks) x layer "
                        f"count, composed over a {len(step_lengths)}-step schedule (mean draft length "
                        f"{statistics.mean(step_lengths):.2f}, {tokens_per_seq * batch / len(step_lengths) / batch:.2f} "
                        f"tokens/step/seq); sample wall {wall:.1f}s"),
@@ -313,17 +323,21 @@ def main():
     gm = {"auto": L.GEMM_AUTO, "simt": L.GEMM_SIMT, "tc": L.GEMM_TC}[args.gemm]
     wm.set_gemm(gm)
     wd.set_gemm(gm)
-    b, P, new = cfg["batch"], cfg["prompt"], cfg["new"]
+    from paper_2404_15778_b200.shard import gather_tokens, global_sequence_ids, reduce_run
+    # sequence-sharded: a rank owns a contiguous range of global sequences;
+    # prompts and RNG keys derive from the global id, so outputs are
+    # sharding-independent.  c2/c3: batch per GPU (weak scaling); c5: a fixed
+    # global batch split over the ranks (strong scaling)
+    n_total = cfg.get("global_batch", cfg["batch"] * world)
+    scaling = "strong" if "global_batch" in cfg else "weak"
+    sids = global_sequence_ids(n_total, world, rank)
+    b, P, new = len(sids), cfg["prompt"], cfg["new"]
     ctl_params = B.DraftLengthParams()
     cap = P + new + ctl_params.limit + 8
     main_m = B.CudaModel(wm, b, args.strategy, capacity=cap)
     draft_m = B.CudaModel(wd, b, args.strategy, capacity=cap)
     eng = B.CudaEngine(main_m, draft_m)
     eng.set_strategy(args.strategy)
-    # sequence-sharded: rank owns global sequences [rank*b, (rank+1)*b); prompts
-    # and RNG keys derive from the global id, so outputs are sharding-independent
-    from paper_2404_15778_b200.shard import gather_tokens, global_sequence_ids, reduce_run
-    sids = global_sequence_ids(b * world, world, rank)
     prompts = [np.random.default_rng(1_000_003 + sid).integers(0, mcfg.vocab_size, P).tolist()
                for sid in sids]
     req = B.GenerationRequest(prompts, new, temperature=cfg["temperature"], top_p=cfg["top_p"],
@@ -422,7 +436,7 @@ def main():
     if world > 1:
         dev_s, host_s, tokens = reduce_run(torch.distributed, "cuda", dev_s, host_s, tokens)
         gathered = gather_tokens(torch.distributed, world, sids, results[-1][0].tokens)   # final gather
-        assert sorted(gathered) == list(range(b * world))
+        assert sorted(gathered) == list(range(n_total))
     if rank != 0:
         torch.distributed.destroy_process_group()
         return
@@ -482,9 +496,9 @@ def main():
         "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init weights, uniform prompt ids)",
-        "config": {"workload": cfg["workload"], "batch_per_gpu": b, "global_batch": b * world,
+        "config": {"workload": cfg["workload"], "batch_per_gpu": b, "global_batch": n_total,
                    "prompt_len": P, "max_new_tokens": new, "step": "one full generation",
                    "draft_harness": (f"keyed override, align={args.align}" if args.align >= 0
                                      else "natural acceptance (draft samples its own proposals)"),
