@@ -141,12 +141,12 @@ int bass_attention(bass_ctx* ctx, int strategy, int dtype, int n_seq,
                    const void* k_dev, const void* v_dev, int kv_stride,
                    void* out_dev);
 
-/* microbenchmark of the bf16 d_head = 128 tcgen05 attention as the forward
- * runs it: one plan, then `reps` back-to-back launches (+ split combine);
- * launch i reads K/V copy i % n_kv (k_dev / v_dev hold n_kv contiguous
- * [n_seq, n_head, kv_stride, 128] copies, so > L2 defeats caching).  Device
- * time per call from CUDA events on the context stream. */
-int bass_attention_bench(bass_ctx* ctx, int strategy, int n_seq, int n_head,
+/* microbenchmark of the bf16 tcgen05 attention (d_head 64 or 128) as the
+ * forward runs it: one plan, then `reps` back-to-back launches (+ split
+ * combine); launch i reads K/V copy i % n_kv (k_dev / v_dev hold n_kv
+ * contiguous [n_seq, n_head, kv_stride, d_head] copies, so > L2 defeats
+ * caching).  Device time per call from CUDA events on the context stream. */
+int bass_attention_bench(bass_ctx* ctx, int strategy, int n_seq, int n_head, int d_head,
                          const int32_t* cu_q_host, const int32_t* offsets_host,
                          const void* q_dev, const void* k_dev, const void* v_dev,
                          int kv_stride, int n_kv, void* out_dev, int reps,

@@ -82,7 +82,7 @@ SIGNATURES = {
                                   C.c_int, f64p]),
     "bass_attention": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, i32p, i32p,
                                  vp, vp, vp, C.c_int, vp]),
-    "bass_attention_bench": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, i32p, i32p, vp, vp, vp, C.c_int,
+    "bass_attention_bench": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, i32p, i32p, vp, vp, vp, C.c_int,
                                        C.c_int, vp, C.c_int, f64p]),
     "bass_trace_enable": (C.c_int, [vp, C.c_int64]),
     "bass_trace_read": (C.c_int, [vp, C.POINTER(C.c_uint64), C.c_int64, C.POINTER(C.c_int64)]),

@@ -1,6 +1,9 @@
 // Persistent warp-specialised flash-decoding attention on tcgen05 (sm_100a),
-// d_head = 128 — the ragged verify / draft / prefill attention of BASS
-// (PAD and SPLIT, ref:attention.py:85-154).
+// d_head = 128 or 64 — the ragged verify / draft / prefill attention of BASS
+// (PAD and SPLIT, ref:attention.py:85-154).  d_head = 64 (the OPT-125M-shape
+// draft of C3) keeps the same 128-lane orientation: S^T = K . Q^T is one
+// 64-wide K block instead of two, and O^T = V^T . P^T runs as an M = 128 MMA
+// whose upper 64 rows (the K block stored after V) are never read back.
 //
 // Work item = (sequence, query tile of NQ rows, head, 1024-key split).  The
 // grid is persistent (<= one CTA per SM); CTA b walks items b, b + grid, ...
@@ -29,6 +32,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <utility>
 
 #include "runtime.h"
@@ -36,7 +40,7 @@
 namespace bass {
 namespace ast {
 
-constexpr int DH = 128, CH = 128, SPLIT_CH = 8, SPLIT = CH * SPLIT_CH, THREADS = 192;
+constexpr int CH = 128, SPLIT_CH = 8, SPLIT = CH * SPLIT_CH, THREADS = 192;
 constexpr float TH = 8.f;   // reuse the reference max while scores stay below it + TH (log2 units)
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -256,14 +260,19 @@ __device__ unsigned long long* g_attn_probe;
 // histories (decode / verify: items of 1-3 chunks, measured faster end to
 // end) and 3 for long ones (the launch picks by the longest history);
 // NQ = 64 is smem bound at 2.
-template <int NQ, int ST = (NQ == 32 ? 3 : 2)>
+template <int NQ, int DH = 128, int ST = (NQ == 32 || DH == 64 ? 3 : 2)>
 struct Cfg {
     static constexpr int STAGES = ST;
+    static constexpr int SUB = DH / 64;           // 64-wide (128-byte swizzle) column blocks of K, V, Q
     static constexpr int KV_TILE = CH * 128;      // 128 rows x 64 bf16 (one 128B-swizzle sub-tile)
-    static constexpr int STAGE = 4 * KV_TILE;     // K0 K1 V0 V1
+    static constexpr int STAGE = 2 * SUB * KV_TILE;   // d_head 128: K0 K1 V0 V1; d_head 64: V0 K0
+    // (V0 first for d_head 64, so the PV MMA's second 64-row A block, LBO =
+    // KV_TILE past V0, lands on K0 of the same stage — inside the allocation)
+    static constexpr int K_OFF = DH == 64 ? KV_TILE : 0;
+    static constexpr int V_OFF = DH == 64 ? 0 : SUB * KV_TILE;
     static constexpr int R_TILE = NQ * 128;       // NQ rows x 64 bf16: one sub-tile of Q or P
-    static constexpr int OFF_Q = STAGES * STAGE;  // 2 buffers x 2 sub-tiles
-    static constexpr int OFF_P = OFF_Q + 4 * R_TILE;
+    static constexpr int OFF_Q = STAGES * STAGE;  // 2 buffers x SUB sub-tiles
+    static constexpr int OFF_P = OFF_Q + 2 * SUB * R_TILE;
     static constexpr int P_BUF = CH * NQ * 2;     // P^T [128 keys][NQ] bf16, MN-major (queries contiguous)
     static constexpr int OFF_RED = OFF_P + 2 * P_BUF;    // red[4][NQ], fin, mref, thr, alph [NQ]
     static constexpr int OFF_BAR = OFF_RED + 8 * NQ * 4;
@@ -278,15 +287,15 @@ struct Cfg {
 __host__ __device__ constexpr int softmax_groups(int nq) { return nq >= 32 ? 4 : 2; }
 __host__ __device__ constexpr int attn_threads(int nq) { return 64 + 128 * softmax_groups(nq); }
 
-template <int NQ, int STG>
+template <int NQ, int DH, int STG>
 __global__ void __launch_bounds__(attn_threads(NQ), 1) attn_stream_kernel(
     const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
     const __grid_constant__ CUtensorMap tv, Seqs seqs, const Work* __restrict__ work, int n_items, int H, int cap,
     float* __restrict__ part_o, float* __restrict__ part_ml, int max_splits, __nv_bfloat16* __restrict__ out,
     TraceArg tr) {
     const unsigned long long t_start = tr.buf ? gtimer() : 0ull;
-    using Cf = Cfg<NQ, STG>;
-    constexpr int ST = Cf::STAGES;
+    using Cf = Cfg<NQ, DH, STG>;
+    constexpr int ST = Cf::STAGES, SUB = Cf::SUB;
     constexpr int SG = softmax_groups(NQ), CQ = NQ / SG;
     if (threadIdx.x == 0) APROBE(0);
     extern __shared__ uint8_t smem_raw[];
@@ -361,12 +370,14 @@ __global__ void __launch_bounds__(attn_threads(NQ), 1) attn_stream_kernel(
                 const int st = g % ST;
                 if (g >= ST) mbar_wait(su32(&kv_empty[st]), ((g / ST) - 1) & 1);
                 const uint32_t sb = base + st * Cf::STAGE;
-                mbar_expect_tx(su32(&k_full[st]), 2 * Cf::KV_TILE);
-                for (int s = 0; s < 2; ++s)
-                    tma_2d_ef(&tk, sb + s * Cf::KV_TILE, su32(&k_full[st]), s * 64, kv_row0 + c * CH, kpol);
-                mbar_expect_tx(su32(&v_full[st]), 2 * Cf::KV_TILE);
-                for (int s = 0; s < 2; ++s)
-                    tma_2d_ef(&tv, sb + (2 + s) * Cf::KV_TILE, su32(&v_full[st]), s * 64, kv_row0 + c * CH, kpol);
+                mbar_expect_tx(su32(&k_full[st]), SUB * Cf::KV_TILE);
+                for (int s = 0; s < SUB; ++s)
+                    tma_2d_ef(&tk, sb + Cf::K_OFF + s * Cf::KV_TILE, su32(&k_full[st]), s * 64, kv_row0 + c * CH,
+                              kpol);
+                mbar_expect_tx(su32(&v_full[st]), SUB * Cf::KV_TILE);
+                for (int s = 0; s < SUB; ++s)
+                    tma_2d_ef(&tv, sb + Cf::V_OFF + s * Cf::KV_TILE, su32(&v_full[st]), s * 64, kv_row0 + c * CH,
+                              kpol);
                 ++g;
             };
             // first item: its leading history chunks before the dependency wait
@@ -381,9 +392,9 @@ __global__ void __launch_bounds__(attn_threads(NQ), 1) attn_stream_kernel(
                 const int slot = wk.slot, q0row = wk.q0row;
                 const int qb = n & 1;
                 if (n >= 2) mbar_wait(su32(&q_empty[qb]), ((n >> 1) - 1) & 1);
-                mbar_expect_tx(su32(&q_full[qb]), 2 * Cf::R_TILE);
-                for (int s = 0; s < 2; ++s)
-                    tma_2d(&tq, base + Cf::OFF_Q + (2 * qb + s) * Cf::R_TILE, su32(&q_full[qb]), h * DH + s * 64,
+                mbar_expect_tx(su32(&q_full[qb]), SUB * Cf::R_TILE);
+                for (int s = 0; s < SUB; ++s)
+                    tma_2d(&tq, base + Cf::OFF_Q + (SUB * qb + s) * Cf::R_TILE, su32(&q_full[qb]), h * DH + s * 64,
                            q0row + wk.t0);
                 const int kv_row0 = (slot * H + h) * cap + wk.split * SPLIT;
                 if (n == 0) APROBE(3);
@@ -408,7 +419,9 @@ __global__ void __launch_bounds__(attn_threads(NQ), 1) attn_stream_kernel(
                 mbar_wait(su32(&p_full[sb]), (p.g >> 1) & 1);
                 mbar_wait(su32(&v_full[p.st]), (p.g / ST) & 1);
                 fence_after();
-                const uint32_t vs = base + p.st * Cf::STAGE + 2 * Cf::KV_TILE;
+                // A = V^T (MN-major): the second 64-dim block is LBO = KV_TILE past V0
+                // (d_head 64: K0 of the same stage; those O^T rows are never read)
+                const uint32_t vs = base + p.st * Cf::STAGE + Cf::V_OFF;
                 const uint32_t ps = base + Cf::OFF_P + sb * Cf::P_BUF;
                 const uint32_t d = tmem + 2 * NQ + p.ob * NQ;
 #pragma unroll
@@ -434,8 +447,8 @@ __global__ void __launch_bounds__(attn_threads(NQ), 1) attn_stream_kernel(
                     if (g < 4) APROBE(8 + g);
                     if (g >= 2) mbar_wait(su32(&s_free[sb]), ((g >> 1) - 1) & 1);
                     fence_after();
-                    const uint32_t ks = base + st * Cf::STAGE;
-                    const uint32_t qs = base + Cf::OFF_Q + 2 * qb * Cf::R_TILE;
+                    const uint32_t ks = base + st * Cf::STAGE + Cf::K_OFF;
+                    const uint32_t qs = base + Cf::OFF_Q + SUB * qb * Cf::R_TILE;
 #pragma unroll
                     for (int kk = 0; kk < DH / 16; ++kk) {
                         const uint32_t sub = kk >> 2, in = (kk & 3) * 32;
@@ -606,6 +619,7 @@ __global__ void __launch_bounds__(attn_threads(NQ), 1) attn_stream_kernel(
                 if (j >= ncol || off + t < s0) continue;   // padded row / row does not see this split
                 const int row = q0row + t;
                 const float l = fin_g[j];
+                if (DH < 128 && key >= DH) continue;   // O^T lanes past d_head: padding rows
                 if (off + t < SPLIT) {   // whole history in split 0: normalised output
                     out[((int64_t)row * H + h) * DH + key] = __float2bfloat16_rn(o[j] / l);
                 } else {
@@ -659,41 +673,44 @@ static CUtensorMap map2d(const void* ptr, int64_t rows, int64_t cols, int64_t ro
     return m;
 }
 
-static const CUtensorMap& kv_map(const void* ptr, int64_t rows) {
-    static std::map<std::pair<const void*, int64_t>, CUtensorMap> cache;
-    auto key = std::make_pair(ptr, rows);
+// K / V cache tensor maps (rows of d_head elements, 64-column x 128-row boxes),
+// keyed by everything they encode
+static const CUtensorMap& kv_map(const void* ptr, int64_t rows, int dh) {
+    static std::map<std::tuple<const void*, int64_t, int>, CUtensorMap> cache;
+    auto key = std::make_tuple(ptr, rows, dh);
     auto it = cache.find(key);
-    if (it == cache.end()) it = cache.emplace(key, map2d(ptr, rows, DH, DH, CH)).first;
+    if (it == cache.end()) it = cache.emplace(key, map2d(ptr, rows, dh, dh, CH)).first;
     return it->second;
 }
 
-template <int NQ, int STG = Cfg<NQ>::STAGES>
+template <int NQ, int DH, int STG = Cfg<NQ, DH>::STAGES>
 static void launch(bass_ctx* ctx, const AttnPlan& p, const CUtensorMap& tk, const CUtensorMap& tv, const Seqs& seqs,
                    const Work* wp, int nw, float* po, float* pml, __nv_bfloat16* out) {
-    if constexpr (NQ == 16 && STG == 2) {
+    if constexpr (NQ == 16 && DH == 128 && STG == 2) {
         // long histories stream better with a third K/V stage
         if (p.max_len > 768) {
-            launch<16, 3>(ctx, p, tk, tv, seqs, wp, nw, po, pml, out);
+            launch<16, DH, 3>(ctx, p, tk, tv, seqs, wp, nw, po, pml, out);
             return;
         }
     }
-    using Cf = Cfg<NQ, STG>;
+    using Cf = Cfg<NQ, DH, STG>;
     static unsigned attr = 0;
     once_per_device(attr, [] {
-        BASS_CUDA(cudaFuncSetAttribute(attn_stream_kernel<NQ, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        BASS_CUDA(cudaFuncSetAttribute(attn_stream_kernel<NQ, DH, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        Cf::SMEM));
     });
     const int n_items = nw * p.H;
     const int grid = std::max(1, std::min(n_items, ctx->sm_count));
-    BASS_CUDA(launch_pdl(attn_stream_kernel<NQ, STG>, dim3(grid), dim3(attn_threads(NQ)), (size_t)Cf::SMEM, ctx->stream, p.tq, tk,
-                         tv, seqs, wp, n_items, p.H, p.cap, po, pml, p.mc, out, ctx->trace(grid, BASS_TR_ATTN)));
+    BASS_CUDA(launch_pdl(attn_stream_kernel<NQ, DH, STG>, dim3(grid), dim3(attn_threads(NQ)), (size_t)Cf::SMEM,
+                         ctx->stream, p.tq, tk, tv, seqs, wp, n_items, p.H, p.cap, po, pml, p.mc, out,
+                         ctx->trace(grid, BASS_TR_ATTN)));
 }
 
 }  // namespace ast
 
 int stream_split_len() { return ast::SPLIT; }
 
-bool tc_attention_supported(int dtype, int dh) { return dtype == BASS_BF16 && dh == ast::DH; }
+bool tc_attention_supported(int dtype, int dh) { return dtype == BASS_BF16 && (dh == 128 || dh == 64); }
 
 // Plan: work items (seq, q tile, split, chunks seen) — RAGGED/SPLIT exact,
 // PAD over the padded [max q] x [max L] grid (padded keys streamed, masked).
@@ -745,8 +762,8 @@ void stream_attention_work(int strategy, const std::vector<int32_t>& slot, const
 
 void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, int n_slots,
                            const std::vector<int32_t>& slot, const std::vector<int32_t>& qn,
-                           const std::vector<int32_t>& off, int H, int cap, DevBuf& work_buf, AttnPlan& plan,
-                           const void* pre_work) {
+                           const std::vector<int32_t>& off, int H, int dh, int cap, DevBuf& work_buf,
+                           AttnPlan& plan, const void* pre_work) {
     using namespace ast;
     const int n_seq = (int)qn.size();
     int max_L = 0;
@@ -770,7 +787,8 @@ void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, in
         BASS_CUDA(cudaMemcpyAsync(wd, hst, w.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
         ctx->h2d_bytes += (int64_t)w.size() * 4;
     }
-    plan.tq = map2d(q, M, (int64_t)H * DH, (int64_t)H * DH, NQ);
+    plan.tq = map2d(q, M, (int64_t)H * dh, (int64_t)H * dh, NQ);
+    plan.dh = dh;
     plan.NQ = NQ;
     plan.pad_len = strategy == BASS_PAD ? max_L : 0;
     plan.max_len = max_L;
@@ -790,16 +808,20 @@ void stream_attention_run(bass_ctx* ctx, const AttnPlan& p, const void* kc, cons
                           float* part_o, float* part_ml, void* out) {
     using namespace ast;
     const int64_t kv_rows = (int64_t)p.n_slots * p.H * p.cap;
-    const CUtensorMap& tk = kv_map(kc, kv_rows);
-    const CUtensorMap& tv = kv_map(vc, kv_rows);
+    const CUtensorMap& tk = kv_map(kc, kv_rows, p.dh);
+    const CUtensorMap& tv = kv_map(vc, kv_rows, p.dh);
     const Work* wd = static_cast<const Work*>(p.work);
     __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out);
     auto go = [&](const Work* wp, int nw) {
         if (nw == 0) return;
+        const bool d64 = p.dh == 64;
         switch (p.NQ) {
-            case 16: launch<16>(ctx, p, tk, tv, seqs_dev, wp, nw, part_o, part_ml, o); break;
-            case 32: launch<32>(ctx, p, tk, tv, seqs_dev, wp, nw, part_o, part_ml, o); break;
-            default: launch<64>(ctx, p, tk, tv, seqs_dev, wp, nw, part_o, part_ml, o); break;
+            case 16: d64 ? launch<16, 64>(ctx, p, tk, tv, seqs_dev, wp, nw, part_o, part_ml, o)
+                         : launch<16, 128>(ctx, p, tk, tv, seqs_dev, wp, nw, part_o, part_ml, o); break;
+            case 32: d64 ? launch<32, 64>(ctx, p, tk, tv, seqs_dev, wp, nw, part_o, part_ml, o)
+                         : launch<32, 128>(ctx, p, tk, tv, seqs_dev, wp, nw, part_o, part_ml, o); break;
+            default: d64 ? launch<64, 64>(ctx, p, tk, tv, seqs_dev, wp, nw, part_o, part_ml, o)
+                         : launch<64, 128>(ctx, p, tk, tv, seqs_dev, wp, nw, part_o, part_ml, o); break;
         }
         ctx->launches++;
         cudaError_t e = cudaGetLastError();

@@ -333,7 +333,7 @@ static void launch_attention_t(bass_ctx* ctx, int strategy, const void* q, const
                                int H, int cap, int n_slots, DevBuf& work_buf, DevBuf& po, DevBuf& pml,
                                void* out) {
     const int n_seq = (int)qn.size();
-    if constexpr (std::is_same<TA, __nv_bfloat16>::value && DH == 128) {
+    if constexpr (std::is_same<TA, __nv_bfloat16>::value && (DH == 128 || DH == 64)) {
         if (tc_attention_supported(BASS_BF16, DH)) {   // persistent TMA + tcgen05 kernel (attn_stream.cu)
             double abytes = 0.0, aflops = 0.0;
             for (int i = 0; i < n_seq; ++i) {
@@ -344,7 +344,7 @@ static void launch_attention_t(bass_ctx* ctx, int strategy, const void* q, const
             AttnPlan plan;
             std::vector<int32_t> ident(n_seq);
             for (int i = 0; i < n_seq; ++i) ident[i] = i;   // standalone: sequence i uses K/V entry i
-            stream_attention_plan(ctx, strategy, q, M, n_slots, ident, qn, off, H, cap, work_buf, plan);
+            stream_attention_plan(ctx, strategy, q, M, n_slots, ident, qn, off, H, DH, cap, work_buf, plan);
             float* so = (float*)po.need((size_t)M * H * plan.mc * DH * 4, ctx->stream);
             float* sml = (float*)pml.need((size_t)M * H * plan.mc * 2 * 4, ctx->stream);
             stream_attention_run(ctx, plan, kc, vc, seqs_dev, so, sml, out);
@@ -506,7 +506,7 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
     double attn_bytes = 0.0, attn_flops = 0.0;
     float *pa_o = nullptr, *pa_ml = nullptr;
     if (m.dtype == BASS_BF16 && tc_attention_supported(BASS_BF16, dh)) {
-        stream_attention_plan(ctx, strategy, q, M, kv.n_slots, b.slot, b.qn, b.off, H, kv.cap, work_buf, plan,
+        stream_attention_plan(ctx, strategy, q, M, kv.n_slots, b.slot, b.qn, b.off, H, dh, kv.cap, work_buf, plan,
                               pre ? pre->work : nullptr);
         pa_o = (float*)m.part_o.need((size_t)M * H * plan.mc * dh * 4, st);
         pa_ml = (float*)m.part_ml.need((size_t)M * H * plan.mc * 2 * 4, st);
@@ -522,9 +522,14 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
             ProfScope prof(ctx, BASS_PROF_ATTN, attn_bytes, attn_flops);
             stream_attention_run(ctx, plan, kc, vc, seqs, pa_o, pa_ml, cx);
             if (plan.needs_combine) {
-                BASS_CUDA(launch_pdl(attn_combine_kernel<__nv_bfloat16, 128>, dim3(M, H), dim3(128), 0, st,
-                                     (const float*)pa_o, (const float*)pa_ml, rows.pos, H, plan.mc,
-                                     stream_split_len(), (__nv_bfloat16*)cx, 1));
+                if (dh == 64)
+                    BASS_CUDA(launch_pdl(attn_combine_kernel<__nv_bfloat16, 64>, dim3(M, H), dim3(64), 0, st,
+                                         (const float*)pa_o, (const float*)pa_ml, rows.pos, H, plan.mc,
+                                         stream_split_len(), (__nv_bfloat16*)cx, 1));
+                else
+                    BASS_CUDA(launch_pdl(attn_combine_kernel<__nv_bfloat16, 128>, dim3(M, H), dim3(128), 0, st,
+                                         (const float*)pa_o, (const float*)pa_ml, rows.pos, H, plan.mc,
+                                         stream_split_len(), (__nv_bfloat16*)cx, 1));
                 check_launch(ctx);
             }
         } else {
@@ -1212,11 +1217,13 @@ int bass_attn_probe(int on, unsigned long long* out) {
     return 0;
 }
 #endif
-int bass_attention_bench(bass_ctx* c, int strategy, int n_seq, int n_head, const int32_t* cu_q, const int32_t* offsets,
-                         const void* q, const void* k, const void* v, int kv_stride, int n_kv, void* out, int reps,
-                         double* ms_per_call) {
+int bass_attention_bench(bass_ctx* c, int strategy, int n_seq, int n_head, int d_head, const int32_t* cu_q,
+                         const int32_t* offsets, const void* q, const void* k, const void* v, int kv_stride, int n_kv,
+                         void* out, int reps, double* ms_per_call) {
     return guarded(c, [&] {
         BASS_REQUIRE(n_seq >= 1 && reps >= 1 && n_kv >= 1, "attention bench: bad sizes");
+        BASS_REQUIRE(tc_attention_supported(BASS_BF16, d_head), "attention bench: d_head must be 64 or 128");
+        const int DHb = d_head;
         std::vector<int32_t> slot(n_seq), q0(n_seq), qn(n_seq), off(n_seq), row_pos;
         for (int i = 0; i < n_seq; ++i) {
             slot[i] = i;
@@ -1235,18 +1242,23 @@ int bass_attention_bench(bass_ctx* c, int strategy, int n_seq, int n_head, const
         upload_i32(c, dm, hm.data(), hm.size());
         Seqs seqs{dm, dm + n_seq, dm + 2 * n_seq, dm + 3 * n_seq};
         AttnPlan plan;
-        stream_attention_plan(c, strategy, q, M, n_seq, slot, qn, off, H, kv_stride, work, plan);
-        float* so = (float*)po.need((size_t)M * H * plan.mc * 128 * 4, c->stream);
+        stream_attention_plan(c, strategy, q, M, n_seq, slot, qn, off, H, DHb, kv_stride, work, plan);
+        float* so = (float*)po.need((size_t)M * H * plan.mc * DHb * 4, c->stream);
         float* sml = (float*)pml.need((size_t)M * H * plan.mc * 2 * 4, c->stream);
-        const size_t kv_bytes = (size_t)n_seq * H * kv_stride * 128 * 2;
+        const size_t kv_bytes = (size_t)n_seq * H * kv_stride * DHb * 2;
         auto call = [&](int i) {
             const char* kc = (const char*)k + (size_t)(i % n_kv) * kv_bytes;
             const char* vc = (const char*)v + (size_t)(i % n_kv) * kv_bytes;
             stream_attention_run(c, plan, kc, vc, seqs, so, sml, out);
             if (plan.needs_combine) {
-                BASS_CUDA(launch_pdl(attn_combine_kernel<__nv_bfloat16, 128>, dim3(M, H), dim3(128), 0, c->stream,
-                                     (const float*)so, (const float*)sml, (const int32_t*)(dm + 4 * n_seq), H, plan.mc,
-                                     stream_split_len(), (__nv_bfloat16*)out, 1));
+                if (DHb == 64)
+                    BASS_CUDA(launch_pdl(attn_combine_kernel<__nv_bfloat16, 64>, dim3(M, H), dim3(64), 0, c->stream,
+                                         (const float*)so, (const float*)sml, (const int32_t*)(dm + 4 * n_seq), H,
+                                         plan.mc, stream_split_len(), (__nv_bfloat16*)out, 1));
+                else
+                    BASS_CUDA(launch_pdl(attn_combine_kernel<__nv_bfloat16, 128>, dim3(M, H), dim3(128), 0, c->stream,
+                                         (const float*)so, (const float*)sml, (const int32_t*)(dm + 4 * n_seq), H,
+                                         plan.mc, stream_split_len(), (__nv_bfloat16*)out, 1));
                 check_launch(c);
             }
         };

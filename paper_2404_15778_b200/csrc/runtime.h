@@ -229,7 +229,7 @@ struct AttnPlan {
     bool stream = false;                 // streaming flash-decoding kernel (attn_stream.cu)
     bool needs_combine = false;          // some row spans more than one 1024-key split
     int max_len = 0;                     // longest history + block (stream kernel: stage count choice)
-    int NQ = 0, pad_len = 0, strategy = 0, H = 0, cap = 0, n_slots = 0, mc = 0, tmem_cols = 32;
+    int NQ = 0, pad_len = 0, strategy = 0, H = 0, dh = 128, cap = 0, n_slots = 0, mc = 0, tmem_cols = 32;
     std::vector<int> first;
     void* work = nullptr;
     CUtensorMap tq;
@@ -239,8 +239,8 @@ bool tc_attention_supported(int dtype, int dh);
 int stream_split_len();
 void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, int n_slots,
                            const std::vector<int32_t>& slot, const std::vector<int32_t>& qn,
-                           const std::vector<int32_t>& off, int H, int cap, DevBuf& work_buf, AttnPlan& plan,
-                           const void* pre_work = nullptr);
+                           const std::vector<int32_t>& off, int H, int dh, int cap, DevBuf& work_buf,
+                           AttnPlan& plan, const void* pre_work = nullptr);
 // the stream attention's work list for a batch (what stream_attention_plan uploads)
 void stream_attention_work(int strategy, const std::vector<int32_t>& slot, const std::vector<int32_t>& qn,
                            const std::vector<int32_t>& off, const std::vector<int32_t>& safe,

@@ -2,8 +2,8 @@
 C2 decode shapes, through bass_attention_bench: one plan, back-to-back
 launches timed with CUDA events, K/V copies rotated so the working set
 exceeds L2 (as in the forward, where ~0.5 GB of weights stream between two
-attention launches).  H = 36 (16 for the draft rows), d_head = 128, bf16
-K/V/Q ~ N(0, 1).  Achieved GB/s = algorithmic bytes (real K/V rows + Q in +
+attention launches).  H = 36 (16 for the draft rows), d_head = 128 (and 64),
+bf16 K/V/Q ~ N(0, 1).  Achieved GB/s = algorithmic bytes (real K/V rows + Q in +
 O out) / device time per call.  One JSON line per point.
 
     python tools/attn_bench.py [sweep|c2|all] [strategies]
@@ -37,45 +37,59 @@ stream = torch.cuda.current_stream()
 ctx.set_stream(stream.cuda_stream)
 
 
-def point(lens, q_lens, H, strategy, tag, reps=20):
+_KV = {}
+
+
+def _kv(n, dh):
+    """one pool of random K/V rows per d_head, reused across points (views)"""
+    if _KV.get(dh) is None or _KV[dh][0].numel() < n:
+        _KV[dh] = None
+        torch.cuda.empty_cache()
+        _KV[dh] = (torch.randn(n, device="cuda", dtype=torch.bfloat16),
+                   torch.randn(n, device="cuda", dtype=torch.bfloat16))
+    return _KV[dh][0][:n], _KV[dh][1][:n]
+
+
+def point(lens, q_lens, H, strategy, tag, reps=20, dh=128):
     b = len(lens)
     stride = int(max(lens))
-    kv_bytes = b * H * stride * 128 * 2
+    kv_bytes = b * H * stride * dh * 2
     n_kv = max(1, min(16, int(300e6 // kv_bytes) + 1))
-    K = torch.randn(n_kv * b, H, stride, 128, device="cuda", dtype=torch.bfloat16)
-    V = torch.randn(n_kv * b, H, stride, 128, device="cuda", dtype=torch.bfloat16)
+    K, V = _kv(n_kv * b * H * stride * dh, dh)
     cu = np.concatenate([[0], np.cumsum(q_lens)]).astype(np.int32)
     offs = np.array([n - q for n, q in zip(lens, q_lens)], dtype=np.int32)
-    Q = torch.randn(int(cu[-1]), H, 128, device="cuda", dtype=torch.bfloat16)
+    Q = torch.randn(int(cu[-1]), H, dh, device="cuda", dtype=torch.bfloat16)
     out = torch.empty_like(Q)
     ms = C.c_double()
     torch.cuda.synchronize()
-    ctx.check(ctx.lib.bass_attention_bench(ctx.handle, strategy_code(strategy), b, H, L.ptr(cu, C.c_int32),
+    ctx.check(ctx.lib.bass_attention_bench(ctx.handle, strategy_code(strategy), b, H, dh, L.ptr(cu, C.c_int32),
                                            L.ptr(offs, C.c_int32), C.c_void_p(Q.data_ptr()),
                                            C.c_void_p(K.data_ptr()), C.c_void_p(V.data_ptr()), stride, n_kv,
                                            C.c_void_p(out.data_ptr()), reps, C.byref(ms)))
     t = ms.value / 1e3
-    by = sum(2 * H * int(n) * 128 * 2 + 2 * H * int(q) * 128 * 2 for n, q in zip(lens, q_lens))
+    by = sum(2 * H * int(n) * dh * 2 + 2 * H * int(q) * dh * 2 for n, q in zip(lens, q_lens))
     gbs = by / t / 1e9
-    rec = {"tag": tag, "b": b, "H": H, "q": int(max(q_lens)), "L": int(max(lens)), "strategy": strategy,
+    rec = {"tag": tag, "b": b, "H": H, "dh": dh, "q": int(max(q_lens)), "L": int(max(lens)), "strategy": strategy,
            "us": round(t * 1e6, 2), "MB": round(by / 1e6, 2), "GB/s": round(gbs, 1), "frac": round(gbs / HBM, 3)}
     print(json.dumps(rec), flush=True)
-    del K, V
-    torch.cuda.empty_cache()
     return rec
 
 
 def sweep(strategies):
-    for b in (1, 8, 64):
-        for Lc in (512, 2048, 8192):
+    """SURVEY 8(d) C4 grid: b in {1..64}, L in {512..8K}, draft length k in
+    {1, 2, 4, 8, 16} (q = k + 1) plus k = 32 (Alg. 1's limit); ragged lengths
+    L_i ~ U[L/2, L] for every strategy (PAD streams the padding), equal
+    lengths for the ragged kernel; d_head 64 (H = 36) on ragged lengths."""
+    for b in (1, 2, 4, 8, 16, 32, 64):
+        for Lc in (512, 1024, 2048, 4096, 8192):
             for ragged in (True, False):
                 rng = np.random.default_rng(b * 100003 + Lc)
                 lens = rng.integers(Lc // 2, Lc + 1, b) if ragged else np.full(b, Lc)
-                for k in (1, 8, 16, 32):
-                    for s in strategies:
-                        if s == "split" and b > 8:
-                            continue
+                for k in (1, 2, 4, 8, 16, 32):
+                    for s in (strategies if ragged else ["ragged"]):
                         point(lens.tolist(), [k + 1] * b, 36, s, f"c4{'r' if ragged else 'e'}")
+                    if ragged:
+                        point(lens.tolist(), [k + 1] * b, 36, "ragged", "c4r-dh64", dh=64)
 
 
 def c2(strategies):
@@ -95,9 +109,10 @@ def c2(strategies):
 
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
-    if what == "one":   # python tools/attn_bench.py one b q L H [strategy]  (ncu captures)
+    if what == "one":   # python tools/attn_bench.py one b q L H [strategy [dh]]  (ncu captures)
         b, q, Lc, H = (int(a) for a in sys.argv[2:6])
-        point([Lc] * b, [q] * b, H, sys.argv[6] if len(sys.argv) > 6 else "ragged", "one", reps=3)
+        point([Lc] * b, [q] * b, H, sys.argv[6] if len(sys.argv) > 6 else "ragged", "one", reps=3,
+              dh=int(sys.argv[7]) if len(sys.argv) > 7 else 128)
         sys.exit(0)
     strategies = (sys.argv[2] if len(sys.argv) > 2 else "ragged").split(",")
     if what in ("c2", "all"):
