@@ -95,6 +95,11 @@ int bass_model_get_weight(const bass_model* m, int tensor, int layer,
  * N(0,0.02) on the fp32 grid, ref:model.py:106-132); LN gains 1, biases 0 */
 int bass_model_init_random(bass_model* m, uint64_t seed, float std);
 int bass_model_set_gemm(bass_model* m, int gemm_mode);
+/* split-K count of the tcgen05 GEMM for one (N, K) projection shape of this
+ * model (1..8; 0 restores the default rule of gemm_tc.cu choose_splits).
+ * Splits are a function of the shape only, never of M (row bits stay
+ * batch-invariant); this is the per-model tuning hook. */
+int bass_model_set_split(bass_model* m, int N, int K, int splits);
 int64_t bass_model_weight_bytes(const bass_model* m);
 
 /* Ragged KV cache: per (layer, slot, head) contiguous [capacity, d_head]

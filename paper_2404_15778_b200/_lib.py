@@ -72,6 +72,7 @@ SIGNATURES = {
     "bass_model_init_random": (C.c_int, [vp, C.c_uint64, C.c_float]),
     "bass_model_set_gemm": (C.c_int, [vp, C.c_int]),
     "bass_model_weight_bytes": (C.c_int64, [vp]),
+    "bass_model_set_split": (C.c_int, [vp, C.c_int, C.c_int, C.c_int]),
     "bass_kv_create": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(vp)]),
     "bass_kv_destroy": (C.c_int, [vp]),
     "bass_kv_lengths": (C.c_int, [vp, i32p]),

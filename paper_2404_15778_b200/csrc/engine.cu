@@ -12,7 +12,7 @@
 #include <cstring>
 
 #include "runtime.h"
-#include "sampling_kernels.cuh"
+#include "cluster_sampling.cuh"
 
 using namespace bass;
 
@@ -354,7 +354,7 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                     ProfScope prof(c, BASS_PROF_SAMPLE, (double)nA * V * 4);
                     if (greedy) BASS_CUDA(launch_pdl(draft_greedy_split_kernel, dim3(nA, GREEDY_PARTS), dim3(256), 0, st,
                                                      (const float*)out, V, dp, pick_v, pick_i, pick_cnt));
-                    else draft_sample_kernel<<<nA, SM_THREADS, 0, st>>>(out, V, r->temperature, r->top_p, r->seed,
+                    else cl_draft_sample_kernel<<<nA * CL_CTAS, CL_THREADS, 0, st>>>(out, V, r->temperature, r->top_p, r->seed,
                                                                          scratch, dp);
                     launched(c);
                 }
@@ -378,9 +378,9 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                                   e->props(), e->pstride, vlog, dlog, scratch, accf, corr, btok};
                     ProfScope prof(c, BASS_PROF_SAMPLE, (double)R * V * 8);
                     Shaped* shp = (Shaped*)e->shaped.need((size_t)nA * (l + 1) * 2 * sizeof(Shaped), st);
-                    verify_shape_kernel<<<dim3(l + 1, nA, 2), SM_THREADS, 0, st>>>(va, shp);
+                    cl_verify_shape_kernel<<<dim3((l + 1) * CL_CTAS, nA, 2), CL_THREADS, 0, st>>>(va, shp);
                     launched(c);
-                    verify_accept_kernel<<<dim3(l + 1, nA), SM_THREADS, 0, st>>>(va, shp);
+                    cl_verify_accept_kernel<<<dim3((l + 1) * CL_CTAS, nA), CL_THREADS, 0, st>>>(va, shp);
                     launched(c);
                 }
                 StepArgs sa{nA, l, V, d_slot, d_com, d_gen, e->props(), e->pstride, vlog, vamax, vlse,
@@ -536,7 +536,7 @@ int bass_regular_generate(bass_engine* e, const bass_gen_request* r, bass_gen_re
                            r->top_p, r->seed, scratch, d_tok, d_lp};
             {
                 ProfScope prof(c, BASS_PROF_SAMPLE, (double)nA * V * 4);
-                regular_pick_kernel<<<nA, SM_THREADS, 0, st>>>(cur, ra);
+                cl_regular_pick_kernel<<<nA * CL_CTAS, CL_THREADS, 0, st>>>(cur, ra);
             }
             launched(c);
             c->d2h_bytes += (int64_t)nA * 12;

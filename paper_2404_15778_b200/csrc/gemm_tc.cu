@@ -990,6 +990,13 @@ void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N
     if (err != cudaSuccess) throw Error(BASS_ERR_CUDA, std::string("tcgen05 gemm launch: ") + cudaGetErrorString(err));
 }
 
+void tc_set_split(bass_model& m, int N, int K, int splits) {
+    tc::State& S = tc::state(m);
+    const auto key = std::make_pair(N, K);
+    if (splits > 0) S.splits[key] = splits;
+    else S.splits.erase(key);
+}
+
 void tc_release(bass_model& m) {
     if (!m.tc_state) return;
     tc::State* s = static_cast<tc::State*>(m.tc_state);

@@ -8,7 +8,7 @@
 #include <cstring>
 
 #include "runtime.h"
-#include "sampling_kernels.cuh"
+#include "cluster_sampling.cuh"
 
 using namespace bass;
 
@@ -981,6 +981,13 @@ int bass_model_set_gemm(bass_model* m, int mode) {
     });
 }
 
+int bass_model_set_split(bass_model* m, int N, int K, int splits) {
+    return guarded(m->ctx, [&] {
+        BASS_REQUIRE(splits >= 0 && splits <= 8, "split count must be in [0, 8] (0: the default rule)");
+        tc_set_split(*m, N, K, splits);
+    });
+}
+
 int64_t bass_model_weight_bytes(const bass_model* m) { return m ? m->weight_bytes : 0; }
 
 // ------------------------------------------------------------------- KV
@@ -1341,7 +1348,7 @@ int bass_shape_sample(bass_ctx* c, int n, int V, const float* logits, double T, 
         if (probs_out) BASS_CUDA(cudaMallocAsync((void**)&dp, (size_t)n * V * 8, c->stream));
         BASS_CUDA(cudaMemcpyAsync(dl, logits, (size_t)n * V * 4, cudaMemcpyHostToDevice, c->stream));
         BASS_CUDA(cudaMemcpyAsync(du, u, (size_t)n * 8, cudaMemcpyHostToDevice, c->stream));
-        shape_sample_kernel<<<n, SM_THREADS, 0, c->stream>>>(dl, V, T, top_p, du, scr, dt, dp);
+        cl_shape_sample_kernel<<<n * CL_CTAS, CL_THREADS, 0, c->stream>>>(dl, V, T, top_p, du, scr, dt, dp);
         check_launch(c);
         BASS_CUDA(cudaMemcpyAsync(tok_out, dt, (size_t)n * 4, cudaMemcpyDeviceToHost, c->stream));
         if (probs_out)
@@ -1375,7 +1382,7 @@ int bass_accept(bass_ctx* c, int n, int V, const float* ql, const float* pl, dou
         BASS_CUDA(cudaMemcpyAsync(dt, tok, (size_t)n * 4, cudaMemcpyHostToDevice, st));
         BASS_CUDA(cudaMemcpyAsync(ds, sid, (size_t)n * 8, cudaMemcpyHostToDevice, st));
         BASS_CUDA(cudaMemcpyAsync(dr, ctr, (size_t)n * 8, cudaMemcpyHostToDevice, st));
-        accept_pairs_kernel<<<n, SM_THREADS, 0, st>>>(dq, dp, V, T, top_p, dt, seed, ds, dr, scr, da, dc);
+        cl_accept_pairs_kernel<<<n * CL_CTAS, CL_THREADS, 0, st>>>(dq, dp, V, T, top_p, dt, seed, ds, dr, scr, da, dc);
         check_launch(c);
         BASS_CUDA(cudaMemcpyAsync(acc_out, da, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
         BASS_CUDA(cudaMemcpyAsync(corr_out, dc, (size_t)n * 4, cudaMemcpyDeviceToHost, st));

@@ -219,6 +219,8 @@ struct TcNorm {
 void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K,
              const Epi& e, bool packed, const TcNorm* norm = nullptr);
 void tc_release(bass_model& m);
+// per-model split-count override for one (N, K) projection shape (0: the default rule)
+void tc_set_split(bass_model& m, int N, int K, int splits);
 // pack n_mat contiguous [N, K] bf16 matrices into the packed layout (dst: n_mat * packed_rows(N) * K)
 void pack_weights(cudaStream_t st, const void* src, void* dst, int N, int K, int n_mat);
 

@@ -256,6 +256,10 @@ class DeviceWeights:
                                               C.c_void_p(w.data_ptr()), C.c_void_p(y.data_ptr())))
         return y
 
+    def set_split(self, N: int, K: int, splits: int):
+        """Split-K count for the (N, K) projection (0: default rule)."""
+        self.ctx.check(self.ctx.lib.bass_model_set_split(self.handle, N, K, splits))
+
     def set_gemm(self, mode: int):
         self.ctx.check(self.ctx.lib.bass_model_set_gemm(self.handle, mode))
 
