@@ -287,6 +287,8 @@ def main():
                          "natural acceptance: an overridden proposal may have zero draft probability")
     ap.add_argument("--strategy", default="ragged", choices=["pad", "split", "ragged"])
     ap.add_argument("--gemm", default="auto", choices=["auto", "simt", "tc"])
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "int8"],
+                    help="int8: the W8A8 path (SURVEY 8(f1), ref:quant.py) for main and draft")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="one profiled generation (ncu)")
     ap.add_argument("--save-traj", default=None, help="save the greedy trajectory (.npy)")
@@ -320,8 +322,8 @@ def main():
     stream = torch.cuda.Stream(device=local)
     ctx.set_stream(stream.cuda_stream)
     mcfg, dcfg = B.ModelConfig(*cfg["main"]), B.ModelConfig(*cfg["draft"])
-    wm = B.DeviceWeights.random(mcfg, seed=1000, ctx=ctx)
-    wd = B.DeviceWeights.random(dcfg, seed=2000, ctx=ctx)
+    wm = B.DeviceWeights.random(mcfg, seed=1000, dtype=args.dtype, ctx=ctx)
+    wd = B.DeviceWeights.random(dcfg, seed=2000, dtype=args.dtype, ctx=ctx)
     gm = {"auto": L.GEMM_AUTO, "simt": L.GEMM_SIMT, "tc": L.GEMM_TC}[args.gemm]
     wm.set_gemm(gm)
     wd.set_gemm(gm)
@@ -503,8 +505,10 @@ def main():
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_ms,
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
-        "dtype": "bf16", "data": "synthetic (random-init weights, uniform prompt ids)",
-        "config": {"workload": cfg["workload"], "batch_per_gpu": b, "global_batch": n_total,
+        "dtype": args.dtype, "data": "synthetic (random-init weights, uniform prompt ids)",
+        "config": {"workload": cfg["workload"] + (", INT8 W8A8 (int8 x int8 -> s32 tcgen05 GEMMs; "
+                                                  "bf16 attention / KV)" if args.dtype == "int8" else ""),
+                   "batch_per_gpu": b, "global_batch": n_total,
                    "prompt_len": P, "max_new_tokens": new, "step": "one full generation",
                    "draft_harness": (f"keyed override, align={args.align}" if args.align >= 0
                                      else "natural acceptance (draft samples its own proposals)"),

@@ -32,7 +32,13 @@ extern "C" {
 #define BASS_ERR_MEMORY   -3
 #define BASS_ERR_STATE    -4
 
-enum { BASS_BF16 = 0, BASS_F32 = 1 };                    /* weight/activation dtype */
+/* weight/activation dtype.  BASS_INT8: W8A8 — the reference's quantized
+ * inference path (ref:quant.py:55-129, model.py:135-143, 160-164, 219-222):
+ * int8 per-output-channel weights, per-token int8 activations into every
+ * linear layer, int8 x int8 -> s32 tensor-core GEMMs dequantized in the
+ * epilogue, q/k/v fake-quantized per (token, head); embeddings, residual
+ * stream, attention and KV cache as in the bf16 path. */
+enum { BASS_BF16 = 0, BASS_F32 = 1, BASS_INT8 = 2 };
 enum { BASS_PAD = 0, BASS_SPLIT = 1, BASS_RAGGED = 2 };  /* ref:attention.py:30-32 (+ragged work list) */
 enum { BASS_GEMM_AUTO = 0, BASS_GEMM_SIMT = 1, BASS_GEMM_TC = 2 };
 enum { BASS_ROLE_DRAFT = 0, BASS_ROLE_VERIFY = 1 };      /* ref:sampling.py:20-22 */
@@ -94,6 +100,11 @@ int bass_model_get_weight(const bass_model* m, int tensor, int layer,
 /* device-side N(0, std) init for benchmark-scale models (ref init is
  * N(0,0.02) on the fp32 grid, ref:model.py:106-132); LN gains 1, biases 0 */
 int bass_model_init_random(bass_model* m, uint64_t seed, float std);
+/* BASS_INT8 models: the quantized payload of one matrix in the reference
+ * layout ([in, out] int8, ref:quant.py:55-63 QuantTensor.payload) and its
+ * per-output-channel scales ([out] fp64, QuantTensor.scales). */
+int bass_model_get_qweight(const bass_model* m, int tensor, int layer,
+                           int8_t* payload_host, double* scales_host, int64_t n);
 int bass_model_set_gemm(bass_model* m, int gemm_mode);
 /* split-K count of the tcgen05 GEMM for one (N, K) projection shape of this
  * model (1..8; 0 restores the default rule of gemm_tc.cu choose_splits).
@@ -126,6 +137,17 @@ int bass_forward_ragged(bass_model* m, bass_kv* kv, int n_seq,
  * ref:model.py:160-164 (_linear), output-major weights. */
 int bass_gemm(bass_model* m, int gemm_mode, int M, int N, int K,
               const void* x_dev, const void* w_dev, float* y_dev);
+/* Integer-accumulate GEMM with the fused dequantizing epilogue
+ * (ref:quant.py:98-123 int_gemm_dequant, without bias / residual):
+ * out[t, c] = (sum_i a[t, i] w[i, c]) * sa[t] * sw[c] on the tcgen05
+ * kind::i8 path.  Host arrays: a [M, K] int8 (per-token payload), sa [M],
+ * w [K, N] int8 in the reference layout (per-channel payload), sw [N];
+ * out [M, N] fp32.  K % 128 == 0, N >= 128. */
+int bass_int_gemm_dequant(bass_ctx* ctx, int M, int N, int K,
+                          const int8_t* a_host, const double* sa_host,
+                          const int8_t* w_host, const double* sw_host,
+                          float* out_host);
+
 /* microbenchmark: `reps` back-to-back launches; launch i uses weight copy
  * i % n_w (w_dev holds n_w contiguous [N, K] copies); device time per launch
  * from CUDA events on the context stream.  gemm_mode 3: tcgen05 on copies

@@ -58,22 +58,32 @@ class Outcome:
 class OracleModel:
     """MainModel equivalent (ref:model.py:288-332)."""
 
-    def __init__(self, weights, n_slot, strategy="pad"):
+    def __init__(self, weights, n_slot, strategy="pad", quantized=False):
         g = weights["geometry"]
         self.w, self.strategy = weights, strategy
         self.cache = RaggedCache(g.n_layer, n_slot, g.n_head, g.d_head)
         self.vocab_size, self.max_seq_len = g.vocab_size, g.max_seq_len
+        # INT8 W8A8 path (ref:model.py:296-302 `quantized=True`)
+        self.qw = None
+        if quantized:
+            from .quant import prepare
+            self.qw = prepare(weights)
+
+    def _fwd(self, slots, blocks):
+        if self.qw is not None:
+            from .quant import forward_ragged_int8
+            return forward_ragged_int8(self.w, self.qw, self.cache, slots, blocks, self.strategy)
+        return forward_ragged(self.w, self.cache, slots, blocks, self.strategy)
 
     def prefill(self, slot, prompt):
         if len(prompt) == 0:
             raise ValueError("empty prompt: prefill needs at least one token")
         if self.cache.length(slot) != 0:
             raise ValueError(f"sequence {slot} already has cached context")
-        return forward_ragged(self.w, self.cache, [slot], [list(prompt)],
-                              self.strategy)[0][-1]
+        return self._fwd([slot], [list(prompt)])[0][-1]
 
     def forward(self, slots, blocks):
-        return forward_ragged(self.w, self.cache, slots, blocks, self.strategy)
+        return self._fwd(slots, blocks)
 
     def rollback(self, slot, n):
         self.cache.truncate(slot, n)

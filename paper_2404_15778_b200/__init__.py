@@ -13,6 +13,7 @@ from .engine import (CudaEngine, GenerationRequest, GenerationResult, SpecStepOu
                      decode_regular, decode_speculative, step_trace)
 from .model import (CudaAlignedDraft, CudaContext, CudaModel, DeviceWeights, ModelConfig,
                     desk_config)
+from .quant import GroupAxis, QuantTensor, int_gemm_dequant
 from .sampling import (ROLE_DRAFT, ROLE_VERIFY, device_accept, device_shape_sample,
                        device_uniforms)
 

@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BASS_LIB", os.path.join(_HERE, "libbass.so"))
 
 BASS_OK, BASS_ERR_VALUE, BASS_ERR_CUDA, BASS_ERR_MEMORY, BASS_ERR_STATE = 0, -1, -2, -3, -4
-BF16, F32 = 0, 1
+BF16, F32, INT8 = 0, 1, 2
 PAD, SPLIT, RAGGED = 0, 1, 2
 GEMM_AUTO, GEMM_SIMT, GEMM_TC = 0, 1, 2
 (W_TOK_EMB, W_POS_EMB, W_LN1_G, W_LN1_B, W_WQ, W_WK, W_WV, W_WO, W_LN2_G, W_LN2_B,
@@ -21,6 +21,7 @@ GEMM_AUTO, GEMM_SIMT, GEMM_TC = 0, 1, 2
 
 i32p = C.POINTER(C.c_int32)
 i64p = C.POINTER(C.c_int64)
+i8p = C.POINTER(C.c_int8)
 f32p = C.POINTER(C.c_float)
 f64p = C.POINTER(C.c_double)
 vp = C.c_void_p
@@ -70,6 +71,8 @@ SIGNATURES = {
     "bass_model_set_weight": (C.c_int, [vp, C.c_int, C.c_int, f32p, C.c_int64]),
     "bass_model_get_weight": (C.c_int, [vp, C.c_int, C.c_int, f32p, C.c_int64]),
     "bass_model_init_random": (C.c_int, [vp, C.c_uint64, C.c_float]),
+    "bass_model_get_qweight": (C.c_int, [vp, C.c_int, C.c_int, i8p, f64p, C.c_int64]),
+    "bass_int_gemm_dequant": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, i8p, f64p, i8p, f64p, f32p]),
     "bass_model_set_gemm": (C.c_int, [vp, C.c_int]),
     "bass_model_weight_bytes": (C.c_int64, [vp]),
     "bass_model_set_split": (C.c_int, [vp, C.c_int, C.c_int, C.c_int]),

@@ -119,6 +119,18 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
 __host__ __device__ constexpr uint32_t idesc(int tt) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(tt >> 3) << 17) | ((uint32_t)(BN >> 4) << 24);
 }
+// kind::i8: signed int8 x signed int8 -> s32 (D format 2, A / B format 1 = signed)
+__host__ __device__ constexpr uint32_t idesc_i8(int tt) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(tt >> 3) << 17) | ((uint32_t)(BN >> 4) << 24);
+}
+// one kind::i8 MMA consumes 32 int8 of k (32 bytes, the same step as 16 bf16)
+__device__ __forceinline__ void umma_i8(uint32_t dtmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(
+            dtmem),
+        "l"(a), "l"(b), "r"(id), "r"(acc)
+        : "memory");
+}
 __device__ __forceinline__ void umma(uint32_t dtmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
     asm volatile(
         "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(
@@ -146,9 +158,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 
 struct Split {
     int S;             // number of K splits
-    int k_iters;       // K / BK
-    float* ws;         // per (tile, token group): [S][TT][NB*BN] fp32 partials (S > 1)
+    int k_iters;       // K / BK (int8: K / 128 — a stage is always 128 bytes of k)
+    float* ws;         // per (tile, token group): [S][TT][NB*BN] fp32 partials (S > 1; int8: s32 bits)
     int evict_first;   // weights streamed with an L2 evict-first policy
+    const double* sx;  // int8 (W8A8): per-token activation scales [M]
+    const double* sw;  // int8 (W8A8): per-channel weight scales [N]
 };
 
 // LayerNorm folded into the GEMM (XN):  LN(x) W^T = rstd * ((x*g) W^T - mean * c) + e
@@ -167,7 +181,7 @@ struct XNorm {
 // before the first add, then summed in split order s = 0..S-1 (the fixed
 // order every path uses, so the bits do not depend on the path or on M).
 constexpr int MAX_S = 8;
-template <int U>
+template <int U, bool INT = false>
 __device__ __forceinline__ void dsmem_sum(uint32_t addr0, uint32_t row_stride, int S, float* acc) {
     float p[MAX_S][U];
 #pragma unroll
@@ -180,6 +194,17 @@ __device__ __forceinline__ void dsmem_sum(uint32_t addr0, uint32_t row_stride, i
                 asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(p[s][u]) : "r"(ra));
             }
         }
+    if constexpr (INT) {   // s32 partials (kind::i8): exact integer sum, bits returned in a float
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            int a = 0;
+#pragma unroll
+            for (int s = 0; s < MAX_S; ++s)
+                if (s < S) a += __float_as_int(p[s][u]);
+            acc[u] = __int_as_float(a);
+        }
+        return;
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) acc[u] = 0.f;
 #pragma unroll
@@ -189,7 +214,7 @@ __device__ __forceinline__ void dsmem_sum(uint32_t addr0, uint32_t row_stride, i
             for (int u = 0; u < U; ++u) acc[u] += p[s][u];
         }
 }
-template <int U>
+template <int U, bool INT = false>
 __device__ __forceinline__ void l2_sum(const float* p0, int64_t split_stride, int64_t row_stride, int S, float* acc) {
     float p[MAX_S][U];
 #pragma unroll
@@ -198,6 +223,17 @@ __device__ __forceinline__ void l2_sum(const float* p0, int64_t split_stride, in
 #pragma unroll
             for (int u = 0; u < U; ++u) p[s][u] = __ldcg(p0 + s * split_stride + u * row_stride);
         }
+    if constexpr (INT) {   // s32 partials (kind::i8): exact integer sum, bits returned in a float
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            int a = 0;
+#pragma unroll
+            for (int s = 0; s < MAX_S; ++s)
+                if (s < S) a += __float_as_int(p[s][u]);
+            acc[u] = __int_as_float(a);
+        }
+        return;
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) acc[u] = 0.f;
 #pragma unroll
@@ -229,12 +265,17 @@ __device__ int g_gp_n, g_gp_k;
 // (see XNorm); 2 (residual producer) the epilogue also emits the next
 // LayerNorm's row sums and X = bf16(x * g_next).  Compile-time, so the plain
 // kernels carry none of it.
-template <int TT, int MODE, int NB, bool PACKED, int LNF>
+// I8: W8A8 — int8 packed weights and int8 activations (kind::i8, s32
+// accumulators), dequantized in the epilogue: acc * sx[m] * sw[n] in fp64
+// (ref:quant.py:98-123 int_gemm_dequant).  LNF must be 0.
+template <int TT, int MODE, int NB, bool PACKED, int LNF, bool I8 = false>
 __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tw,
                                                              const __grid_constant__ CUtensorMap tx,
                                                              const __nv_bfloat16* __restrict__ wpk, int M, int N,
                                                              Split sp, Epi e, XNorm xn, TraceArg tr) {
     constexpr bool XN = LNF == 1;
+    static_assert(!I8 || (LNF == 0 && PACKED), "W8A8 GEMMs take packed weights and no folded LayerNorm");
+    constexpr int XK = I8 ? 128 : BK;   // k elements of X per stage (128 bytes either way)
     const unsigned long long t_start = tr.buf ? gtimer() : 0ull;
 #ifdef BASS_GEMM_PROBE
     const int gp_cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
@@ -315,7 +356,7 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
             asm volatile("griddepcontrol.wait;" ::: "memory");
             GPROBE(1);
             for (int i = 0; i < pre; ++i)
-                tma_2d(&tx, base + i * C::STAGE + C::W_BYTES, su32(&bars[i]), (it0 + i) * BK, m0);
+                tma_2d(&tx, base + i * C::STAGE + C::W_BYTES, su32(&bars[i]), (it0 + i) * XK, m0);
             for (int i = pre; i < nit; ++i) {
                 const int s = i % C::STAGES;
                 mbar_wait(su32(&bars[C::STAGES + s]), ((i / C::STAGES) - 1) & 1);
@@ -323,13 +364,13 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
                 const uint32_t st = base + s * C::STAGE;
                 mbar_expect_tx(full, C::STAGE);
                 load_w(st, full, it0 + i);
-                tma_2d(&tx, st + C::W_BYTES, full, (it0 + i) * BK, m0);
+                tma_2d(&tx, st + C::W_BYTES, full, (it0 + i) * XK, m0);
             }
         }
         __syncwarp();
     } else if (warp == 1) {
         if (lane == 0) {   // ---- MMA issuer: one accumulator (TT columns) per sub-tile
-            constexpr uint32_t ID = idesc(TT);
+            constexpr uint32_t ID = I8 ? idesc_i8(TT) : idesc(TT);
             for (int i = 0; i < nit; ++i) {
                 const int s = i % C::STAGES;
                 mbar_wait(su32(&bars[s]), (i / C::STAGES) & 1);
@@ -341,9 +382,14 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
                 for (int sub = 0; sub < NB; ++sub) {
                     const uint64_t a = sdesc(st + sub * BN * BK * 2);
 #pragma unroll
-                    for (int kk = 0; kk < BK / UK; ++kk)   // +32 bytes per UMMA_K step inside the swizzle row
-                        umma(tmem + sub * TT, a + (uint64_t)(kk * 2), b + (uint64_t)(kk * 2), ID,
-                             (i > 0 || kk > 0) ? 1u : 0u);
+                    for (int kk = 0; kk < BK / UK; ++kk) {   // +32 bytes per UMMA_K step inside the swizzle row
+                        if constexpr (I8)
+                            umma_i8(tmem + sub * TT, a + (uint64_t)(kk * 2), b + (uint64_t)(kk * 2), ID,
+                                    (i > 0 || kk > 0) ? 1u : 0u);
+                        else
+                            umma(tmem + sub * TT, a + (uint64_t)(kk * 2), b + (uint64_t)(kk * 2), ID,
+                                 (i > 0 || kk > 0) ? 1u : 0u);
+                    }
                 }
                 umma_commit(su32(&bars[C::STAGES + s]));
             }
@@ -410,6 +456,32 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
     fence_after();
     const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
     const int rows = min(TT, M - m0);
+    // W8A8: s32 accumulator bits -> acc * s_token * s_channel (fp64, ref:quant.py:119)
+    auto deq = [&](int m, int n, float bits) -> float {
+        if constexpr (I8) return (float)((double)__float_as_int(bits) * __ldg(sp.sx + m) * __ldg(sp.sw + n));
+        else return bits;
+    };
+    // W8A8 epilogues whose output is quantized next (ref:model.py:219-222, 243-244):
+    // QKV stores fp32 q|k|v and the max |value| per (row, head); FC applies the
+    // exact GELU, stores fp32 and the max per row.  Lanes hold consecutive
+    // columns, so a group's max is a warp shuffle reduction and one uint-ordered
+    // atomicMax (|v| >= 0) per group: order-independent, hence deterministic.
+    auto emit = [&](int m, int n, float bits) {
+        const float v0 = deq(m, n, bits);
+        if constexpr (I8 && (MODE == EPI_QKV || MODE == EPI_GELU)) {
+            const float v = MODE == EPI_GELU ? gelu_erf(v0) : v0;
+            reinterpret_cast<float*>(e.out)[(int64_t)m * N + n] = v;
+            const int grp = MODE == EPI_QKV ? min(e.dh, 32) : 32;
+            float a = fabsf(v);
+            for (int o = 1; o < grp; o <<= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+            if ((lane & (grp - 1)) == 0) {
+                const int64_t slot = MODE == EPI_QKV ? (int64_t)m * (N / e.dh) + n / e.dh : m;
+                atomicMax(reinterpret_cast<unsigned*>(e.amax) + slot, __float_as_uint(a));
+            }
+        } else {
+            epilogue<MODE, __nv_bfloat16>(e, m, n, N, v0);
+        }
+    };
     if constexpr (LNF == 0) {
     if (sp.S == 1) {
 #pragma unroll
@@ -423,7 +495,7 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
                 if (n < N) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
-                        if (c0 + j < rows) epilogue<MODE, __nv_bfloat16>(e, m0 + c0 + j, n, N, v[j]);
+                        if (c0 + j < rows) emit(m0 + c0 + j, n, v[j]);
                 }
             }
         }
@@ -462,14 +534,14 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
                 int r = rb;
                 for (; r + 4 <= re; r += 4) {   // 4 rows x S partials in flight
                     float acc[4];
-                    dsmem_sum<4>(part_s + (uint32_t)((r * WR + nn) * 4), WR * 4, sp.S, acc);
+                    dsmem_sum<4, I8>(part_s + (uint32_t)((r * WR + nn) * 4), WR * 4, sp.S, acc);
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) epilogue<MODE, __nv_bfloat16>(e, m0 + r + u, n, N, acc[u]);
+                    for (int u = 0; u < 4; ++u) emit(m0 + r + u, n, acc[u]);
                 }
                 for (; r < re; ++r) {
                     float acc;
-                    dsmem_sum<1>(part_s + (uint32_t)((r * WR + nn) * 4), WR * 4, sp.S, &acc);
-                    epilogue<MODE, __nv_bfloat16>(e, m0 + r, n, N, acc);
+                    dsmem_sum<1, I8>(part_s + (uint32_t)((r * WR + nn) * 4), WR * 4, sp.S, &acc);
+                    emit(m0 + r, n, acc);
                 }
             }
         }
@@ -508,14 +580,14 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
                 int r = rb;
                 for (; r + 4 <= re; r += 4) {   // 4 rows x S partials in flight
                     float acc[4];
-                    l2_sum<4>(blk + (int64_t)r * WR + nn, (int64_t)TT * WR, WR, sp.S, acc);
+                    l2_sum<4, I8>(blk + (int64_t)r * WR + nn, (int64_t)TT * WR, WR, sp.S, acc);
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) epilogue<MODE, __nv_bfloat16>(e, m0 + r + u, n, N, acc[u]);
+                    for (int u = 0; u < 4; ++u) emit(m0 + r + u, n, acc[u]);
                 }
                 for (; r < re; ++r) {
                     float acc;
-                    l2_sum<1>(blk + (int64_t)r * WR + nn, (int64_t)TT * WR, WR, sp.S, &acc);
-                    epilogue<MODE, __nv_bfloat16>(e, m0 + r, n, N, acc);
+                    l2_sum<1, I8>(blk + (int64_t)r * WR + nn, (int64_t)TT * WR, WR, sp.S, &acc);
+                    emit(m0 + r, n, acc);
                 }
             }
         }
@@ -814,14 +886,17 @@ static EncodeFn encoder() {
     return fn;
 }
 
-// 2D bf16 row-major [rows, cols] map with a box of {64 cols, box_rows}, 128B swizzle
-static CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int box_rows) {
+// 2D row-major [rows, cols] map with a box of {128 bytes of cols, box_rows}, 128B swizzle
+// (bf16: 64 columns; int8: 128 columns)
+static CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int box_rows, bool i8 = false) {
     CUtensorMap m;
+    const int es = i8 ? 1 : 2;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-    cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * es};
+    cuuint32_t box[2] = {(cuuint32_t)(128 / es), (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+    CUresult r = encoder()(&m, i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                           const_cast<void*>(ptr), dims, strides, box, estr,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(BASS_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
@@ -830,7 +905,7 @@ static CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int box
 
 struct State {
     std::map<std::tuple<const void*, int, int>, CUtensorMap> wmaps;
-    std::map<std::tuple<const void*, int, int, int>, CUtensorMap> xmaps;   // (X, M, K, TT)
+    std::map<std::tuple<const void*, int, int, int>, CUtensorMap> xmaps;   // (X, M, K, TT); int8 X: K < 0
     std::map<std::pair<int, int>, int> splits;
     DevBuf ws;
 };
@@ -868,13 +943,13 @@ struct LaunchArgs {
     XNorm xn;
 };
 
-template <int TT, int MODE, bool PACKED, int LNF>
+template <int TT, int MODE, bool PACKED, int LNF, bool I8 = false>
 static void launch_k(bass_model& m, const LaunchArgs& a, const Epi& e) {
     constexpr int NB = 1;   // (NB = 2 measured slower at every benchmark shape: profiles/r1_gemm_nb_split_sweep.txt)
     using C = Cfg<TT, NB>;
     static unsigned attr = 0;
     once_per_device(attr, [] {
-        BASS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<TT, MODE, NB, PACKED, LNF>,
+        BASS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<TT, MODE, NB, PACKED, LNF, I8>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     });
     cudaLaunchConfig_t cfg = {};
@@ -892,13 +967,23 @@ static void launch_k(bass_model& m, const LaunchArgs& a, const Epi& e) {
     cfg.attrs = at;
     cfg.numAttrs = a.sp.S > 1 ? 2 : 1;
     const int nblk = (int)(cfg.gridDim.x * cfg.gridDim.y * cfg.gridDim.z);
-    BASS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TT, MODE, NB, PACKED, LNF>, *a.wm, *a.xm,
+    BASS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TT, MODE, NB, PACKED, LNF, I8>, *a.wm, *a.xm,
                                  (const __nv_bfloat16*)a.W, a.M, a.N, a.sp, e, a.xn,
                                  m.ctx->trace(nblk, BASS_TR_GEMM)));
 }
 
 template <int TT>
 static void launch_mode(bass_model& m, int mode, bool packed, bool xn, const LaunchArgs& a, const Epi& e) {
+    if (a.sp.sx) {   // W8A8 (packed int8 weights): plain epilogues after the dequantization
+        if (!packed || xn) throw Error(BASS_ERR_STATE, "int8 GEMM: packed weights, no folded LayerNorm");
+        if ((mode == EPI_QKV || mode == EPI_GELU) && (!e.amax || a.N % 32 != 0))
+            throw Error(BASS_ERR_STATE, "int8 QKV / GELU epilogues need the amax buffer and N % 32 == 0");
+        if (mode == EPI_RESID) launch_k<TT, EPI_RESID, true, 0, true>(m, a, e);
+        else if (mode == EPI_STORE) launch_k<TT, EPI_STORE, true, 0, true>(m, a, e);
+        else if (mode == EPI_QKV) launch_k<TT, EPI_QKV, true, 0, true>(m, a, e);
+        else launch_k<TT, EPI_GELU, true, 0, true>(m, a, e);
+        return;
+    }
     if (!packed) {   // raw [N, K] pointers (bass_gemm): plain fp32 store
         if (mode != EPI_STORE || xn) throw Error(BASS_ERR_STATE, "tcgen05 GEMM: fused epilogues need packed weights");
         launch_k<TT, EPI_STORE, false, 0>(m, a, e);
@@ -925,11 +1010,13 @@ static void launch_mode(bass_model& m, int mode, bool packed, bool xn, const Lau
 }  // namespace tc
 
 bool tc_gemm_supported(const bass_model& m, int N, int K) {
+    if (m.dtype == BASS_INT8) return K % 128 == 0 && N >= tc::BN;
     return m.dtype == BASS_BF16 && K % tc::BK == 0 && K >= tc::BK && N >= tc::BN;
 }
 
 void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K, const Epi& e, bool packed,
-             const TcNorm* norm) {
+             const TcNorm* norm, const double* sx, const double* sw) {
+    const bool i8 = sx != nullptr;
     using namespace tc;
     State& S = state(m);
     // token tile: smallest of 16/32/64/128/160/192/256 covering M; beyond
@@ -959,15 +1046,16 @@ void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N
     }
     XNorm xn{};
     if (norm) xn = XNorm{norm->stats, norm->c, norm->e, norm->kmean, norm->stat_tiles};   // X = bf16(x * g) (caller)
-    auto xkey = std::make_tuple(X, M, K, TT);
+    auto xkey = std::make_tuple(X, M, i8 ? -K : K, TT);
     auto xit = S.xmaps.find(xkey);
-    if (xit == S.xmaps.end()) xit = S.xmaps.emplace(xkey, make_map(X, M, K, TT)).first;
+    if (xit == S.xmaps.end()) xit = S.xmaps.emplace(xkey, make_map(X, M, K, TT, i8)).first;
     const CUtensorMap* xm = &xit->second;
     auto sk = std::make_pair(N, K);
     auto si = S.splits.find(sk);
-    if (si == S.splits.end()) si = S.splits.emplace(sk, choose_splits(m.ctx->sm_count, N, K)).first;
+    // int8: a k block is 128 elements, so the split rule sees K / 2 bf16-equivalent columns
+    if (si == S.splits.end()) si = S.splits.emplace(sk, choose_splits(m.ctx->sm_count, N, i8 ? K / 2 : K)).first;
     // one token group: every weight byte is read once (prefill re-reads it per group from L2)
-    Split sp{si->second, K / BK, nullptr, (packed && M <= TT) ? 1 : 0};
+    Split sp{si->second, i8 ? K / 128 : K / BK, nullptr, (packed && M <= TT) ? 1 : 0, sx, sw};
     // reduction loops and cluster size hold <= 8; every split owns >= 1 k block
     sp.S = std::max(1, std::min(std::min(MAX_S, sp.S), sp.k_iters));
     if (sp.S > 1) {

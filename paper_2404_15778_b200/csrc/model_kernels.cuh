@@ -203,6 +203,7 @@ struct Epi {
     const int32_t* row_slot;
     const int32_t* row_pos;
     int d, dh, H, cap;
+    float* amax;         // W8A8 QKV / GELU epilogues: running max |value| per (row, head) / per row (uint-ordered atomics)
 };
 
 BASS_DEV float gelu_erf(float v) {   // ref:model.py:156-157 (exact erf form)

@@ -9,6 +9,7 @@
 
 #include "runtime.h"
 #include "cluster_sampling.cuh"
+#include "quant.cuh"
 
 using namespace bass;
 
@@ -216,7 +217,7 @@ static void launch_layernorm(bass_model& m, const float* x, const int32_t* gathe
 
 static void launch_layernorm_any(bass_model& m, const float* x, const int32_t* gather, const float* g,
                                  const float* b, int rows, void* out) {
-    if (m.dtype == BASS_BF16) launch_layernorm(m, x, gather, g, b, rows, (__nv_bfloat16*)out);
+    if (m.dtype != BASS_F32) launch_layernorm(m, x, gather, g, b, rows, (__nv_bfloat16*)out);
     else launch_layernorm(m, x, gather, g, b, rows, (float*)out);
 }
 
@@ -229,9 +230,20 @@ static void gemm_simt(bass_model& m, const void* X, const void* W, int M, int N,
 
 // algorithmic bytes of one GEMM launch: weights + activations in + results out
 static double gemm_bytes(const bass_model& m, int mode, int M, int N, int K) {
-    const double es = (double)m.esize;
+    const double es = (double)m.esize, ws = (double)m.wsize;
     double out = mode == EPI_STORE ? 4.0 * M * N : mode == EPI_RESID ? 8.0 * M * N : es * M * N;
-    return es * N * K + es * M * K + out;
+    return ws * N * K + (m.int8() ? 1.0 : es) * M * K + out;
+}
+
+// W8A8 projection (BASS_INT8 models): int8 X [M, K] with per-token scales sx,
+// packed int8 W with per-channel scales sw, on the tcgen05 kind::i8 GEMM
+// (ref:model.py:160-164 `_linear` with a QuantTensor, quant.py:98-123)
+static void gemm_i8(bass_model& m, int mode, const int8_t* X, const double* sx, const void* W, const double* sw,
+                    int M, int N, int K, const Epi& e) {
+    if (M == 0) return;
+    ProfScope prof(m.ctx, BASS_PROF_GEMM, gemm_bytes(m, mode, M, N, K), 2.0 * M * N * K);
+    BASS_REQUIRE(tc_gemm_supported(m, N, K), "int8 GEMM needs K % 128 == 0 and N >= 128");
+    tc_gemm(m, mode, X, W, M, N, K, e, true, nullptr, sx, sw);
 }
 
 // c[n] = sum_k g[k] W[n, k], e[n] = sum_k b[k] W[n, k] (W packed bf16): the
@@ -300,6 +312,7 @@ void gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, i
           const TcNorm* norm) {
     if (M == 0) return;
     ProfScope prof(m.ctx, BASS_PROF_GEMM, gemm_bytes(m, mode, M, N, K), 2.0 * M * N * K);
+    if (m.int8()) throw Error(BASS_ERR_STATE, "int8 models project through gemm_i8");
     const bool tc = m.dtype == BASS_BF16 && m.gemm_mode != BASS_GEMM_SIMT && tc_gemm_supported(m, N, K);
     if (m.gemm_mode == BASS_GEMM_TC && !tc)
         throw Error(BASS_ERR_STATE, "tcgen05 GEMM requested but unsupported for this shape/dtype");
@@ -452,7 +465,7 @@ static void append_meta(const Batch& b, std::vector<int32_t>& hm) {
 
 // the forward's attention runs the stream kernel (its work list can be pre-staged)
 static bool uses_stream_attention(const bass_model& m) {
-    return m.dtype == BASS_BF16 && tc_attention_supported(BASS_BF16, m.g.d_head);
+    return m.dtype != BASS_F32 && tc_attention_supported(BASS_BF16, m.g.d_head);
 }
 
 PreMetaOff forward_premeta(const bass_model& m, const Batch& b, int strategy, const std::vector<int32_t>& safe,
@@ -498,14 +511,15 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
     void* h = m.h.need((size_t)M * d * es, st);
     void* q = m.q.need((size_t)M * d * es, st);
     void* cx = m.ctxb.need((size_t)M * d * es, st);
-    void* f = m.f.need((size_t)M * 4 * d * es, st);
+    // int8 models: fp32 [M, 3d] QKV output / [M, 4d] FC pre-activation
+    void* f = m.f.need((size_t)M * 4 * d * (m.int8() ? 4 : es), st);
     DevBuf& work_buf = m.attn_work;
 
     // tcgen05 attention: one plan (work list, Q map) for all layers of this forward
     AttnPlan plan;
     double attn_bytes = 0.0, attn_flops = 0.0;
     float *pa_o = nullptr, *pa_ml = nullptr;
-    if (m.dtype == BASS_BF16 && tc_attention_supported(BASS_BF16, dh)) {
+    if (uses_stream_attention(m)) {
         stream_attention_plan(ctx, strategy, q, M, kv.n_slots, b.slot, b.qn, b.off, H, dh, kv.cap, work_buf, plan,
                               pre ? pre->work : nullptr);
         pa_o = (float*)m.part_o.need((size_t)M * H * plan.mc * dh * 4, st);
@@ -533,7 +547,8 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
                 check_launch(ctx);
             }
         } else {
-            launch_attention(ctx, m.dtype, dh, strategy, q, kc, vc, seqs, b.qn, b.off, rows.pos, M, H, kv.cap,
+            launch_attention(ctx, m.dtype == BASS_F32 ? BASS_F32 : BASS_BF16, dh, strategy, q, kc, vc, seqs, b.qn,
+                             b.off, rows.pos, M, H, kv.cap,
                              kv.n_slots, work_buf, m.part_o, m.part_ml, cx);
         }
         (void)li;
@@ -557,6 +572,75 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
     Epi so{};
     so.out = logits_out;
     void* hs = R > 0 ? m.hs.need((size_t)R * d * es, st) : nullptr;
+
+    if (m.int8()) {
+        // W8A8 forward (ref:model.py:211-246 with `quantized`): every linear
+        // layer takes a per-token int8 input (its LayerNorm / GELU / the
+        // attention context quantized by one row kernel) and dequantizes in the
+        // GEMM epilogue; q / k / v are fake-quantized per (token, head) on
+        // their way to the attention and the cache.
+        const int RM = std::max(M, R);
+        int8_t* xq = (int8_t*)m.xq.need((size_t)RM * 4 * d, st);
+        // per-token scales [RM] | QKV amax [RM][3H] | FC amax [RM]
+        double* xs = (double*)m.xs.need((size_t)RM * (8 + 4 * 3 * H + 4), st);
+        float* amax_qkv = (float*)(xs + RM);
+        float* amax_fc = amax_qkv + (size_t)RM * 3 * H;
+        float* f32 = (float*)f;
+        BASS_CUDA(launch_pdl(embed_kernel<__nv_bfloat16>, dim3(M), dim3(256), 0, st,
+                             (const __nv_bfloat16*)m.tok_emb, (const __nv_bfloat16*)m.pos_emb, rows, proposals,
+                             pstride, d, x, (float*)nullptr, (float*)nullptr, (__nv_bfloat16*)nullptr,
+                             (const float*)nullptr));
+        check_launch(ctx);
+        auto ln_q = [&](const float* g_, const float* b_, const int32_t* gather, int nrows) {
+            ProfScope prof(ctx, BASS_PROF_NORM, (double)nrows * d * 5.0);
+            BASS_CUDA(launch_pdl(ln_quant_kernel, dim3(nrows), dim3(LN_THREADS), 0, st, (const float*)x, gather, g_,
+                                 b_, d, xq, xs, amax_qkv, 3 * H, amax_fc, ctx->trace(nrows, BASS_TR_NORM)));
+            check_launch(ctx);
+        };
+        Epi eq{};
+        eq.out = f32;
+        eq.amax = amax_qkv;
+        eq.dh = dh;
+        Epi ef{};
+        ef.out = f32;
+        ef.amax = amax_fc;
+        const int qchunks = (4 * d + QR_CHUNK - 1) / QR_CHUNK, cchunks = (d + QR_CHUNK - 1) / QR_CHUNK;
+        for (int li = 0; li < g.n_layer; ++li) {
+            const bass_layer& L = m.layers[li];
+            ln_q(L.ln1_g, L.ln1_b, nullptr, M);
+            gemm_i8(m, EPI_QKV, xq, xs, L.wqkv, L.sqkv, M, 3 * d, d, eq);
+            {
+                ProfScope prof(ctx, BASS_PROF_NORM, (double)M * 3 * d * 6.0);
+                BASS_CUDA(launch_pdl(qkv_quant_kernel, dim3(M, (3 * H + 7) / 8), dim3(256), 0, st, (const float*)f32,
+                                     (const float*)amax_qkv, rows, H, dh, kv.cap, (__nv_bfloat16*)q,
+                                     (__nv_bfloat16*)kc_of(li), (__nv_bfloat16*)vc_of(li),
+                                     ctx->trace(M * ((3 * H + 7) / 8), BASS_TR_NORM)));
+                check_launch(ctx);
+            }
+            run_attention(li, kc_of(li), vc_of(li));
+            {
+                ProfScope prof(ctx, BASS_PROF_NORM, (double)M * d * 3.0);
+                BASS_CUDA(launch_pdl(quant_ctx_kernel, dim3(M, cchunks), dim3(256), 0, st, (const __nv_bfloat16*)cx,
+                                     d, xq, xs, ctx->trace(M * cchunks, BASS_TR_NORM)));
+                check_launch(ctx);
+            }
+            gemm_i8(m, EPI_RESID, xq, xs, L.wo, L.so, M, d, d, r);
+            ln_q(L.ln2_g, L.ln2_b, nullptr, M);
+            gemm_i8(m, EPI_GELU, xq, xs, L.wfc, L.sfc, M, 4 * d, d, ef);
+            {
+                ProfScope prof(ctx, BASS_PROF_NORM, (double)M * 4 * d * 5.0);
+                BASS_CUDA(launch_pdl(quant_amax_rows_kernel, dim3(M, qchunks), dim3(256), 0, st, (const float*)f32,
+                                     4 * d, (const float*)amax_fc, xq, xs, ctx->trace(M * qchunks, BASS_TR_NORM)));
+                check_launch(ctx);
+            }
+            gemm_i8(m, EPI_RESID, xq, xs, L.wproj, L.sproj, M, d, 4 * d, r);
+        }
+        if (R > 0) {
+            ln_q(m.lnf_g, m.lnf_b, lrows, R);
+            gemm_i8(m, EPI_STORE, xq, xs, m.head, m.shead, R, V, d, so);
+        }
+        return;
+    }
 
     // LayerNorms folded into the QKV / FC GEMMs (bf16 tcgen05 path):
     //   LN(x) W^T = rstd * (((x - K) * g) W^T - (mean - K) * c) + e,  c = W g, e = W b,
@@ -772,7 +856,10 @@ int bass_model_create(bass_ctx* c, const bass_geometry* g, int dtype, bass_model
         BASS_REQUIRE(g->d_model == g->n_head * g->d_head, "geometry: d_model != n_head * d_head");
         BASS_REQUIRE(g->d_model % 4 == 0 && g->d_model <= 4 * LN_THREADS * LN_NV,
                      "d_model must be a multiple of 4 and <= 8192");
-        BASS_REQUIRE(dtype == BASS_BF16 || dtype == BASS_F32, "dtype must be BASS_BF16 or BASS_F32");
+        BASS_REQUIRE(dtype == BASS_BF16 || dtype == BASS_F32 || dtype == BASS_INT8,
+                     "dtype must be BASS_BF16, BASS_F32 or BASS_INT8");
+        BASS_REQUIRE(dtype != BASS_INT8 || (g->d_model % 128 == 0 && g->vocab_size >= 128),
+                     "INT8 models need d_model % 128 == 0 and vocab_size >= 128 (tcgen05 kind::i8 tiles)");
         BASS_REQUIRE(g->d_head == 16 || g->d_head == 32 || g->d_head == 64 || g->d_head == 128,
                      "d_head must be 16, 32, 64 or 128");
         BASS_CUDA(cudaSetDevice(c->device));
@@ -780,35 +867,45 @@ int bass_model_create(bass_ctx* c, const bass_geometry* g, int dtype, bass_model
         m->ctx = c;
         m->g = *g;
         m->dtype = dtype;
-        m->esize = dtype == BASS_BF16 ? 2 : 4;
+        m->esize = dtype == BASS_F32 ? 4 : 2;
+        m->wsize = dtype == BASS_INT8 ? 1 : m->esize;
         const int64_t d = g->d_model, V = g->vocab_size, S = g->max_seq_len, L = g->n_layer;
-        // bf16 GEMM weights live in the packed tile layout (rows padded to 128)
-        m->packed = dtype == BASS_BF16 && d % 64 == 0;
+        // bf16 / int8 GEMM weights live in the packed tile layout (rows padded to 128)
+        m->packed = (dtype == BASS_BF16 && d % 64 == 0) || dtype == BASS_INT8;
         auto rows = [&](int64_t N) { return m->packed ? packed_rows(N) : N; };
         const int64_t per_layer = (rows(3 * d) + rows(d) + rows(4 * d)) * d + rows(d) * 4 * d;
-        const int64_t total = V * d + S * d + L * per_layer + rows(V) * d;
-        m->weight_bytes = total * m->esize;
+        const int64_t emb = V * d + S * d, mats = L * per_layer + rows(V) * d;
+        m->weight_bytes = emb * (int64_t)m->esize + mats * (int64_t)m->wsize;
         BASS_CUDA(cudaMalloc(&m->wblob, (size_t)m->weight_bytes));
         const int64_t nf = L * 4 * d + 2 * d;
         BASS_CUDA(cudaMalloc((void**)&m->fblob, (size_t)nf * 4));
+        if (dtype == BASS_INT8) BASS_CUDA(cudaMalloc((void**)&m->sblob, (size_t)(L * 9 * d + V) * 8));
         char* p = (char*)m->wblob;
         auto take = [&](int64_t n) { void* r = p; p += n * m->esize; return r; };
+        auto take_w = [&](int64_t n) { void* r = p; p += n * m->wsize; return r; };
         m->tok_emb = take(V * d);
         m->pos_emb = take(S * d);
         float* fp = m->fblob;
+        double* sp = m->sblob;
+        auto take_s = [&](int64_t n) { double* r = sp; if (sp) sp += n; return r; };
         m->layers.resize(L);
         for (int i = 0; i < L; ++i) {
             bass_layer& ly = m->layers[i];
-            ly.wqkv = take(rows(3 * d) * d);
-            ly.wo = take(rows(d) * d);
-            ly.wfc = take(rows(4 * d) * d);
-            ly.wproj = take(rows(d) * 4 * d);
+            ly.wqkv = take_w(rows(3 * d) * d);
+            ly.wo = take_w(rows(d) * d);
+            ly.wfc = take_w(rows(4 * d) * d);
+            ly.wproj = take_w(rows(d) * 4 * d);
             ly.ln1_g = fp; fp += d;
             ly.ln1_b = fp; fp += d;
             ly.ln2_g = fp; fp += d;
             ly.ln2_b = fp; fp += d;
+            ly.sqkv = take_s(3 * d);
+            ly.so = take_s(d);
+            ly.sfc = take_s(4 * d);
+            ly.sproj = take_s(d);
         }
-        m->head = take(rows(V) * d);
+        m->head = take_w(rows(V) * d);
+        m->shead = take_s(V);
         m->lnf_g = fp; fp += d;
         m->lnf_b = fp; fp += d;
         // LN defaults (gain 1, bias 0) — ref:model.py:121-130
@@ -833,8 +930,9 @@ int bass_model_destroy(bass_model* m) {
     tc_release(*m);
     cudaFree(m->wblob);
     cudaFree(m->fblob);
+    if (m->sblob) cudaFree(m->sblob);
     for (DevBuf* b : {&m->x, &m->h, &m->q, &m->ctxb, &m->f, &m->hs, &m->meta, &m->part_o, &m->part_ml,
-                      &m->logits_tmp, &m->lnstats, &m->lnfold, &m->attn_work})
+                      &m->logits_tmp, &m->lnstats, &m->lnfold, &m->attn_work, &m->xq, &m->xs})
         b->release();
     delete m;
     return BASS_OK;
@@ -856,10 +954,22 @@ int bass_model_set_weight(bass_model* m, int tensor, int layer, const float* hos
             BASS_CUDA(cudaMemcpyAsync(tmp, host, count * 4, cudaMemcpyHostToDevice, st));
             return tmp;
         };
-        auto put_matrix = [&](int64_t K, int64_t N, void* dst, int64_t row_off) {
+        auto put_matrix = [&](int64_t K, int64_t N, void* dst, int64_t row_off, double* scale = nullptr) {
             // reference [K, N] -> device output-major rows [row_off + n][K]
             float* tmp = upload_tmp(K * N);
             dim3 grid((N + 31) / 32, (K + 31) / 32), blk(32, 8);
+            if (m->int8()) {
+                // fp32 [N, K], then per-output-channel int8 quantization into the
+                // packed layout (ref:model.py:135-143 prepare_quantized)
+                float* t2;
+                BASS_CUDA(cudaMallocAsync((void**)&t2, K * N * 4, st));
+                transpose_convert<<<grid, blk, 0, st>>>(tmp, (int)K, (int)N, t2, K, 0, false);
+                quant_weight_rows_kernel<<<(unsigned)N, 256, 0, st>>>(t2, (int)K, (int8_t*)dst, row_off, scale);
+                BASS_CUDA(cudaGetLastError());
+                BASS_CUDA(cudaFreeAsync(t2, st));
+                BASS_CUDA(cudaFreeAsync(tmp, st));
+                return;
+            }
             if (m->dtype == BASS_BF16)
                 transpose_convert<<<grid, blk, 0, st>>>(tmp, (int)K, (int)N, (__nv_bfloat16*)dst, K, row_off,
                                                         m->packed);
@@ -870,7 +980,7 @@ int bass_model_set_weight(bass_model* m, int tensor, int layer, const float* hos
         };
         auto put_rows = [&](int64_t count, void* dst) {
             float* tmp = upload_tmp(count);
-            if (m->dtype == BASS_BF16) convert_copy<<<256, 256, 0, st>>>(tmp, count, (__nv_bfloat16*)dst);
+            if (m->dtype != BASS_F32) convert_copy<<<256, 256, 0, st>>>(tmp, count, (__nv_bfloat16*)dst);
             else convert_copy<<<256, 256, 0, st>>>(tmp, count, (float*)dst);
             BASS_CUDA(cudaGetLastError());
             BASS_CUDA(cudaFreeAsync(tmp, st));
@@ -889,15 +999,15 @@ int bass_model_set_weight(bass_model* m, int tensor, int layer, const float* hos
             case BASS_W_LN1_B: put_f32(m->layers[layer].ln1_b); break;
             case BASS_W_LN2_G: put_f32(m->layers[layer].ln2_g); break;
             case BASS_W_LN2_B: put_f32(m->layers[layer].ln2_b); break;
-            case BASS_W_WQ: put_matrix(d, d, m->layers[layer].wqkv, 0); break;
-            case BASS_W_WK: put_matrix(d, d, m->layers[layer].wqkv, d); break;
-            case BASS_W_WV: put_matrix(d, d, m->layers[layer].wqkv, 2 * d); break;
-            case BASS_W_WO: put_matrix(d, d, m->layers[layer].wo, 0); break;
-            case BASS_W_FC: put_matrix(d, 4 * d, m->layers[layer].wfc, 0); break;
-            case BASS_W_PROJ: put_matrix(4 * d, d, m->layers[layer].wproj, 0); break;
+            case BASS_W_WQ: put_matrix(d, d, m->layers[layer].wqkv, 0, m->layers[layer].sqkv); break;
+            case BASS_W_WK: put_matrix(d, d, m->layers[layer].wqkv, d, m->layers[layer].sqkv); break;
+            case BASS_W_WV: put_matrix(d, d, m->layers[layer].wqkv, 2 * d, m->layers[layer].sqkv); break;
+            case BASS_W_WO: put_matrix(d, d, m->layers[layer].wo, 0, m->layers[layer].so); break;
+            case BASS_W_FC: put_matrix(d, 4 * d, m->layers[layer].wfc, 0, m->layers[layer].sfc); break;
+            case BASS_W_PROJ: put_matrix(4 * d, d, m->layers[layer].wproj, 0, m->layers[layer].sproj); break;
             case BASS_W_LNF_G: put_f32(m->lnf_g); break;
             case BASS_W_LNF_B: put_f32(m->lnf_b); break;
-            case BASS_W_HEAD: put_matrix(d, V, m->head, 0); break;
+            case BASS_W_HEAD: put_matrix(d, V, m->head, 0, m->shead); break;
         }
         BASS_CUDA(cudaStreamSynchronize(st));
     });
@@ -914,11 +1024,14 @@ int bass_model_get_weight(const bass_model* mc, int tensor, int layer, float* ho
         BASS_REQUIRE(!per_layer || (layer >= 0 && layer < g.n_layer), "layer index out of range");
         cudaStream_t st = m->ctx->stream;
         float* tmp = nullptr;
-        auto get_matrix = [&](int64_t K, int64_t N, const void* src, int64_t row_off) {
+        auto get_matrix = [&](int64_t K, int64_t N, const void* src, int64_t row_off, const double* scale = nullptr) {
             BASS_REQUIRE(n == K * N, "geometry: element count does not match the tensor");
             BASS_CUDA(cudaMallocAsync((void**)&tmp, K * N * 4, st));
             dim3 grid((N + 31) / 32, (K + 31) / 32), blk(32, 8);
-            if (m->dtype == BASS_BF16)
+            if (m->int8())   // dequantized values payload * scale (ref:quant.py:86-95)
+                dequant_gather_kernel<<<1184, 256, 0, st>>>((const int8_t*)src, scale, (int)K, (int)N, row_off, tmp,
+                                                            nullptr);
+            else if (m->dtype == BASS_BF16)
                 transpose_gather<<<grid, blk, 0, st>>>((const __nv_bfloat16*)src, (int)K, (int)N, tmp, K, row_off,
                                                        m->packed);
             else
@@ -927,7 +1040,7 @@ int bass_model_get_weight(const bass_model* mc, int tensor, int layer, float* ho
         auto get_rows = [&](int64_t count, const void* src) {
             BASS_REQUIRE(n == count, "geometry: element count does not match the tensor");
             BASS_CUDA(cudaMallocAsync((void**)&tmp, count * 4, st));
-            if (m->dtype == BASS_BF16) to_f32<<<256, 256, 0, st>>>((const __nv_bfloat16*)src, count, tmp);
+            if (m->dtype != BASS_F32) to_f32<<<256, 256, 0, st>>>((const __nv_bfloat16*)src, count, tmp);
             else to_f32<<<256, 256, 0, st>>>((const float*)src, count, tmp);
         };
         auto get_f32 = [&](const float* src) {
@@ -942,15 +1055,15 @@ int bass_model_get_weight(const bass_model* mc, int tensor, int layer, float* ho
             case BASS_W_LN1_B: get_f32(L->ln1_b); break;
             case BASS_W_LN2_G: get_f32(L->ln2_g); break;
             case BASS_W_LN2_B: get_f32(L->ln2_b); break;
-            case BASS_W_WQ: get_matrix(d, d, L->wqkv, 0); break;
-            case BASS_W_WK: get_matrix(d, d, L->wqkv, d); break;
-            case BASS_W_WV: get_matrix(d, d, L->wqkv, 2 * d); break;
-            case BASS_W_WO: get_matrix(d, d, L->wo, 0); break;
-            case BASS_W_FC: get_matrix(d, 4 * d, L->wfc, 0); break;
-            case BASS_W_PROJ: get_matrix(4 * d, d, L->wproj, 0); break;
+            case BASS_W_WQ: get_matrix(d, d, L->wqkv, 0, L->sqkv); break;
+            case BASS_W_WK: get_matrix(d, d, L->wqkv, d, L->sqkv); break;
+            case BASS_W_WV: get_matrix(d, d, L->wqkv, 2 * d, L->sqkv); break;
+            case BASS_W_WO: get_matrix(d, d, L->wo, 0, L->so); break;
+            case BASS_W_FC: get_matrix(d, 4 * d, L->wfc, 0, L->sfc); break;
+            case BASS_W_PROJ: get_matrix(4 * d, d, L->wproj, 0, L->sproj); break;
             case BASS_W_LNF_G: get_f32(m->lnf_g); break;
             case BASS_W_LNF_B: get_f32(m->lnf_b); break;
-            case BASS_W_HEAD: get_matrix(d, V, m->head, 0); break;
+            case BASS_W_HEAD: get_matrix(d, V, m->head, 0, m->shead); break;
         }
         BASS_CUDA(cudaGetLastError());
         if (tmp) {
@@ -961,9 +1074,71 @@ int bass_model_get_weight(const bass_model* mc, int tensor, int layer, float* ho
     });
 }
 
+// one (layer, matrix) of an int8 model: where its packed rows and scales live
+struct QMat {
+    const int8_t* w;
+    const double* s;
+    int64_t K, N, row_off;
+};
+static QMat qmat(const bass_model* m, int tensor, int layer) {
+    const int64_t d = m->g.d_model;
+    if (tensor == BASS_W_HEAD) return {(const int8_t*)m->head, m->shead, d, m->g.vocab_size, 0};
+    const bass_layer& L = m->layers[layer];
+    switch (tensor) {
+        case BASS_W_WQ: return {(const int8_t*)L.wqkv, L.sqkv, d, d, 0};
+        case BASS_W_WK: return {(const int8_t*)L.wqkv, L.sqkv, d, d, d};
+        case BASS_W_WV: return {(const int8_t*)L.wqkv, L.sqkv, d, d, 2 * d};
+        case BASS_W_WO: return {(const int8_t*)L.wo, L.so, d, d, 0};
+        case BASS_W_FC: return {(const int8_t*)L.wfc, L.sfc, d, 4 * d, 0};
+        case BASS_W_PROJ: return {(const int8_t*)L.wproj, L.sproj, 4 * d, d, 0};
+        default: throw Error(BASS_ERR_VALUE, "tensor is not a quantized matrix");
+    }
+}
+
+int bass_model_get_qweight(const bass_model* mc, int tensor, int layer, int8_t* payload, double* scales, int64_t n) {
+    bass_model* m = const_cast<bass_model*>(mc);
+    return guarded(m->ctx, [&] {
+        BASS_REQUIRE(m->int8(), "not an INT8 model");
+        BASS_REQUIRE(tensor == BASS_W_HEAD || (layer >= 0 && layer < m->g.n_layer), "layer index out of range");
+        const QMat q = qmat(m, tensor, layer);
+        BASS_REQUIRE(n == q.K * q.N, "geometry: element count does not match the tensor");
+        cudaStream_t st = m->ctx->stream;
+        int8_t* tmp;
+        BASS_CUDA(cudaMallocAsync((void**)&tmp, n, st));
+        dequant_gather_kernel<<<1184, 256, 0, st>>>(q.w, q.s, (int)q.K, (int)q.N, q.row_off, nullptr, tmp);
+        BASS_CUDA(cudaGetLastError());
+        BASS_CUDA(cudaMemcpyAsync(payload, tmp, n, cudaMemcpyDeviceToHost, st));
+        BASS_CUDA(cudaMemcpyAsync(scales, q.s + q.row_off, q.N * 8, cudaMemcpyDeviceToHost, st));
+        BASS_CUDA(cudaFreeAsync(tmp, st));
+        BASS_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
 int bass_model_init_random(bass_model* m, uint64_t seed, float std) {
     return guarded(m->ctx, [&] {
         m->lnfold_valid = false;
+        if (m->int8()) {
+            // bf16 embeddings; every matrix drawn in fp32 [N, K] and quantized per channel
+            cudaStream_t st = m->ctx->stream;
+            const int64_t d = m->g.d_model, V = m->g.vocab_size, S = m->g.max_seq_len;
+            random_normal<<<m->ctx->sm_count * 8, 256, 0, st>>>((__nv_bfloat16*)m->wblob, (V + S) * d, seed, std);
+            float* t;
+            BASS_CUDA(cudaMallocAsync((void**)&t, (size_t)std::max(V, 4 * d) * d * 4, st));
+            uint64_t sub = 0;
+            auto one = [&](const QMat& q) {
+                random_normal<<<m->ctx->sm_count * 8, 256, 0, st>>>(t, q.K * q.N, seed * 0x9E3779B97F4A7C15ull + ++sub, std);
+                quant_weight_rows_kernel<<<(unsigned)q.N, 256, 0, st>>>(t, (int)q.K, const_cast<int8_t*>(q.w),
+                                                                         q.row_off, const_cast<double*>(q.s));
+            };
+            for (int l = 0; l < m->g.n_layer; ++l)
+                for (int tid : {BASS_W_WQ, BASS_W_WK, BASS_W_WV, BASS_W_WO, BASS_W_FC, BASS_W_PROJ})
+                    one(qmat(m, tid, l));
+            one(qmat(m, BASS_W_HEAD, 0));
+            BASS_CUDA(cudaGetLastError());
+            BASS_CUDA(cudaFreeAsync(t, st));
+            BASS_CUDA(cudaStreamSynchronize(st));
+            return;
+        }
         const int64_t n = m->weight_bytes / (int64_t)m->esize;
         if (m->dtype == BASS_BF16)
             random_normal<<<m->ctx->sm_count * 8, 256, 0, m->ctx->stream>>>((__nv_bfloat16*)m->wblob, n, seed, std);
@@ -1110,6 +1285,53 @@ int bass_gemm_bench(bass_model* m, int mode, int M, int N, int K, const void* x,
         cudaEventDestroy(a);
         cudaEventDestroy(b);
         if (wp) cudaFree(wp);
+    });
+}
+
+int bass_int_gemm_dequant(bass_ctx* c, int M, int N, int K, const int8_t* a, const double* sa, const int8_t* w,
+                          const double* sw, float* out) {
+    return guarded(c, [&] {
+        BASS_REQUIRE(M >= 1 && N >= 1 && K >= 1, "geometry: GEMM sizes must be positive");
+        BASS_REQUIRE(K % 128 == 0 && N >= 128, "int8 GEMM needs K % 128 == 0 and N >= 128");
+        cudaStream_t st = c->stream;
+        bass_model tmp;   // a weightless int8 'model': only the GEMM state (tensor maps, split rule)
+        tmp.ctx = c;
+        tmp.dtype = BASS_INT8;
+        tmp.esize = 2;
+        tmp.wsize = 1;
+        tmp.packed = true;
+        struct Bufs {
+            bass_model* m;
+            std::vector<void*> p;
+            ~Bufs() {
+                for (void* q : p) cudaFree(q);
+                tc_release(*m);
+            }
+        } bufs{&tmp, {}};
+        auto dalloc = [&](size_t n) {
+            void* q = nullptr;
+            BASS_CUDA(cudaMalloc(&q, n));
+            bufs.p.push_back(q);
+            return q;
+        };
+        int8_t* ad = (int8_t*)dalloc((size_t)M * K);
+        double* sad = (double*)dalloc((size_t)M * 8);
+        int8_t* wr = (int8_t*)dalloc((size_t)K * N);
+        int8_t* wp = (int8_t*)dalloc((size_t)packed_rows(N) * K);
+        double* swd = (double*)dalloc((size_t)N * 8);
+        float* od = (float*)dalloc((size_t)M * N * 4);
+        BASS_CUDA(cudaMemcpyAsync(ad, a, (size_t)M * K, cudaMemcpyHostToDevice, st));
+        BASS_CUDA(cudaMemcpyAsync(sad, sa, (size_t)M * 8, cudaMemcpyHostToDevice, st));
+        BASS_CUDA(cudaMemcpyAsync(wr, w, (size_t)K * N, cudaMemcpyHostToDevice, st));
+        BASS_CUDA(cudaMemcpyAsync(swd, sw, (size_t)N * 8, cudaMemcpyHostToDevice, st));
+        BASS_CUDA(cudaMemsetAsync(wp, 0, (size_t)packed_rows(N) * K, st));
+        pack_i8_ref_kernel<<<1184, 256, 0, st>>>(wr, K, N, wp);
+        BASS_CUDA(cudaGetLastError());
+        Epi e{};
+        e.out = od;
+        gemm_i8(tmp, EPI_STORE, ad, sad, wp, swd, M, N, K, e);
+        BASS_CUDA(cudaMemcpyAsync(out, od, (size_t)M * N * 4, cudaMemcpyDeviceToHost, st));
+        BASS_CUDA(cudaStreamSynchronize(st));
     });
 }
 

@@ -123,6 +123,7 @@ struct ProfScope {
 struct bass_layer {
     float *ln1_g, *ln1_b, *ln2_g, *ln2_b;
     void *wqkv, *wo, *wfc, *wproj;   // output-major [N, K]
+    double *sqkv, *so, *sfc, *sproj; // BASS_INT8: per-output-channel weight scales
 };
 
 struct bass_model {
@@ -131,7 +132,11 @@ struct bass_model {
     int dtype = BASS_BF16;
     int gemm_mode = BASS_GEMM_AUTO;
     bool packed = false;             // GEMM weights in the packed tile layout (bf16, d % 64 == 0)
-    size_t esize = 2;
+    size_t esize = 2;                // activation / embedding / KV element size (int8 models: bf16)
+    size_t wsize = 2;                // GEMM weight element size (int8 models: 1)
+    double* sblob = nullptr;         // BASS_INT8: all per-channel weight scales
+    double* shead = nullptr;
+    bool int8() const { return dtype == BASS_INT8; }
     void* wblob = nullptr;           // all matrices, one allocation
     float* fblob = nullptr;          // LN params
     int64_t weight_bytes = 0;
@@ -145,6 +150,7 @@ struct bass_model {
     bool lnfold_valid = false;       // recomputed after any weight / LN parameter change
     void* tc_state = nullptr;        // tcgen05 split-K GEMM descriptors (gemm_tc.cu)
     bass::DevBuf attn_work;          // stream-attention work list of the current forward
+    bass::DevBuf xq, xs;             // BASS_INT8: per-token int8 GEMM input and its scales
 };
 
 struct bass_kv {
@@ -216,8 +222,10 @@ struct TcNorm {
     float* kmean;      // row means (see forward()), updated by the consumer
     int stat_tiles;
 };
+// sx / sw (W8A8 models): per-token / per-channel scales; X, W int8 (W packed)
 void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N, int K,
-             const Epi& e, bool packed, const TcNorm* norm = nullptr);
+             const Epi& e, bool packed, const TcNorm* norm = nullptr, const double* sx = nullptr,
+             const double* sw = nullptr);
 void tc_release(bass_model& m);
 // per-model split-count override for one (N, K) projection shape (0: the default rule)
 void tc_set_split(bass_model& m, int N, int K, int splits);

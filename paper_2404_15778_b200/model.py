@@ -132,6 +132,8 @@ def _dtype_code(dtype) -> int:
         return L.BF16
     if dtype in ("fp32", "float32", L.F32):
         return L.F32
+    if dtype in ("int8", "w8a8", L.INT8):
+        return L.INT8
     raise ValueError(f"unknown dtype {dtype!r}")
 
 
@@ -255,6 +257,16 @@ class DeviceWeights:
         self.ctx.check(self.ctx.lib.bass_gemm(self.handle, mode, M, N, K, C.c_void_p(x.data_ptr()),
                                               C.c_void_p(w.data_ptr()), C.c_void_p(y.data_ptr())))
         return y
+
+    def qweight(self, tensor: int, layer: int = 0):
+        """INT8 models: (payload [in, out] int8, scales [out] fp64) of one matrix
+        as quantized on the device (ref:model.py:135-143, quant.py:55-63)."""
+        shape = self._SHAPES[tensor](self.config)
+        p = np.empty(shape, dtype=np.int8)
+        s = np.empty(shape[1], dtype=np.float64)
+        self.ctx.check(self.ctx.lib.bass_model_get_qweight(self.handle, tensor, layer, L.ptr(p, C.c_int8),
+                                                           L.ptr(s, C.c_double), p.size))
+        return p, s
 
     def set_split(self, N: int, K: int, splits: int):
         """Split-K count for the (N, K) projection (0: default rule)."""

@@ -104,7 +104,8 @@ def test_run_config_validation():
     with pytest.raises(R.ConfigError):
         tiny_config(main={"n_layer": 2, "bogus": 1}).main_config()
     with pytest.raises(R.ConfigError):
-        tiny_config(quant_enabled=True)
+        tiny_config(quant_enabled=True, dtype="fp32")
+    assert tiny_config(quant_enabled=True).device_dtype == "int8"
 
 
 def test_run_config_file_round_trip_and_prompts(tmp_path):
