@@ -287,6 +287,8 @@ def main():
                          "natural acceptance: an overridden proposal may have zero draft probability")
     ap.add_argument("--strategy", default="ragged", choices=["pad", "split", "ragged"])
     ap.add_argument("--gemm", default="auto", choices=["auto", "simt", "tc"])
+    ap.add_argument("--loop", default="device", choices=["device", "host"],
+                    help="decode-loop driver: one CUDA graph per generation (device) or per-step host planning")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "int8"],
                     help="int8: the W8A8 path (SURVEY 8(f1), ref:quant.py) for main and draft")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -346,6 +348,7 @@ def main():
     draft_m = B.CudaModel(wd, b, args.strategy, capacity=cap)
     eng = B.CudaEngine(main_m, draft_m)
     eng.set_strategy(args.strategy)
+    eng.set_loop(args.loop)
     prompts = [np.random.default_rng(1_000_003 + sid).integers(0, mcfg.vocab_size, P).tolist()
                for sid in sids]
     req = B.GenerationRequest(prompts, new, temperature=cfg["temperature"], top_p=cfg["top_p"],
@@ -407,6 +410,7 @@ def main():
         ev1.record(stream)
         barrier()
         t_host1 = time.perf_counter()
+    loop_info = eng.loop_info()
     launches = ctx.launches - launches0
     h2d1, d2h1 = ctx.transfer_bytes()
     algo1 = ctx.algo_read()
@@ -528,6 +532,7 @@ def main():
                 "h2d_bytes_per_step": (h2d1 - h2d0) // max(args.steps, 1),
                 "d2h_bytes_per_step": (d2h1 - d2h0) // max(args.steps, 1)},
         "gpu_launches": launches,
+        "loop": loop_info,
         "roofline": roofline,
         "attention_roofline": roof("attention", "attn", "attn_stream_kernel (persistent TMA + tcgen05)"),
         "algorithmic_bytes_per_generation": {k: v["bytes"] for k, v in algo.items()},

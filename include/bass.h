@@ -40,6 +40,14 @@ extern "C" {
  * stream, attention and KV cache as in the bf16 path. */
 enum { BASS_BF16 = 0, BASS_F32 = 1, BASS_INT8 = 2 };
 enum { BASS_PAD = 0, BASS_SPLIT = 1, BASS_RAGGED = 2 };  /* ref:attention.py:30-32 (+ragged work list) */
+/* decode-loop driver of bass_spec_generate: DEVICE (default) runs every step
+ * after the first (prompt) step from one CUDA graph — the step planning,
+ * bookkeeping and Algorithm 1 on the GPU, one host synchronisation per
+ * generation; HOST plans each step on the host and reads its outcome back
+ * (one synchronisation per step).  Both give identical results.  DEVICE falls
+ * back to HOST where it does not apply (fp32 models, d_head outside {64, 128},
+ * draft limit > 48, timeline tracing or per-kernel event profiling on). */
+enum { BASS_LOOP_HOST = 0, BASS_LOOP_DEVICE = 1 };
 enum { BASS_GEMM_AUTO = 0, BASS_GEMM_SIMT = 1, BASS_GEMM_TC = 2 };
 enum { BASS_ROLE_DRAFT = 0, BASS_ROLE_VERIFY = 1 };      /* ref:sampling.py:20-22 */
 
@@ -263,6 +271,11 @@ int bass_engine_create(bass_model* main_model, bass_kv* main_kv,
                        bass_engine** out);
 int bass_engine_destroy(bass_engine* e);
 int bass_engine_set_strategy(bass_engine* e, int strategy);
+int bass_engine_set_loop(bass_engine* e, int loop_mode);
+/* how the last bass_spec_generate ran: BASS_LOOP_HOST / DEVICE, its host
+ * synchronisations, and how many times this engine captured a loop graph */
+int bass_engine_loop_info(const bass_engine* e, int32_t* last_mode, int32_t* last_syncs,
+                          int64_t* graph_builds);
 int bass_spec_generate(bass_engine* e, const bass_gen_request* req,
                        bass_gen_result* res);        /* ref:engine.py:200-385 */
 int bass_regular_generate(bass_engine* e, const bass_gen_request* req,

@@ -16,6 +16,7 @@ BASS_OK, BASS_ERR_VALUE, BASS_ERR_CUDA, BASS_ERR_MEMORY, BASS_ERR_STATE = 0, -1,
 BF16, F32, INT8 = 0, 1, 2
 PAD, SPLIT, RAGGED = 0, 1, 2
 GEMM_AUTO, GEMM_SIMT, GEMM_TC = 0, 1, 2
+LOOP_HOST, LOOP_DEVICE = 0, 1
 (W_TOK_EMB, W_POS_EMB, W_LN1_G, W_LN1_B, W_WQ, W_WK, W_WV, W_WO, W_LN2_G, W_LN2_B,
  W_FC, W_PROJ, W_LNF_G, W_LNF_B, W_HEAD) = range(15)
 
@@ -98,6 +99,8 @@ SIGNATURES = {
     "bass_engine_create": (C.c_int, [vp, vp, vp, vp, C.POINTER(vp)]),
     "bass_engine_destroy": (C.c_int, [vp]),
     "bass_engine_set_strategy": (C.c_int, [vp, C.c_int]),
+    "bass_engine_set_loop": (C.c_int, [vp, C.c_int]),
+    "bass_engine_loop_info": (C.c_int, [vp, i32p, i32p, i64p]),
     "bass_spec_generate": (C.c_int, [vp, C.POINTER(GenRequest), C.POINTER(GenResult)]),
     "bass_regular_generate": (C.c_int, [vp, C.POINTER(GenRequest), C.POINTER(GenResult)]),
 }

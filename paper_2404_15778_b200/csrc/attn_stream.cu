@@ -709,6 +709,41 @@ static void launch(bass_ctx* ctx, const AttnPlan& p, const CUtensorMap& tk, cons
 }  // namespace ast
 
 int stream_split_len() { return ast::SPLIT; }
+int stream_chunk_len() { return ast::CH; }
+int stream_split_chunks() { return ast::SPLIT_CH; }
+int stream_nq_for(int q) { return q <= 16 ? 16 : q <= 32 ? 32 : 64; }
+int stream_items_per_seq(int q, int max_len) {
+    const int nq = stream_nq_for(q);
+    const int chunks = (std::max(max_len, 1) + ast::CH - 1) / ast::CH;
+    return ((q + nq - 1) / nq) * ((chunks + ast::SPLIT_CH - 1) / ast::SPLIT_CH);
+}
+
+void stream_attention_plan_dev(bass_ctx* ctx, int strategy, const void* q, int M, int n_slots,
+                               const std::vector<int32_t>& qn, int H, int dh, int cap, const void* work,
+                               int work_stride, int max_len, AttnPlan& plan) {
+    using namespace ast;
+    (void)ctx;
+    const int n_seq = (int)qn.size();
+    int max_qn = 0;
+    for (int v : qn) max_qn = std::max(max_qn, v);
+    const int NQ = stream_nq_for(max_qn);
+    plan.tq = map2d(q, M, (int64_t)H * dh, (int64_t)H * dh, NQ);
+    plan.dh = dh;
+    plan.NQ = NQ;
+    plan.pad_len = 0;
+    plan.max_len = max_len;
+    plan.strategy = strategy;
+    plan.H = H;
+    plan.cap = cap;
+    plan.n_slots = n_slots;
+    plan.mc = (cap + SPLIT - 1) / SPLIT;
+    plan.stream = true;
+    plan.needs_combine = max_len > SPLIT;   // some row may span two splits (single-split rows skip the combine)
+    plan.first.resize(n_seq + 1);
+    for (int i = 0; i <= n_seq; ++i) plan.first[i] = i * work_stride;   // idle items pad each region
+    plan.work = const_cast<void*>(work);
+    plan.valid = true;
+}
 
 bool tc_attention_supported(int dtype, int dh) { return dtype == BASS_BF16 && (dh == 128 || dh == 64); }
 

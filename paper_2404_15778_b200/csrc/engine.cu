@@ -10,11 +10,37 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <cstdio>
+#include <cstdlib>
+
+#include <array>
+#include <numeric>
 
 #include "runtime.h"
 #include "cluster_sampling.cuh"
+#include "loop_graph.cuh"
 
 using namespace bass;
+
+// the captured device-resident decode loop of one request shape (loop_graph.cuh)
+struct LoopGraph {
+    std::vector<double> key;          // every scalar / pointer baked into its kernels
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int lmin = 1, lmax = 1;
+    // per branch (l - lmin): launches and algorithmic {launches, bytes, flops} per
+    // kernel class of one step, recorded while capturing (attention excluded:
+    // its bytes depend on the lengths and are counted from the step trace)
+    std::vector<int64_t> launches;
+    std::vector<std::array<double, 3 * BASS_PROF_N>> algo;
+    void reset() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        exec = nullptr;
+        graph = nullptr;
+        key.clear();
+    }
+};
 
 struct bass_engine {
     bass_ctx* ctx = nullptr;          // kept so destroy never touches a freed model
@@ -31,6 +57,14 @@ struct bass_engine {
     char* step_host = nullptr;        // pinned: per-step slot records (slot_rec_bytes)
     size_t step_host_cap = 0;
     int32_t* props() { return (int32_t*)proposals.p; }
+    // device-resident loop (BASS_LOOP_DEVICE): state, plan arena, the graph
+    int loop_mode = BASS_LOOP_DEVICE;
+    DevBuf loopbuf, looparena;
+    LoopGraph lg;
+    int64_t graph_builds = 0;
+    int last_mode = BASS_LOOP_HOST, last_syncs = 0;
+    char* loop_host = nullptr;        // pinned read-back of the device loop state
+    size_t loop_host_cap = 0;
 };
 
 namespace {
@@ -145,7 +179,9 @@ int bass_engine_destroy(bass_engine* e) {
     if (!e) return BASS_OK;
     cudaStreamSynchronize(e->ctx->stream);
     if (e->step_host) cudaFreeHost(e->step_host);
-    for (DevBuf* b : {&e->proposals, &e->vlog, &e->dlog, &e->vamax, &e->vlse, &e->accf, &e->corr, &e->bonus, &e->scratch,
+    e->lg.reset();
+    if (e->loop_host) cudaFreeHost(e->loop_host);
+    for (DevBuf* b : {&e->loopbuf, &e->looparena, &e->proposals, &e->vlog, &e->dlog, &e->vamax, &e->vlse, &e->accf, &e->corr, &e->bonus, &e->scratch,
                       &e->slotbuf, &e->stepbuf, &e->align_tok, &e->arena, &e->pick, &e->shaped})
         b->release();
     delete e;
@@ -157,6 +193,21 @@ int bass_engine_set_strategy(bass_engine* e, int strategy) {
         BASS_REQUIRE(strategy >= BASS_PAD && strategy <= BASS_RAGGED, "unknown strategy");
         e->strategy = strategy;
     });
+}
+
+int bass_engine_set_loop(bass_engine* e, int mode) {
+    return guarded_e(e, [&] {
+        BASS_REQUIRE(mode == BASS_LOOP_HOST || mode == BASS_LOOP_DEVICE, "unknown loop mode");
+        e->loop_mode = mode;
+    });
+}
+
+int bass_engine_loop_info(const bass_engine* e, int32_t* last_mode, int32_t* last_syncs, int64_t* graph_builds) {
+    if (!e) return BASS_ERR_STATE;
+    if (last_mode) *last_mode = e->last_mode;
+    if (last_syncs) *last_syncs = e->last_syncs;
+    if (graph_builds) *graph_builds = e->graph_builds;
+    return BASS_OK;
 }
 
 // ------------------------------------------------------------------ spec
@@ -266,10 +317,370 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
         int* pick_cnt = pick_i + (size_t)b * GREEDY_PARTS;
         BASS_CUDA(cudaMemsetAsync(pick_cnt, 0, (size_t)b * 4, st));
 
+        // ------------------------------------------------------------------
+        // device-resident loop (loop_graph.cuh): the prompt step is planned on
+        // the host and enqueued as usual, its outcome booked on the device, and
+        // every later step runs from one CUDA graph; one synchronisation per
+        // generation
+        const bool use_graph = e->loop_mode == BASS_LOOP_DEVICE && model_uses_stream_attention(M) &&
+                               model_uses_stream_attention(D) && !c->profile && !c->trace_buf &&
+                               limit <= GL_MAXL && b <= 1024;
+        e->last_mode = use_graph ? BASS_LOOP_DEVICE : BASS_LOOP_HOST;
+        e->last_syncs = 0;
+        const int g_lmin = ctl.fixed ? ctl.fixed : 1, g_lmax = ctl.fixed ? ctl.fixed : limit;
+        const int g_nbr = g_lmax - g_lmin + 1;
+        const int com_cap = e->cap, steps_cap = maxnew + 2;
+        // DevLoop + arrays in one device buffer (offsets)
+        auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+        size_t o_end = al(sizeof(DevLoop));
+        auto lay = [&](size_t n) { const size_t r0 = o_end; o_end += al(n); return r0; };
+        const size_t o_com = lay((size_t)b * com_cap * 4), o_C = lay((size_t)b * 4), o_ngen = lay((size_t)b * 4),
+                     o_done = lay((size_t)b * 4), o_kvm = lay((size_t)b * 4), o_kvd = lay((size_t)b * 4),
+                     o_tok = lay((size_t)b * maxnew * 4), o_lp = lay((size_t)b * maxnew * 8),
+                     o_reason = lay((size_t)b * 4), o_cstep = lay((size_t)b * 4), o_tfin = lay((size_t)b * 8),
+                     o_tstep = lay((size_t)steps_cap * 8), o_trl = lay((size_t)steps_cap * 4),
+                     o_tracc = lay((size_t)steps_cap * b * 4), o_tremit = lay((size_t)steps_cap * b * 4),
+                     o_trkv = lay((size_t)steps_cap * b * 4), o_ident = lay((size_t)b * 4);
+        const size_t g_total = o_end;
+        char* dbase = nullptr;
+        DevLoop* dS = nullptr;
+        DevLoop hs{};
+        double g_t_start = 0.0;
+        auto graph_setup = [&]() {   // before the prompt step's first kernel
+            dbase = (char*)e->loopbuf.need(g_total, st);
+            dS = reinterpret_cast<DevLoop*>(dbase);
+            std::vector<char> h(g_total, 0);
+            hs.b = b; hs.l = ctl.length(); hs.s = ctl.s; hs.step = 0; hs.err = 0; hs.lmin = g_lmin; hs.active = 1;
+            hs.fixed = ctl.fixed; hs.incre = ctl.incre; hs.mod = ctl.mod; hs.limit = ctl.limit;
+            hs.maxnew = maxnew; hs.estride = estride; hs.com_cap = com_cap; hs.greedy = greedy ? 1 : 0;
+            hs.eos = r->eos_token; hs.steps_cap = steps_cap;
+            auto P32 = [&](size_t off) { return (int32_t*)(dbase + off); };
+            hs.com = P32(o_com); hs.C = P32(o_C); hs.ngen = P32(o_ngen); hs.done = P32(o_done);
+            hs.kvm = P32(o_kvm); hs.kvd = P32(o_kvd); hs.tokens = P32(o_tok); hs.lps = (double*)(dbase + o_lp);
+            hs.reason = P32(o_reason); hs.cstep = P32(o_cstep);
+            hs.tfin = (unsigned long long*)(dbase + o_tfin); hs.tstep = (unsigned long long*)(dbase + o_tstep);
+            hs.tr_l = P32(o_trl); hs.tr_acc = P32(o_tracc); hs.tr_emit = P32(o_tremit); hs.tr_kv = P32(o_trkv);
+            hs.rec = step_dev;
+            std::memcpy(h.data(), &hs, sizeof(hs));
+            auto H32 = [&](size_t off) { return (int32_t*)(h.data() + off); };
+            for (int s = 0; s < b; ++s) {
+                BASS_REQUIRE((int)com[s].size() <= com_cap, "device loop: prompt longer than the cache");
+                std::memcpy(H32(o_com) + (size_t)s * com_cap, com[s].data(), com[s].size() * 4);
+                H32(o_C)[s] = (int32_t)com[s].size();
+                H32(o_kvm)[s] = e->kv_main->len[s];
+                H32(o_kvd)[s] = e->kv_draft->len[s];
+                H32(o_reason)[s] = -1;
+                H32(o_ident)[s] = s;
+            }
+            BASS_CUDA(cudaMemcpyAsync(dbase, h.data(), g_total, cudaMemcpyHostToDevice, st));
+            c->h2d_bytes += (int64_t)g_total;
+            g_t_start = secs(t0, clk::now());
+            loop_stamp_kernel<<<1, 1, 0, st>>>(dS);   // device time of the generation start
+            launched(c);
+        };
+        // capture the loop graph (once per request shape; again when a workspace moved)
+        auto graph_capture = [&]() {
+            const int32_t* ident = (const int32_t*)(dbase + o_ident);
+            const int max_len = std::min(e->cap, max_seq);
+            struct Branch {
+                PlanArgs pa;
+                std::vector<Batch> bts;   // shapes only (the device writes the values)
+            };
+            std::vector<Branch> brs(g_nbr);
+            size_t arena_ints = 0;
+            for (int k = 0; k < g_nbr; ++k) {
+                const int l = g_lmin + k, nd = l + (greedy ? 0 : 1);
+                Branch& B = brs[k];
+                PlanArgs& pa = B.pa;
+                std::memset(&pa, 0, sizeof(pa));
+                pa.b = b; pa.l = l; pa.strategy = e->strategy;
+                pa.ch = stream_chunk_len(); pa.split_ch = stream_split_chunks();
+                size_t off = 0;
+                auto take = [&](size_t n) { off = (off + 7) & ~(size_t)7; const size_t r0 = off; off += n; return (int)r0; };
+                auto add_fwd = [&](int kind, int j, int qq) {
+                    PlanFwd& F = pa.f[pa.nf++];
+                    F.kind = kind; F.j = j; F.q = qq;
+                    const int Mr = b * qq, R = kind == 2 ? Mr : b;
+                    F.meta = take((size_t)3 * Mr + 4 * b + R);
+                    F.nq = stream_nq_for(qq);
+                    F.stride = stream_items_per_seq(qq, max_len);
+                    F.work = take((size_t)b * F.stride * 8);
+                    Batch bt;
+                    std::vector<int32_t> dummy(qq, 0);
+                    for (int s = 0; s < b; ++s) {
+                        bt.add_seq(s, 0, dummy.data(), qq);
+                        if (kind == 2)
+                            for (int t = 0; t < qq; ++t) bt.logit_rows.push_back(s * qq + t);
+                        else
+                            bt.logit_rows.push_back(s * qq + qq - 1);
+                    }
+                    B.bts.push_back(std::move(bt));
+                };
+                add_fwd(0, 0, 2);
+                for (int j = 1; j < nd; ++j) add_fwd(1, j, 1);
+                add_fwd(2, 0, l + 1);
+                for (int j = 0; j <= l; ++j) pa.pos[j] = take((size_t)b);
+                arena_ints = std::max(arena_ints, off);
+            }
+            int32_t* ar = (int32_t*)e->looparena.need(arena_ints * 4 + 256, st);
+            Shaped* shp = greedy ? nullptr : (Shaped*)e->shaped.need((size_t)b * Lmax * 2 * sizeof(Shaped), st);
+            std::vector<double> key = {(double)b, (double)greedy, (double)e->strategy, r->temperature, r->top_p,
+                                       (double)r->seed, (double)r->eos_token, (double)maxnew, r->align,
+                                       (double)r->align_seed, (double)g_lmin, (double)g_lmax, (double)estride,
+                                       (double)e->pstride, (double)max_len, (double)devbuf_epoch()};
+            const size_t k_epoch = key.size() - 1;
+            for (const void* p : {(const void*)dbase, (const void*)ar, (const void*)vlog, (const void*)dlog,
+                                  (const void*)vamax, (const void*)vlse, (const void*)accf, (const void*)corr,
+                                  (const void*)btok, (const void*)scratch, (const void*)step_dev, (const void*)pick_v,
+                                  (const void*)e->props(), (const void*)d_sid, (const void*)d_plen,
+                                  (const void*)d_align, (const void*)shp, (const void*)M.wblob, (const void*)D.wblob,
+                                  (const void*)e->kv_main->k, (const void*)e->kv_draft->k})
+                key.push_back((double)(uintptr_t)p);
+            LoopGraph& G = e->lg;
+            if (G.key == key && G.exec) return;
+            if (std::getenv("BASS_DEBUG_GRAPH")) {
+                for (size_t i = 0; i < key.size(); ++i)
+                    if (i >= G.key.size() || G.key[i] != key[i])
+                        std::fprintf(stderr, "loop graph rebuild: key[%zu] %.17g -> %.17g\n", i,
+                                     i < G.key.size() ? G.key[i] : -1.0, key[i]);
+            }
+            G.reset();
+            G.lmin = g_lmin;
+            G.lmax = g_lmax;
+            G.launches.assign(g_nbr, 0);
+            G.algo.assign(g_nbr, {});
+            // capture on a private stream (the caller's stream may still run the
+            // prompt step); every launch helper uses ctx->stream
+            cudaStream_t cs;
+            BASS_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+            struct Restore {
+                bass_ctx* c;
+                cudaStream_t st, cs;
+                ~Restore() {
+                    c->stream = st;
+                    cudaStreamDestroy(cs);
+                }
+            } restore{c, st, cs};
+            c->stream = cs;
+            BASS_CUDA(cudaGraphCreate(&G.graph, 0));
+            cudaGraphConditionalHandle h_loop, h_len;
+            BASS_CUDA(cudaGraphConditionalHandleCreate(&h_loop, G.graph, 0, 0));
+            // init -> WHILE(h_loop) { select -> SWITCH(h_len) { step(l) } -> continue }
+            auto knode = [&](cudaGraphNode_t* out, cudaGraph_t g, const cudaGraphNode_t* dep, void* fn, void** args) {
+                cudaKernelNodeParams kp = {};
+                kp.func = fn;
+                kp.gridDim = dim3(1);
+                kp.blockDim = dim3(1);
+                kp.kernelParams = args;
+                BASS_CUDA(cudaGraphAddKernelNode(out, g, dep, dep ? 1 : 0, &kp));
+            };
+            cudaGraphNode_t n_init, n_while, n_sel, n_switch, n_cond;
+            void* a_init[] = {(void*)&dS, (void*)&h_loop};
+            knode(&n_init, G.graph, nullptr, (void*)loop_init_kernel, a_init);
+            cudaGraphNodeParams wp = {};
+            wp.type = cudaGraphNodeTypeConditional;
+            wp.conditional.handle = h_loop;
+            wp.conditional.type = cudaGraphCondTypeWhile;
+            wp.conditional.size = 1;
+            BASS_CUDA(cudaGraphAddNode(&n_while, G.graph, &n_init, 1, &wp));
+            cudaGraph_t body = wp.conditional.phGraph_out[0];
+            BASS_CUDA(cudaGraphConditionalHandleCreate(&h_len, body, 0, 0));
+            void* a_sel[] = {(void*)&dS, (void*)&h_len};
+            knode(&n_sel, body, nullptr, (void*)loop_select_kernel, a_sel);
+            cudaGraphNodeParams sw = {};
+            sw.type = cudaGraphNodeTypeConditional;
+            sw.conditional.handle = h_len;
+            sw.conditional.type = cudaGraphCondTypeSwitch;
+            sw.conditional.size = (unsigned)g_nbr;
+            BASS_CUDA(cudaGraphAddNode(&n_switch, body, &n_sel, 1, &sw));
+            void* a_cond[] = {(void*)&dS, (void*)&h_loop};
+            knode(&n_cond, body, &n_switch, (void*)loop_continue_kernel, a_cond);
+            // branches, largest draft length first (workspaces only grow)
+            for (int k = g_nbr - 1; k >= 0; --k) {
+                const int l = g_lmin + k, nd = l + (greedy ? 0 : 1), R = b * (l + 1);
+                Branch& B = brs[k];
+                const int64_t l0 = c->launches;
+                double a0[3 * BASS_PROF_N];
+                for (int x = 0; x < BASS_PROF_N; ++x) {
+                    a0[3 * x] = (double)c->algo_n[x];
+                    a0[3 * x + 1] = c->algo_bytes[x];
+                    a0[3 * x + 2] = c->algo_flops[x];
+                }
+                BASS_CUDA(cudaStreamBeginCaptureToGraph(cs, sw.conditional.phGraph_out[k], nullptr, nullptr, 0,
+                                                        cudaStreamCaptureModeRelaxed));
+                loop_plan_kernel<<<1, ((b + 31) / 32) * 32, 0, cs>>>(dS, ar, B.pa);
+                launched(c);
+                for (int j = 0; j < nd; ++j) {
+                    const PlanFwd& F = B.pa.f[j];
+                    PreMeta pm{ar + F.meta, ar + F.work, true, F.stride, max_len};
+                    float* out = dlog + (size_t)j * b * V;
+                    forward(D, *e->kv_draft, B.bts[j], e->strategy, out, e->props(), e->pstride, &pm);
+                    if (j == l) break;   // sampled bonus row: no pick
+                    DraftPick dp{ident, d_sid, ar + B.pa.pos[j], e->props(), e->pstride, j,
+                                 r->align, r->align_seed, d_align, d_plen, maxnew};
+                    ProfScope prof(c, BASS_PROF_SAMPLE, (double)b * V * 4);
+                    if (greedy)
+                        BASS_CUDA(launch_pdl(draft_greedy_split_kernel, dim3(b, GREEDY_PARTS), dim3(256), 0, cs,
+                                             (const float*)out, V, dp, pick_v, pick_i, pick_cnt));
+                    else
+                        cl_draft_sample_kernel<<<b * CL_CTAS, CL_THREADS, 0, cs>>>(out, V, r->temperature, r->top_p,
+                                                                                  r->seed, scratch, dp);
+                    launched(c);
+                }
+                {
+                    const PlanFwd& F = B.pa.f[nd];
+                    PreMeta pm{ar + F.meta, ar + F.work, true, F.stride, max_len};
+                    forward(M, *e->kv_main, B.bts[nd], e->strategy, vlog, e->props(), e->pstride, &pm);
+                }
+                {
+                    ProfScope prof(c, BASS_PROF_SAMPLE, (double)R * V * 4);
+                    BASS_CUDA(launch_pdl(row_stats_kernel, dim3(R), dim3(SM_THREADS), 0, cs, (const float*)vlog, V,
+                                         vamax, vlse));
+                }
+                launched(c);
+                if (!greedy) {
+                    VerifyArgs va{b, l, V, r->temperature, r->top_p, r->seed, ident, d_sid, hs.C,
+                                  e->props(), e->pstride, vlog, dlog, scratch, accf, corr, btok};
+                    ProfScope prof(c, BASS_PROF_SAMPLE, (double)R * V * 8);
+                    cl_verify_shape_kernel<<<dim3((l + 1) * CL_CTAS, b, 2), CL_THREADS, 0, cs>>>(va, shp);
+                    launched(c);
+                    cl_verify_accept_kernel<<<dim3((l + 1) * CL_CTAS, b), CL_THREADS, 0, cs>>>(va, shp);
+                    launched(c);
+                }
+                StepArgs sa{b, l, V, ident, hs.C, hs.ngen, e->props(), e->pstride, vlog, vamax, vlse,
+                            maxnew, r->eos_token, accf, corr, btok, greedy ? 1 : 0, step_dev, estride};
+                BASS_CUDA(launch_pdl(finalize_kernel, dim3((b + 63) / 64), dim3(64), 0, cs, sa));
+                launched(c);
+                BASS_CUDA(launch_pdl(loop_book_kernel, dim3(1), dim3(((b + 31) / 32) * 32), 0, cs, dS));
+                launched(c);
+                cudaGraph_t got = nullptr;
+                BASS_CUDA(cudaStreamEndCapture(cs, &got));
+                G.launches[k] = c->launches - l0;
+                for (int x = 0; x < BASS_PROF_N; ++x) {
+                    G.algo[k][3 * x] = (double)c->algo_n[x] - a0[3 * x];
+                    G.algo[k][3 * x + 1] = c->algo_bytes[x] - a0[3 * x + 1];
+                    G.algo[k][3 * x + 2] = c->algo_flops[x] - a0[3 * x + 2];
+                }
+                // capture is not execution: its accounting is replayed per executed step
+                c->launches = l0;
+                for (int x = 0; x < BASS_PROF_N; ++x) {
+                    c->algo_n[x] = (int64_t)a0[3 * x];
+                    c->algo_bytes[x] = a0[3 * x + 1];
+                    c->algo_flops[x] = a0[3 * x + 2];
+                }
+            }
+            (void)n_cond;
+            BASS_CUDA(cudaGraphInstantiate(&G.exec, G.graph, 0));
+            key[k_epoch] = (double)devbuf_epoch();   // (moves only when a workspace grew while capturing)
+            G.key = key;
+            ++e->graph_builds;
+        };
+        // after the prompt step's finalize: book it, run the graph, one sync, read back
+        auto graph_finish = [&]() {
+            BASS_CUDA(launch_pdl(loop_book_kernel, dim3(1), dim3(((b + 31) / 32) * 32), 0, st, dS));
+            launched(c);
+            const auto tq = clk::now();
+            graph_capture();
+            BASS_CUDA(cudaGraphLaunch(e->lg.exec, st));
+            if (e->loop_host_cap < g_total) {   // pinned: the read-back stays asynchronous
+                if (e->loop_host) cudaFreeHost(e->loop_host);
+                e->loop_host = nullptr;
+                e->loop_host_cap = 0;
+                BASS_CUDA(cudaMallocHost((void**)&e->loop_host, g_total));
+                e->loop_host_cap = g_total;
+            }
+            char* back_p = e->loop_host;
+            BASS_CUDA(cudaMemcpyAsync(back_p, dbase, g_total, cudaMemcpyDeviceToHost, st));
+            c->d2h_bytes += (int64_t)g_total;
+            const auto tw = clk::now();
+            host_enqueue_s += secs(tq, tw);
+            c->sync();
+            e->last_syncs += 1;
+            sync_wait_s += secs(tw, clk::now());
+            const LoopGraph& G = e->lg;
+            const DevLoop& fs = *reinterpret_cast<const DevLoop*>(back_p);
+            auto B32 = [&](size_t off) { return (const int32_t*)(back_p + off); };
+            const unsigned long long* tstep = (const unsigned long long*)(back_p + o_tstep);
+            const unsigned long long* tfin = (const unsigned long long*)(back_p + o_tfin);
+            const int n_steps = fs.step;
+            BASS_REQUIRE(n_steps <= steps_cap, "device loop: step trace overflow");
+            // accounting of the graph steps (2..n): branch launches / work, attention from the trace
+            std::vector<int32_t> Cprev(b);
+            for (int s = 0; s < b; ++s) Cprev[s] = B32(o_trkv)[s];   // committed length after step 1
+            const int H_m = M.g.n_head, dh_m = M.g.d_head, H_d = D.g.n_head, dh_d = D.g.d_head;
+            const double es_m = (double)M.esize, es_d = (double)D.esize;
+            for (int k = 1; k < n_steps; ++k) {
+                const int l = B32(o_trl)[k], bi = l - G.lmin, nd = l + (greedy ? 0 : 1);
+                c->launches += G.launches[bi] + 3;   // + select / continue / the while bookkeeping
+                for (int x = 0; x < BASS_PROF_N; ++x) {
+                    c->algo_n[x] += (int64_t)G.algo[bi][3 * x];
+                    c->algo_bytes[x] += G.algo[bi][3 * x + 1];
+                    c->algo_flops[x] += G.algo[bi][3 * x + 2];
+                }
+                double ab = 0.0, af = 0.0;
+                auto att = [&](int L, int H, int dh, double es, int off, int qq) {
+                    ab += L * (2.0 * H * (off + qq) * dh + 2.0 * H * qq * dh) * es;
+                    af += L * 4.0 * H * dh * qq * (off + 0.5 * (qq + 1));
+                };
+                for (int s = 0; s < b; ++s) {
+                    if (B32(o_tracc)[(size_t)k * b + s] < 0) continue;   // finished before this step
+                    const int C0 = Cprev[s];
+                    att(D.g.n_layer, H_d, dh_d, es_d, C0 - 2, 2);
+                    for (int j = 1; j < nd; ++j) att(D.g.n_layer, H_d, dh_d, es_d, C0 + j - 1, 1);
+                    att(M.g.n_layer, H_m, dh_m, es_m, C0 - 1, l + 1);
+                    Cprev[s] = B32(o_trkv)[(size_t)k * b + s];
+                }
+                c->algo_n[BASS_PROF_ATTN] += (int64_t)(nd * D.g.n_layer + M.g.n_layer);
+                c->algo_bytes[BASS_PROF_ATTN] += ab;
+                c->algo_flops[BASS_PROF_ATTN] += af;
+            }
+            // results into the host state and the caller's arrays
+            for (int s = 0; s < b; ++s) {
+                const int C = B32(o_C)[s];
+                const int32_t* cm = B32(o_com) + (size_t)s * com_cap;
+                com[s].assign(cm, cm + C);
+                ngen[s] = B32(o_ngen)[s];
+                done[s] = B32(o_done)[s];
+                e->kv_main->len[s] = B32(o_kvm)[s];
+                e->kv_draft->len[s] = B32(o_kvd)[s];
+                std::memcpy(res->tokens + (size_t)s * maxnew, B32(o_tok) + (size_t)s * maxnew, (size_t)maxnew * 4);
+                std::memcpy(res->logprobs + (size_t)s * maxnew, (const double*)(back_p + o_lp) + (size_t)s * maxnew,
+                            (size_t)maxnew * 8);
+                if (done[s]) {
+                    res->finish_reason[s] = B32(o_reason)[s];
+                    res->completion_step[s] = B32(o_cstep)[s];
+                    res->finish_wall_s[s] = g_t_start + (double)(tfin[s] - fs.t0) * 1e-9;
+                }
+            }
+            if (res->step_draft_len)
+                for (int k = 0; k < n_steps && k < res->max_steps; ++k) {
+                    res->step_draft_len[k] = B32(o_trl)[k];
+                    res->step_wall_s[k] = (double)(tstep[k] - (k == 0 ? fs.t0 : tstep[k - 1])) * 1e-9;
+                    for (int s = 0; s < b; ++s) {
+                        res->step_accepted[(size_t)k * b + s] = B32(o_tracc)[(size_t)k * b + s];
+                        res->step_emitted[(size_t)k * b + s] = B32(o_tremit)[(size_t)k * b + s];
+                        res->step_kv_len[(size_t)k * b + s] = B32(o_trkv)[(size_t)k * b + s];
+                    }
+                }
+            // the device counted every step, the prompt step included (the host
+            // enqueue of that step counted it too)
+            main_calls = fs.main_calls;
+            draft_calls = fs.draft_calls;
+            if (!ctl.fixed) {   // a fixed controller keeps the caller's (unused) state
+                ctl.l = fs.l;
+                ctl.s = fs.s;
+            }
+            step = n_steps;
+            if (fs.err == -2) throw Error(BASS_ERR_VALUE, "draft token has zero draft probability");
+            if (fs.err == -3) throw Error(BASS_ERR_VALUE, "residual is empty: q <= p everywhere");
+            if (fs.err) throw Error(BASS_ERR_STATE, "device loop error " + std::to_string(fs.err));
+        };
+
         // any error inside a step (CUDA, a zero draft probability, an empty
         // residual) rolls both caches back to the committed prefix first, so
         // the providers stay usable (ref:engine.py:358-360 invariant)
         try {
+            if (use_graph) graph_setup();
             while (true) {
                 std::vector<int> A;
                 for (int s = 0; s < b; ++s)
@@ -387,11 +798,16 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                             maxnew, r->eos_token, accf, corr, btok, greedy ? 1 : 0, step_dev, estride};
                 BASS_CUDA(launch_pdl(finalize_kernel, dim3((nA + 63) / 64), dim3(64), 0, st, sa));
                 launched(c);
+                if (use_graph) {   // the prompt step's outcome is booked on the device; the graph runs the rest
+                    graph_finish();
+                    break;
+                }
                 c->d2h_bytes += (int64_t)(nA * rec);
                 BASS_CUDA(cudaMemcpyAsync(e->step_host, step_dev, (size_t)nA * rec, cudaMemcpyDeviceToHost, st));
                 const auto t_enq = clk::now();
                 host_enqueue_s += secs(ts, t_enq);
                 c->sync();
+                e->last_syncs += 1;
                 sync_wait_s += secs(t_enq, clk::now());
                 const double now = secs(t0, clk::now());
                 // ---------------------------------------------- bookkeeping

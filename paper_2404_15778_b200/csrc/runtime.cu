@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <type_traits>
 #include <cmath>
 #include <cstring>
@@ -24,11 +25,21 @@ void* Staging::take(size_t n) {
     return p;
 }
 
+static std::atomic<uint64_t> g_devbuf_epoch{0};
+uint64_t devbuf_epoch() { return g_devbuf_epoch.load(); }
+
 void* DevBuf::need(size_t n, cudaStream_t s) {
     if (n <= cap) return p;
+    g_devbuf_epoch.fetch_add(1);   // a captured graph holding the old address is stale
     if (p) {
-        BASS_CUDA(cudaStreamSynchronize(s));
-        BASS_CUDA(cudaFree(p));
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        BASS_CUDA(cudaStreamIsCapturing(s, &cs));
+        if (cs == cudaStreamCaptureStatusNone) {
+            BASS_CUDA(cudaStreamSynchronize(s));
+            BASS_CUDA(cudaFree(p));
+        } else {
+            retired.push_back(p);   // captured graph nodes still use it: freed with the buffer
+        }
         p = nullptr;
     }
     size_t c = std::max(n, cap * 3 / 2);
@@ -38,6 +49,8 @@ void* DevBuf::need(size_t n, cudaStream_t s) {
 }
 
 void DevBuf::release() {
+    for (void* r : retired) cudaFree(r);
+    retired.clear();
     if (p) cudaFree(p);
     p = nullptr;
     cap = 0;
@@ -464,7 +477,9 @@ static void append_meta(const Batch& b, std::vector<int32_t>& hm) {
 }
 
 // the forward's attention runs the stream kernel (its work list can be pre-staged)
-static bool uses_stream_attention(const bass_model& m) {
+bool model_uses_stream_attention(const bass_model& m);
+static bool uses_stream_attention(const bass_model& m) { return model_uses_stream_attention(m); }
+bool model_uses_stream_attention(const bass_model& m) {
     return m.dtype != BASS_F32 && tc_attention_supported(BASS_BF16, m.g.d_head);
 }
 
@@ -519,7 +534,14 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
     AttnPlan plan;
     double attn_bytes = 0.0, attn_flops = 0.0;
     float *pa_o = nullptr, *pa_ml = nullptr;
-    if (uses_stream_attention(m)) {
+    if (uses_stream_attention(m) && pre && pre->dev) {
+        // device-planned (decode-loop graph): lengths live on the device; the
+        // algorithmic bytes are accounted by the engine from the step trace
+        stream_attention_plan_dev(ctx, strategy, q, M, kv.n_slots, b.qn, H, dh, kv.cap, pre->work, pre->work_stride,
+                                  pre->max_len, plan);
+        pa_o = (float*)m.part_o.need((size_t)M * H * plan.mc * dh * 4, st);
+        pa_ml = (float*)m.part_ml.need((size_t)M * H * plan.mc * 2 * 4, st);
+    } else if (uses_stream_attention(m)) {
         stream_attention_plan(ctx, strategy, q, M, kv.n_slots, b.slot, b.qn, b.off, H, dh, kv.cap, work_buf, plan,
                               pre ? pre->work : nullptr);
         pa_o = (float*)m.part_o.need((size_t)M * H * plan.mc * dh * 4, st);

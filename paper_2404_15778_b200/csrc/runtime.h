@@ -42,9 +42,13 @@ struct Staging {
 };
 
 // Device buffer that grows (after a stream sync) when a larger size is needed.
+// Every growth bumps a process-wide epoch (devbuf_epoch): a captured CUDA graph
+// records it and is re-captured when any workspace it references may have moved.
+uint64_t devbuf_epoch();
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
+    std::vector<void*> retired;   // outgrown while a stream capture referenced them
     void* need(size_t n, cudaStream_t s);
     void release();
 };
@@ -183,6 +187,13 @@ struct Batch {
 struct PreMeta {
     const int32_t* meta = nullptr;   // device: the forward's meta block
     const void* work = nullptr;      // device: stream-attention work list (nullptr: forward uploads its own)
+    // device-planned forward (the device-resident decode loop, engine.cu):
+    // the meta block and the work list are written on the device by the
+    // step's plan kernel, so the host knows only the shapes.  The work list
+    // holds n_seq regions of work_stride items (idle items pad a region);
+    // every history is shorter than max_len.
+    bool dev = false;
+    int work_stride = 0, max_len = 0;
 };
 struct PreMetaOff {
     size_t meta = 0, work = 0;       // offsets into the arena (int32 units, 32-byte aligned)
@@ -196,6 +207,10 @@ PreMetaOff forward_premeta(const bass_model& m, const Batch& b, int strategy, co
 inline PreMeta premeta_at(const int32_t* dev_arena, const PreMetaOff& o) {
     return PreMeta{dev_arena + o.meta, o.has_work ? (const void*)(dev_arena + o.work) : nullptr};
 }
+
+// the forward's attention runs the persistent tcgen05 stream kernel (bf16 /
+// int8 models, d_head 64 or 128): the precondition of device-planned forwards
+bool model_uses_stream_attention(const bass_model& m);
 
 // Run `b` through model m over cache kv; logits [logit_rows, V] fp32 -> logits_out (device).
 // `pre`: metadata already on the device (forward_premeta + one upload).
@@ -257,4 +272,15 @@ void stream_attention_work(int strategy, const std::vector<int32_t>& slot, const
                            std::vector<int32_t>& w);
 void stream_attention_run(bass_ctx* ctx, const AttnPlan& plan, const void* kc, const void* vc, const Seqs& seqs_dev,
                           float* part_o, float* part_ml, void* out);
+// device-planned variant (PreMeta::dev): work list written on the device
+void stream_attention_plan_dev(bass_ctx* ctx, int strategy, const void* q, int M, int n_slots,
+                               const std::vector<int32_t>& qn, int H, int dh, int cap, const void* work,
+                               int work_stride, int max_len, AttnPlan& plan);
+// work-list geometry shared with the device planner: query-tile width for a
+// block of q rows, 128-key chunk length, chunks per split, and the items one
+// sequence of q rows needs when its history is shorter than max_len
+int stream_nq_for(int q);
+int stream_chunk_len();
+int stream_split_chunks();
+int stream_items_per_seq(int q, int max_len);
 }  // namespace bass

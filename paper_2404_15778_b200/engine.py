@@ -108,6 +108,23 @@ class CudaEngine:
         from .attention import strategy_code
         self.ctx.check(self.ctx.lib.bass_engine_set_strategy(self.handle, strategy_code(strategy)))
 
+    def set_loop(self, mode: str):
+        """"device" (default): every step after the prompt step runs from one
+        CUDA graph with the step planning, bookkeeping and Algorithm 1 on the
+        GPU (one host synchronisation per generation); "host": the host plans
+        every step and reads its outcome back.  Identical results."""
+        code = {"host": L.LOOP_HOST, "device": L.LOOP_DEVICE}[mode]
+        self.ctx.check(self.ctx.lib.bass_engine_set_loop(self.handle, code))
+
+    def loop_info(self) -> dict:
+        """How the last speculative generation ran: loop mode, host
+        synchronisations, loop-graph captures so far."""
+        mode, syncs, builds = C.c_int32(), C.c_int32(), C.c_int64()
+        self.ctx.check(self.ctx.lib.bass_engine_loop_info(self.handle, C.byref(mode), C.byref(syncs),
+                                                          C.byref(builds)))
+        return {"mode": "device" if mode.value == L.LOOP_DEVICE else "host", "syncs": syncs.value,
+                "graph_builds": builds.value}
+
     def __del__(self):
         try:
             if getattr(self, "handle", None) and L.alive():
