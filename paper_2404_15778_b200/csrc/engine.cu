@@ -438,12 +438,6 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                 key.push_back((double)(uintptr_t)p);
             LoopGraph& G = e->lg;
             if (G.key == key && G.exec) return;
-            if (std::getenv("BASS_DEBUG_GRAPH")) {
-                for (size_t i = 0; i < key.size(); ++i)
-                    if (i >= G.key.size() || G.key[i] != key[i])
-                        std::fprintf(stderr, "loop graph rebuild: key[%zu] %.17g -> %.17g\n", i,
-                                     i < G.key.size() ? G.key[i] : -1.0, key[i]);
-            }
             G.reset();
             G.lmin = g_lmin;
             G.lmax = g_lmax;
