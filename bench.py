@@ -305,8 +305,6 @@ def main():
     cfg = CONFIGS[args.config]
     if args.align is None:
         args.align = 0.874 if cfg["temperature"] == 0.0 else -1.0
-    if cfg["temperature"] > 0.0 and args.align >= 0.0:
-        raise SystemExit("--align is for greedy configs: sampled acceptance needs proposals drawn from the draft")
     if args.impl == "reference":
         run_reference_arm(args, cfg)
         return
@@ -369,6 +367,15 @@ def main():
         reset()
         rd, rd_arr, _ = eng.run(req, None, speculative=False)
         align_tokens = rd_arr["tokens"]
+        if cfg["temperature"] > 0.0 and args.align >= 0.0:
+            # sampled harness: the draft rows become point masses on keyed
+            # override tokens taken from an INDEPENDENT-seed main trajectory,
+            # so proposals never depend on the verify draws and speculative
+            # sampling stays exact (the output law is the main model's)
+            reset()
+            req_t = B.GenerationRequest(prompts, new, temperature=cfg["temperature"], top_p=cfg["top_p"],
+                                        seed=req.seed + 7919, sequence_ids=sids)
+            align_tokens = eng.run(req_t, None, speculative=False)[1]["tokens"]
         if args.save_traj:
             np.save(args.save_traj, align_tokens)
 
@@ -514,7 +521,9 @@ def main():
                                                   "bf16 attention / KV)" if args.dtype == "int8" else ""),
                    "batch_per_gpu": b, "global_batch": n_total,
                    "prompt_len": P, "max_new_tokens": new, "step": "one full generation",
-                   "draft_harness": (f"keyed override, align={args.align}" if args.align >= 0
+                   "draft_harness": (f"keyed override, align={args.align}" + (
+                                         " (sampled: point-mass draft rows on an independent-seed main "
+                                         "trajectory)" if cfg["temperature"] > 0.0 else "") if args.align >= 0
                                      else "natural acceptance (draft samples its own proposals)"),
                    "strategy": args.strategy, "gemm": args.gemm,
                    "l2": "weights (17 GB/replica) >> L2; no flush needed",

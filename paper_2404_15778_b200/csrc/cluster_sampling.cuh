@@ -397,9 +397,15 @@ BASS_DEV int cl_accept_shaped(const float* qrow, const float* prow, int V, const
 // blockIdx.x / CL_CTAS.  The trailing cl_sync keeps each CTA's shared memory
 // alive until the whole cluster is done reading it.
 
-// sampled draft step: proposal ~ shape(row), uniform = RNG(seed, sid, DRAFT, pos)
+// sampled draft step: proposal ~ shape(row), uniform = RNG(seed, sid, DRAFT, pos).
+// With the acceptance harness on (d.align >= 0) the proposal is the keyed
+// override token and the row becomes a point mass on it — the reference's
+// SyntheticAlignedDraft row form (ref:model.py:379-389: logits -inf except 0
+// at y) — so the verify tests and resamples against the distribution the
+// proposal was actually drawn from (speculative sampling stays exact when the
+// override tokens do not depend on the verify draws).
 static __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_THREADS)
-    cl_draft_sample_kernel(const float* __restrict__ logits, int V, double T, double top_p, uint64_t seed,
+    cl_draft_sample_kernel(float* __restrict__ logits, int V, double T, double top_p, uint64_t seed,
                            double* scratch, DraftPick d) {
     __shared__ ClSmem sm;
     pdl_trigger();
@@ -414,7 +420,13 @@ static __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_THRE
     const double u = pcg64_double(g);
     const Shaped sh = sm.sh;
     const int tok = cl_inverse_cdf(V, u, [&](int k) { return sh_prob(sh, row, e, k); }, cl);
-    if (threadIdx.x == 0 && cl_rank() == 0) d.proposals[slot * d.pstride + d.j] = aligned_override(d, slot, pos, V, tok);
+    const int prop = aligned_override(d, slot, pos, V, tok);
+    if (threadIdx.x == 0 && cl_rank() == 0) d.proposals[slot * d.pstride + d.j] = prop;
+    if (d.align >= 0.0) {
+        cl_sync();   // every CTA is done reading the row
+        float* w = logits + (int64_t)i * V;
+        for (int k = cl.c0 + threadIdx.x; k < cl.c1; k += blockDim.x) w[k] = k == prop ? 0.f : -INFINITY;
+    }
     cl_sync();
 }
 

@@ -232,9 +232,9 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
         }
         const int limit = ctl.max_length();
         BASS_REQUIRE(limit >= 1, "draft limit must be >= 1");
-        // the keyed acceptance override replaces proposals by point masses; a
-        // sampled verify would then divide by a zero draft probability
-        BASS_REQUIRE(r->align < 0.0 || r->temperature == 0.0, "the keyed acceptance override (align) needs greedy decoding");
+        // the keyed acceptance override: greedy replaces the proposal token;
+        // sampled also turns the draft row into a point mass on it
+        // (cl_draft_sample_kernel), so the verify never sees a zero draft probability
         const int max_seq = std::min(M.g.max_seq_len, D.g.max_seq_len);
         for (auto& p : q.prompts)
             BASS_REQUIRE((int)p.size() + r->max_new_tokens + limit <= max_seq,

@@ -160,3 +160,21 @@ def test_int8_device_loop_equals_host(B):
     dev = _run(B, wm, wm, req, B.AdaptiveDraftController(), "device")
     _same(host, dev)
     del g
+
+
+def test_sampled_point_mass_harness_device_equals_host(B, models):
+    """The sampled acceptance harness (point-mass draft rows on keyed
+    override tokens from an independent-seed trajectory): accepted proposals,
+    identical on both loop drivers, and the harness tokens really are what
+    the draft rows propose."""
+    wm, wd = models
+    prompts = _prompts(4, 2048, 8)
+    req = B.GenerationRequest(prompts, 32, temperature=0.7, top_p=0.9, seed=77)
+    eng = B.CudaEngine(B.CudaModel(wm, 4), B.CudaModel(wd, 4))
+    traj = eng.run(B.GenerationRequest(prompts, 32, temperature=0.7, top_p=0.9, seed=78), None,
+                   speculative=False)[1]["tokens"]
+    host = _run(B, wm, wd, req, B.AdaptiveDraftController(), "host", "ragged", 0.9, traj)
+    dev = _run(B, wm, wd, req, B.AdaptiveDraftController(), "device", "ragged", 0.9, traj)
+    _same(host, dev)
+    acc = [a for s in dev[0].steps for a in s.accepted]
+    assert sum(acc) > 0   # the random-init draft alone is never accepted
