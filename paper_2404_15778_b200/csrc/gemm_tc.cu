@@ -36,6 +36,7 @@
 #include <tuple>
 
 #include "runtime.h"
+#include "quant.cuh"
 
 namespace bass {
 namespace tc {
@@ -461,25 +462,66 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
         if constexpr (I8) return (float)((double)__float_as_int(bits) * __ldg(sp.sx + m) * __ldg(sp.sw + n));
         else return bits;
     };
-    // W8A8 epilogues whose output is quantized next (ref:model.py:219-222, 243-244):
-    // QKV stores fp32 q|k|v and the max |value| per (row, head); FC applies the
-    // exact GELU, stores fp32 and the max per row.  Lanes hold consecutive
-    // columns, so a group's max is a warp shuffle reduction and one uint-ordered
-    // atomicMax (|v| >= 0) per group: order-independent, hence deterministic.
+    // W8A8 FC epilogue (its output is quantized per token next, ref:model.py:243-244):
+    // the exact GELU, an fp32 store and the row's running max |value| — lanes
+    // hold consecutive columns, so a warp shuffle reduction and one
+    // uint-ordered atomicMax (|v| >= 0) per warp: order-free, deterministic.
     auto emit = [&](int m, int n, float bits) {
         const float v0 = deq(m, n, bits);
-        if constexpr (I8 && (MODE == EPI_QKV || MODE == EPI_GELU)) {
-            const float v = MODE == EPI_GELU ? gelu_erf(v0) : v0;
+        if constexpr (I8 && MODE == EPI_GELU) {
+            const float v = gelu_erf(v0);
             reinterpret_cast<float*>(e.out)[(int64_t)m * N + n] = v;
-            const int grp = MODE == EPI_QKV ? min(e.dh, 32) : 32;
             float a = fabsf(v);
-            for (int o = 1; o < grp; o <<= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
-            if ((lane & (grp - 1)) == 0) {
-                const int64_t slot = MODE == EPI_QKV ? (int64_t)m * (N / e.dh) + n / e.dh : m;
-                atomicMax(reinterpret_cast<unsigned*>(e.amax) + slot, __float_as_uint(a));
-            }
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+            if (lane == 0) atomicMax(reinterpret_cast<unsigned*>(e.amax) + m, __float_as_uint(a));
         } else {
             epilogue<MODE, __nv_bfloat16>(e, m, n, N, v0);
+        }
+    };
+    // W8A8 QKV: q / k / v fake-quantized per (token, head) right here
+    // (ref:model.py:219-222, quant.py:126-129) and written as bf16 to q and
+    // the KV cache — no fp32 round trip, no separate quantizer kernel.  A
+    // head's columns are one warp (d_head <= 32) or 2-4 warps of the same
+    // row half: their maxima meet in a 512-byte exchange at the end of the
+    // (idle) stage ring behind a 128-thread named barrier per half.
+    constexpr bool QQ = I8 && MODE == EPI_QKV;
+    float* qx = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE - 512) + half * 64;   // [16 rows][4 warps]
+    auto qgrp = [&](auto& w, int m_first, int count, int n) {
+        constexpr int U = sizeof(w) / sizeof(float);
+        const int dh = e.dh, g = dh < 32 ? dh : 32;
+        float a[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            a[u] = u < count ? fabsf(w[u]) : 0.f;
+            for (int o = 1; o < g; o <<= 1) a[u] = fmaxf(a[u], __shfl_xor_sync(0xffffffffu, a[u], o));
+        }
+        if (dh > 32) {
+            if (lane == 0)
+#pragma unroll
+                for (int u = 0; u < U; ++u) qx[u * 4 + wq] = a[u];
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + half) : "memory");
+            const int wpg = dh / 32, w0 = (wq / wpg) * wpg;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                float mx = 0.f;
+                for (int t = 0; t < wpg; ++t) mx = fmaxf(mx, qx[u * 4 + w0 + t]);
+                a[u] = mx;
+            }
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + half) : "memory");
+        }
+        const int part = n / e.d, nn = n - part * e.d, hh = nn / dh, c = nn - hh * dh;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (u >= count) break;
+            const int m = m_first + u;
+            const double sc = group_scale(a[u]);
+            const __nv_bfloat16 val = __float2bfloat16_rn((float)((double)quant_round((double)w[u] / sc) * sc));
+            if (part == 0)
+                reinterpret_cast<__nv_bfloat16*>(e.out)[(int64_t)m * e.d + nn] = val;
+            else
+                reinterpret_cast<__nv_bfloat16*>(part == 1 ? e.kc : e.vc)
+                    [(((int64_t)__ldg(e.row_slot + m) * e.H + hh) * e.cap + __ldg(e.row_pos + m)) * dh + c] = val;
         }
     };
     if constexpr (LNF == 0) {
@@ -493,13 +535,20 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
                 float v[16];
                 tmem_ld16(trow + sub * TT + c0, v);
                 if (n < N) {
+                    if constexpr (QQ) {
+                        float w[16];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        if (c0 + j < rows) emit(m0 + c0 + j, n, v[j]);
+                        for (int j = 0; j < 16; ++j) w[j] = c0 + j < rows ? deq(m0 + c0 + j, n, v[j]) : 0.f;
+                        qgrp(w, m0 + c0, min(16, rows - c0), n);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (c0 + j < rows) emit(m0 + c0 + j, n, v[j]);
+                    }
                 }
             }
         }
-    } else if ((size_t)rows * NB * BN * 4 <= (size_t)C::STAGES * C::STAGE) {
+    } else if ((size_t)rows * NB * BN * 4 + (QQ ? 512 : 0) <= (size_t)C::STAGES * C::STAGE) {
         // split-K through distributed shared memory: the S CTAs of this tile
         // are one cluster.  Each parks its fp32 partial [token][row] in its own
         // (now idle) stage ring, the cluster barrier publishes it, and CTA
@@ -535,13 +584,25 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
                 for (; r + 4 <= re; r += 4) {   // 4 rows x S partials in flight
                     float acc[4];
                     dsmem_sum<4, I8>(part_s + (uint32_t)((r * WR + nn) * 4), WR * 4, sp.S, acc);
+                    if constexpr (QQ) {
+                        float w[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) emit(m0 + r + u, n, acc[u]);
+                        for (int u = 0; u < 4; ++u) w[u] = deq(m0 + r + u, n, acc[u]);
+                        qgrp(w, m0 + r, 4, n);
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) emit(m0 + r + u, n, acc[u]);
+                    }
                 }
                 for (; r < re; ++r) {
                     float acc;
                     dsmem_sum<1, I8>(part_s + (uint32_t)((r * WR + nn) * 4), WR * 4, sp.S, &acc);
-                    emit(m0 + r, n, acc);
+                    if constexpr (QQ) {
+                        float w[1] = {deq(m0 + r, n, acc)};
+                        qgrp(w, m0 + r, 1, n);
+                    } else {
+                        emit(m0 + r, n, acc);
+                    }
                 }
             }
         }
@@ -581,13 +642,25 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
                 for (; r + 4 <= re; r += 4) {   // 4 rows x S partials in flight
                     float acc[4];
                     l2_sum<4, I8>(blk + (int64_t)r * WR + nn, (int64_t)TT * WR, WR, sp.S, acc);
+                    if constexpr (QQ) {
+                        float w[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) emit(m0 + r + u, n, acc[u]);
+                        for (int u = 0; u < 4; ++u) w[u] = deq(m0 + r + u, n, acc[u]);
+                        qgrp(w, m0 + r, 4, n);
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) emit(m0 + r + u, n, acc[u]);
+                    }
                 }
                 for (; r < re; ++r) {
                     float acc;
                     l2_sum<1, I8>(blk + (int64_t)r * WR + nn, (int64_t)TT * WR, WR, sp.S, &acc);
-                    emit(m0 + r, n, acc);
+                    if constexpr (QQ) {
+                        float w[1] = {deq(m0 + r, n, acc)};
+                        qgrp(w, m0 + r, 1, n);
+                    } else {
+                        emit(m0 + r, n, acc);
+                    }
                 }
             }
         }
@@ -923,13 +996,17 @@ static State& state(bass_model& m) {
 // within 1.75 CTAs per SM; S = 2 may fill the two-CTA-per-SM wave (<= 2 per SM)
 // when each CTA still streams >= 32 k blocks.  At every C2 shape this gives the
 // measured optimum (qkv 2, o 6, fc 2, proj 6, head 1; draft 4 / 8 / 4 / 8 / 1).
-static int choose_splits(int sm_count, int N, int K) {
+// int8 (W8A8) GEMMs pass K / 2 (a k block is 128 bytes either way) and a
+// 16-block floor for the two-CTA wave: their per-CTA stream is half as long
+// for the same split, and the C2 FC projection measured best at S = 2
+// (1.494 -> 1.457 ms/token; profiles/r2/int8_split_sweep.txt).
+static int choose_splits(int sm_count, int N, int K, int wave_blocks = 32) {
     const int n_tiles = (N + BN - 1) / BN, k_iters = K / BK;
     int best = 1;
     for (int s = 2; s <= MAX_S; ++s) {
         if (k_iters % s != 0 || k_iters / s < 4) continue;
         const int ctas = n_tiles * s;
-        if (ctas * 4 <= sm_count * 7 || (s == 2 && ctas <= 2 * sm_count && k_iters / s >= 32)) best = s;
+        if (ctas * 4 <= sm_count * 7 || (s == 2 && ctas <= 2 * sm_count && k_iters / s >= wave_blocks)) best = s;
     }
     return best;
 }
@@ -976,8 +1053,8 @@ template <int TT>
 static void launch_mode(bass_model& m, int mode, bool packed, bool xn, const LaunchArgs& a, const Epi& e) {
     if (a.sp.sx) {   // W8A8 (packed int8 weights): plain epilogues after the dequantization
         if (!packed || xn) throw Error(BASS_ERR_STATE, "int8 GEMM: packed weights, no folded LayerNorm");
-        if ((mode == EPI_QKV || mode == EPI_GELU) && (!e.amax || a.N % 32 != 0))
-            throw Error(BASS_ERR_STATE, "int8 QKV / GELU epilogues need the amax buffer and N % 32 == 0");
+        if ((mode == EPI_QKV || mode == EPI_GELU) && (a.N % 128 != 0 || (mode == EPI_GELU && !e.amax)))
+            throw Error(BASS_ERR_STATE, "int8 QKV / GELU epilogues: N % 128 == 0 (GELU: with its amax buffer)");
         if (mode == EPI_RESID) launch_k<TT, EPI_RESID, true, 0, true>(m, a, e);
         else if (mode == EPI_STORE) launch_k<TT, EPI_STORE, true, 0, true>(m, a, e);
         else if (mode == EPI_QKV) launch_k<TT, EPI_QKV, true, 0, true>(m, a, e);
@@ -1053,7 +1130,8 @@ void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N
     auto sk = std::make_pair(N, K);
     auto si = S.splits.find(sk);
     // int8: a k block is 128 elements, so the split rule sees K / 2 bf16-equivalent columns
-    if (si == S.splits.end()) si = S.splits.emplace(sk, choose_splits(m.ctx->sm_count, N, i8 ? K / 2 : K)).first;
+    if (si == S.splits.end())
+        si = S.splits.emplace(sk, choose_splits(m.ctx->sm_count, N, i8 ? K / 2 : K, i8 ? 16 : 32)).first;
     // one token group: every weight byte is read once (prefill re-reads it per group from L2)
     Split sp{si->second, i8 ? K / 128 : K / BK, nullptr, (packed && M <= TT) ? 1 : 0, sx, sw};
     // reduction loops and cluster size hold <= 8; every split owns >= 1 k block

@@ -3,8 +3,9 @@
 //   - weights: one scale per output channel, scale = max|w| / 127 (1 for an
 //     all-zero channel), payload = clip(round_half_away(w / scale), +-127);
 //   - activations entering every linear layer: one scale per token row;
-//   - q / k / v: fake-quantized per (token, head) — the attention sees the
-//     dequantized values (stored bf16 here, like the bf16 path's cache);
+//   - q / k / v: fake-quantized per (token, head) in the QKV GEMM epilogue
+//     (gemm_tc.cu) — the attention sees the dequantized values (stored bf16,
+//     like the bf16 path's cache);
 //   - the GEMM accumulates int8 x int8 exactly (tcgen05 kind::i8, s32 in
 //     TMEM) and dequantizes in its epilogue: out = acc * s_token * s_channel.
 // Scales are fp64 like the reference's; the row kernels below compute the
@@ -57,7 +58,7 @@ BASS_DEV double block_max_d(double v, double* scratch) {
 // fp32 matrix src [N, K] -> packed int8 rows row_off + n of dst (row length
 // K), scale -> scale[row_off + n].  One CTA per output channel; fp64 scale and
 // division, so the payload equals the reference's bit for bit.
-__global__ void quant_weight_rows_kernel(const float* __restrict__ src, int K, int8_t* __restrict__ dst,
+static __global__ void quant_weight_rows_kernel(const float* __restrict__ src, int K, int8_t* __restrict__ dst,
                                          int64_t row_off, double* __restrict__ scale) {
     __shared__ double red[32];
     const int n = blockIdx.x;
@@ -73,7 +74,7 @@ __global__ void quant_weight_rows_kernel(const float* __restrict__ src, int K, i
 
 // dequantized packed int8 rows -> reference [K, N] fp32 (get_weight) or the
 // raw payload in the reference layout (get_qweight)
-__global__ void dequant_gather_kernel(const int8_t* __restrict__ w, const double* __restrict__ scale, int K, int N,
+static __global__ void dequant_gather_kernel(const int8_t* __restrict__ w, const double* __restrict__ scale, int K, int N,
                                       int64_t row_off, float* __restrict__ out_f, int8_t* __restrict__ out_q) {
     const int64_t total = (int64_t)K * N;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -86,7 +87,7 @@ __global__ void dequant_gather_kernel(const int8_t* __restrict__ w, const double
 
 // reference-layout int8 payload [K, N] (input-major, ref:quant.py:55-63) ->
 // packed output-major tiles (rows beyond N stay as the caller zeroed them)
-__global__ void pack_i8_ref_kernel(const int8_t* __restrict__ src, int K, int N, int8_t* __restrict__ dst) {
+static __global__ void pack_i8_ref_kernel(const int8_t* __restrict__ src, int K, int N, int8_t* __restrict__ dst) {
     const int64_t total = (int64_t)K * N;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t k = i / N, n = i - k * N;
@@ -101,7 +102,7 @@ __global__ void pack_i8_ref_kernel(const int8_t* __restrict__ src, int K, int N,
 // source rows (final LayerNorm of the logit rows).  It also clears the row's
 // amax accumulators of the QKV (n_groups per row) and FC epilogues: every
 // projection that fills them follows a LayerNorm.
-__global__ void __launch_bounds__(LN_THREADS) ln_quant_kernel(const float* __restrict__ x,
+static __global__ void __launch_bounds__(LN_THREADS) ln_quant_kernel(const float* __restrict__ x,
                                                               const int32_t* __restrict__ gather,
                                                               const float* __restrict__ g,
                                                               const float* __restrict__ b, int d,
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(LN_THREADS) ln_quant_kernel(const float* __res
 // Grid (rows, chunks of QR_CHUNK columns): every CTA reduces the whole row's
 // max |value| (one L2-resident read of d bf16) and quantizes its own chunk.
 constexpr int QR_CHUNK = 1024;
-__global__ void __launch_bounds__(256) quant_ctx_kernel(const __nv_bfloat16* __restrict__ in, int d,
+static __global__ void __launch_bounds__(256) quant_ctx_kernel(const __nv_bfloat16* __restrict__ in, int d,
                                                         int8_t* __restrict__ out, double* __restrict__ scale,
                                                         TraceArg tr) {
     const unsigned long long t_start = tr.buf ? gtimer() : 0ull;
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(256) quant_ctx_kernel(const __nv_bfloat16* __r
 // Per-token quantization of the GELU output (fp32 [M, n], GELU and the row's
 // max |value| already applied / accumulated by the FC GEMM epilogue) before
 // Wproj.  Grid (rows, chunks of QR_CHUNK columns).
-__global__ void __launch_bounds__(256) quant_amax_rows_kernel(const float* __restrict__ in, int n,
+static __global__ void __launch_bounds__(256) quant_amax_rows_kernel(const float* __restrict__ in, int n,
                                                               const float* __restrict__ amax_r,
                                                               int8_t* __restrict__ out, double* __restrict__ scale,
                                                               TraceArg tr) {
@@ -217,36 +218,6 @@ __global__ void __launch_bounds__(256) quant_amax_rows_kernel(const float* __res
     for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x)
         out[(int64_t)r * n + c] = quant_round((double)in[(int64_t)r * n + c] / sc);
     if (threadIdx.x == 0 && blockIdx.y == 0) scale[r] = sc;
-    trace_end(tr, t_start);
-}
-
-// q / k / v of one token row: fake-quantized per (token, head)
-// (ref:quant.py:126-129 fake_quant_per_head, model.py:219-222) with the
-// per-(row, head) max the QKV GEMM epilogue accumulated, then q -> q_out
-// [M, d] and k / v appended to the cache at (slot, pos) (ref:kv_cache.py:63-84).
-// qkv: the QKV GEMM's fp32 output [M, 3d].  Grid (rows, groups of 8 (part,
-// head) pairs), one warp per pair.
-__global__ void __launch_bounds__(256) qkv_quant_kernel(const float* __restrict__ qkv,
-                                                        const float* __restrict__ amax_g, Rows rows, int H,
-                                                        int dh, int cap, __nv_bfloat16* __restrict__ q_out,
-                                                        __nv_bfloat16* __restrict__ kc,
-                                                        __nv_bfloat16* __restrict__ vc, TraceArg tr) {
-    const unsigned long long t_start = tr.buf ? gtimer() : 0ull;
-    pdl_trigger();
-    pdl_wait();
-    const int m = blockIdx.x, lane = threadIdx.x & 31;
-    const int grp = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (grp < 3 * H) {
-        const int d = H * dh;
-        const int part = grp / H, h = grp - part * H;
-        const float* src = qkv + (int64_t)m * 3 * d + (int64_t)part * d + (int64_t)h * dh;
-        const double sc = group_scale(amax_g[(int64_t)m * 3 * H + grp]);
-        __nv_bfloat16* dst = part == 0
-                                 ? q_out + (int64_t)m * d + (int64_t)h * dh
-                                 : (part == 1 ? kc : vc) + (((int64_t)rows.slot[m] * H + h) * cap + rows.pos[m]) * dh;
-        for (int c = lane; c < dh; c += 32)
-            dst[c] = __float2bfloat16_rn((float)((double)quant_round((double)src[c] / sc) * sc));
-    }
     trace_end(tr, t_start);
 }
 

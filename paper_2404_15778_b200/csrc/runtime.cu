@@ -526,7 +526,7 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
     void* h = m.h.need((size_t)M * d * es, st);
     void* q = m.q.need((size_t)M * d * es, st);
     void* cx = m.ctxb.need((size_t)M * d * es, st);
-    // int8 models: fp32 [M, 3d] QKV output / [M, 4d] FC pre-activation
+    // int8 models: fp32 [M, 4d] GELU output of the FC projection
     void* f = m.f.need((size_t)M * 4 * d * (m.int8() ? 4 : es), st);
     DevBuf& work_buf = m.attn_work;
 
@@ -603,10 +603,9 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
         // their way to the attention and the cache.
         const int RM = std::max(M, R);
         int8_t* xq = (int8_t*)m.xq.need((size_t)RM * 4 * d, st);
-        // per-token scales [RM] | QKV amax [RM][3H] | FC amax [RM]
-        double* xs = (double*)m.xs.need((size_t)RM * (8 + 4 * 3 * H + 4), st);
-        float* amax_qkv = (float*)(xs + RM);
-        float* amax_fc = amax_qkv + (size_t)RM * 3 * H;
+        // per-token scales [RM] | FC amax [RM]
+        double* xs = (double*)m.xs.need((size_t)RM * (8 + 4), st);
+        float* amax_fc = (float*)(xs + RM);
         float* f32 = (float*)f;
         BASS_CUDA(launch_pdl(embed_kernel<__nv_bfloat16>, dim3(M), dim3(256), 0, st,
                              (const __nv_bfloat16*)m.tok_emb, (const __nv_bfloat16*)m.pos_emb, rows, proposals,
@@ -616,13 +615,9 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
         auto ln_q = [&](const float* g_, const float* b_, const int32_t* gather, int nrows) {
             ProfScope prof(ctx, BASS_PROF_NORM, (double)nrows * d * 5.0);
             BASS_CUDA(launch_pdl(ln_quant_kernel, dim3(nrows), dim3(LN_THREADS), 0, st, (const float*)x, gather, g_,
-                                 b_, d, xq, xs, amax_qkv, 3 * H, amax_fc, ctx->trace(nrows, BASS_TR_NORM)));
+                                 b_, d, xq, xs, (float*)nullptr, 0, amax_fc, ctx->trace(nrows, BASS_TR_NORM)));
             check_launch(ctx);
         };
-        Epi eq{};
-        eq.out = f32;
-        eq.amax = amax_qkv;
-        eq.dh = dh;
         Epi ef{};
         ef.out = f32;
         ef.amax = amax_fc;
@@ -630,15 +625,8 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
         for (int li = 0; li < g.n_layer; ++li) {
             const bass_layer& L = m.layers[li];
             ln_q(L.ln1_g, L.ln1_b, nullptr, M);
-            gemm_i8(m, EPI_QKV, xq, xs, L.wqkv, L.sqkv, M, 3 * d, d, eq);
-            {
-                ProfScope prof(ctx, BASS_PROF_NORM, (double)M * 3 * d * 6.0);
-                BASS_CUDA(launch_pdl(qkv_quant_kernel, dim3(M, (3 * H + 7) / 8), dim3(256), 0, st, (const float*)f32,
-                                     (const float*)amax_qkv, rows, H, dh, kv.cap, (__nv_bfloat16*)q,
-                                     (__nv_bfloat16*)kc_of(li), (__nv_bfloat16*)vc_of(li),
-                                     ctx->trace(M * ((3 * H + 7) / 8), BASS_TR_NORM)));
-                check_launch(ctx);
-            }
+            // q / k / v fake-quantized per (token, head) in the QKV epilogue
+            gemm_i8(m, EPI_QKV, xq, xs, L.wqkv, L.sqkv, M, 3 * d, d, qkv_epi(li));
             run_attention(li, kc_of(li), vc_of(li));
             {
                 ProfScope prof(ctx, BASS_PROF_NORM, (double)M * d * 3.0);
