@@ -394,17 +394,23 @@ def test_sequence_ids_beyond_int32_and_long_drafts_match_oracle(B):
     assert got.main_forward_calls == ref.main_calls and got.draft_forward_calls == ref.draft_calls
 
 
-def test_align_override_requires_greedy_and_errors_roll_back(B):
-    """The keyed acceptance override (bench harness) is rejected for sampled
-    decoding before any work, and the providers stay usable."""
+def test_align_override_sampled_point_mass_and_providers_stay_usable(B):
+    """The keyed acceptance override in sampled decoding turns each draft row
+    into a point mass on its proposal (cl_draft_sample_kernel), so the verify
+    never meets a zero draft probability; the caches end at the committed
+    prefix and the providers stay usable (ref:engine.py:358-360)."""
     from paper_2404_15778_b200 import engine as E
     tw = B.DeviceWeights.from_reference(OR.init_weights(TINY, 1234), "fp32")
     main, draft = B.CudaModel(tw, 2), B.CudaModel(tw, 2)
     eng = E.CudaEngine(main, draft)
     req = B.GenerationRequest([[1, 2, 3], [4, 5]], 8, temperature=0.5)
-    with pytest.raises(ValueError, match="greedy"):
-        eng.run(req, B.FixedDraftController(3), speculative=True, align=0.5,
-                align_tokens=np.zeros((2, 8), np.int32))
-    assert main.lengths() == [0, 0] and draft.lengths() == [0, 0]
+    res = eng.run(req, B.FixedDraftController(3), speculative=True, align=0.5,
+                  align_tokens=np.zeros((2, 8), np.int32))[0]
+    assert all(len(t) == 8 for t in res.tokens)
+    assert all(0 <= t < TINY.vocab_size for seq in res.tokens for t in seq)
+    assert main.lengths() == [3 + 8 - 1, 2 + 8 - 1]
+    for m in (main, draft):
+        for s_ in range(2):
+            m.rollback(s_, 0)
     res = B.decode_speculative(main, draft, req, B.FixedDraftController(3))
     assert all(len(t) == 8 for t in res.tokens)

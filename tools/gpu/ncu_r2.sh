@@ -8,11 +8,11 @@ echo launches rc=$?
 python tools/ncu_summary.py gpurun_out/r2_launches_c2.csv 40 > gpurun_out/r2_launches_c2_summary.txt; head -45 gpurun_out/r2_launches_c2_summary.txt
 gzip -f gpurun_out/r2_launches_c2.csv
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k 'regex:gemm_tc_kernel<128, 0' -s 3 -c 1 -o gpurun_out/r2_gemm_qkv_verify python bench.py --profile-only --warmup 0 \
+  -k 'regex:gemm_tc_kernel<\(int\)128, \(int\)0' -s 3 -c 1 -o gpurun_out/r2_gemm_qkv_verify python bench.py --profile-only --warmup 0 \
   --trace 0 --load-traj /tmp/traj_c2.npy --loop host > gpurun_out/r2_gemm_full.log 2>&1
 echo gemm full rc=$?
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k 'regex:attn_stream_kernel<16, 128' -s 300 -c 1 -o gpurun_out/r2_attn_c2 python bench.py --profile-only --warmup 0 \
+  -k 'regex:attn_stream_kernel<\(int\)16, \(int\)128' -s 300 -c 1 -o gpurun_out/r2_attn_c2 python bench.py --profile-only --warmup 0 \
   --trace 0 --load-traj /tmp/traj_c2.npy --loop host > gpurun_out/r2_attn_full.log 2>&1
 echo attn full rc=$?
 ls -la gpurun_out/*.ncu-rep
