@@ -380,7 +380,6 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
         };
         // capture the loop graph (once per request shape; again when a workspace moved)
         auto graph_capture = [&]() {
-            const int32_t* ident = (const int32_t*)(dbase + o_ident);
             const int max_len = std::min(e->cap, max_seq);
             struct Branch {
                 PlanArgs pa;
@@ -405,6 +404,7 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                     F.nq = stream_nq_for(qq);
                     F.stride = stream_items_per_seq(qq, max_len);
                     F.work = take((size_t)b * F.stride * 8);
+                    F.live = take(2);
                     Batch bt;
                     std::vector<int32_t> dummy(qq, 0);
                     for (int s = 0; s < b; ++s) {
@@ -420,6 +420,9 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                 for (int j = 1; j < nd; ++j) add_fwd(1, j, 1);
                 add_fwd(2, 0, l + 1);
                 for (int j = 0; j <= l; ++j) pa.pos[j] = take((size_t)b);
+                pa.perm = take((size_t)b);
+                pa.cperm = take((size_t)b);
+                pa.gperm = take((size_t)b);
                 arena_ints = std::max(arena_ints, off);
             }
             int32_t* ar = (int32_t*)e->looparena.need(arena_ints * 4 + 256, st);
@@ -504,13 +507,16 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                                                         cudaStreamCaptureModeRelaxed));
                 loop_plan_kernel<<<1, ((b + 31) / 32) * 32, 0, cs>>>(dS, ar, B.pa);
                 launched(c);
+                const int32_t* perm = ar + B.pa.perm;
+                const int32_t* cperm = ar + B.pa.cperm;
+                const int32_t* gperm = ar + B.pa.gperm;
                 for (int j = 0; j < nd; ++j) {
                     const PlanFwd& F = B.pa.f[j];
-                    PreMeta pm{ar + F.meta, ar + F.work, true, F.stride, max_len};
+                    PreMeta pm{ar + F.meta, ar + F.work, true, F.stride, max_len, ar + F.live, ar + F.live + 1};
                     float* out = dlog + (size_t)j * b * V;
                     forward(D, *e->kv_draft, B.bts[j], e->strategy, out, e->props(), e->pstride, &pm);
                     if (j == l) break;   // sampled bonus row: no pick
-                    DraftPick dp{ident, d_sid, ar + B.pa.pos[j], e->props(), e->pstride, j,
+                    DraftPick dp{perm, d_sid, ar + B.pa.pos[j], e->props(), e->pstride, j,
                                  r->align, r->align_seed, d_align, d_plen, maxnew};
                     ProfScope prof(c, BASS_PROF_SAMPLE, (double)b * V * 4);
                     if (greedy)
@@ -523,7 +529,7 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                 }
                 {
                     const PlanFwd& F = B.pa.f[nd];
-                    PreMeta pm{ar + F.meta, ar + F.work, true, F.stride, max_len};
+                    PreMeta pm{ar + F.meta, ar + F.work, true, F.stride, max_len, ar + F.live, ar + F.live + 1};
                     forward(M, *e->kv_main, B.bts[nd], e->strategy, vlog, e->props(), e->pstride, &pm);
                 }
                 {
@@ -533,7 +539,7 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                 }
                 launched(c);
                 if (!greedy) {
-                    VerifyArgs va{b, l, V, r->temperature, r->top_p, r->seed, ident, d_sid, hs.C,
+                    VerifyArgs va{b, l, V, r->temperature, r->top_p, r->seed, perm, d_sid, cperm,
                                   e->props(), e->pstride, vlog, dlog, scratch, accf, corr, btok};
                     ProfScope prof(c, BASS_PROF_SAMPLE, (double)R * V * 8);
                     cl_verify_shape_kernel<<<dim3((l + 1) * CL_CTAS, b, 2), CL_THREADS, 0, cs>>>(va, shp);
@@ -541,11 +547,11 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                     cl_verify_accept_kernel<<<dim3((l + 1) * CL_CTAS, b), CL_THREADS, 0, cs>>>(va, shp);
                     launched(c);
                 }
-                StepArgs sa{b, l, V, ident, hs.C, hs.ngen, e->props(), e->pstride, vlog, vamax, vlse,
+                StepArgs sa{b, l, V, perm, cperm, gperm, e->props(), e->pstride, vlog, vamax, vlse,
                             maxnew, r->eos_token, accf, corr, btok, greedy ? 1 : 0, step_dev, estride};
                 BASS_CUDA(launch_pdl(finalize_kernel, dim3((b + 63) / 64), dim3(64), 0, cs, sa));
                 launched(c);
-                BASS_CUDA(launch_pdl(loop_book_kernel, dim3(1), dim3(((b + 31) / 32) * 32), 0, cs, dS));
+                BASS_CUDA(launch_pdl(loop_book_kernel, dim3(1), dim3(((b + 31) / 32) * 32), 0, cs, dS, perm));
                 launched(c);
                 cudaGraph_t got = nullptr;
                 BASS_CUDA(cudaStreamEndCapture(cs, &got));
@@ -571,7 +577,9 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
         };
         // after the prompt step's finalize: book it, run the graph, one sync, read back
         auto graph_finish = [&]() {
-            BASS_CUDA(launch_pdl(loop_book_kernel, dim3(1), dim3(((b + 31) / 32) * 32), 0, st, dS));
+            // the prompt step's records are in slot order (every slot active)
+            BASS_CUDA(launch_pdl(loop_book_kernel, dim3(1), dim3(((b + 31) / 32) * 32), 0, st, dS,
+                                 (const int32_t*)(dbase + o_ident)));
             launched(c);
             const auto tq = clk::now();
             graph_capture();

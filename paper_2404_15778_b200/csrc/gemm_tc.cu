@@ -164,6 +164,7 @@ struct Split {
     int evict_first;   // weights streamed with an L2 evict-first policy
     const double* sx;  // int8 (W8A8): per-token activation scales [M]
     const double* sw;  // int8 (W8A8): per-channel weight scales [N]
+    const int32_t* m_dev;   // device-planned forward: rows beyond *m_dev are not live
 };
 
 // LayerNorm folded into the GEMM (XN):  LN(x) W^T = rstd * ((x*g) W^T - mean * c) + e
@@ -299,6 +300,11 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
     // HBM once and re-served from L2 to the other groups
     const int tile = blockIdx.z, split = blockIdx.y, group = blockIdx.x;
     const int n0 = tile * NB * BN, m0 = group * TT;
+    // device-planned forward (decode-loop graph): the live rows are known only
+    // on the device; a token group past them exits before touching anything
+    // (all CTAs of a split-K cluster share the group)
+    const int Mv = sp.m_dev ? min(M, __ldg(sp.m_dev)) : M;
+    if (m0 >= Mv) return;
     const int it0 = (int)((int64_t)split * sp.k_iters / sp.S);
     const int it1 = (int)((int64_t)(split + 1) * sp.k_iters / sp.S);
     const int nit = it1 - it0;
@@ -456,7 +462,7 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
     if (threadIdx.x == 64) GPROBE(5);
     fence_after();
     const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
-    const int rows = min(TT, M - m0);
+    const int rows = min(TT, Mv - m0);
     // W8A8: s32 accumulator bits -> acc * s_token * s_channel (fp64, ref:quant.py:119)
     auto deq = [&](int m, int n, float bits) -> float {
         if constexpr (I8) return (float)((double)__float_as_int(bits) * __ldg(sp.sx + m) * __ldg(sp.sw + n));
@@ -1133,7 +1139,7 @@ void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N
     if (si == S.splits.end())
         si = S.splits.emplace(sk, choose_splits(m.ctx->sm_count, N, i8 ? K / 2 : K, i8 ? 16 : 32)).first;
     // one token group: every weight byte is read once (prefill re-reads it per group from L2)
-    Split sp{si->second, i8 ? K / 128 : K / BK, nullptr, (packed && M <= TT) ? 1 : 0, sx, sw};
+    Split sp{si->second, i8 ? K / 128 : K / BK, nullptr, (packed && M <= TT) ? 1 : 0, sx, sw, m.dev_rows};
     // reduction loops and cluster size hold <= 8; every split owns >= 1 k block
     sp.S = std::max(1, std::min(std::min(MAX_S, sp.S), sp.k_iters));
     if (sp.S > 1) {

@@ -50,10 +50,12 @@ struct DevLoop {                      // device-resident generation state
 // position C - 2), 1 = draft forward j (1 row: proposal j - 1 at C + j - 1),
 // 2 = verify (l + 1 rows from C - 1); meta / work: arena offsets (int32)
 struct PlanFwd {
-    int kind, j, q, meta, work, stride, nq;
+    int kind, j, q, meta, work, stride, nq, live;   // live: arena offset of {m_act, r_act}
 };
 struct PlanArgs {
     int b, l, nf, strategy, ch, split_ch;
+    int perm, cperm, gperm;           // arena offsets: slot of sequence index i (active slots first),
+                                      // its committed length and generated count
     int pos[GL_MAXL + 1];             // arena offsets of the proposal positions (C + j) per draft j
     PlanFwd f[GL_MAXF];
 };
@@ -64,16 +66,33 @@ struct PlanArgs {
 // pre-wait loads of its work list see it.
 __global__ void __launch_bounds__(1024) loop_plan_kernel(const DevLoop* __restrict__ S, int32_t* __restrict__ ar,
                                                          PlanArgs a) {
-    __shared__ int cmax;
-    const int i = threadIdx.x, b = a.b;
-    if (i == 0) cmax = 0;
+    __shared__ int cmax, n_act;
+    __shared__ int16_t order[1024];
+    const int t = threadIdx.x, b = a.b;
+    // sequence order of the step: the active slots first (ascending), then the
+    // finished ones, so every forward's live rows are a prefix (GEMM token
+    // groups past it exit, the LM head stops there)
+    if (t == 0) {
+        int k = 0;
+        for (int s = 0; s < b; ++s)
+            if (!S->done[s]) order[k++] = (int16_t)s;
+        n_act = k;
+        for (int s = 0; s < b; ++s)
+            if (S->done[s]) order[k++] = (int16_t)s;
+        cmax = 0;
+    }
     __syncthreads();
-    const int C = i < b ? S->C[i] : 0;
-    const bool fin = i < b && S->done[i];
+    const int i = t;                                   // sequence index
+    const int slot = i < b ? order[i] : 0;
+    const int C = i < b ? S->C[slot] : 0;
+    const bool fin = i >= n_act;
     if (i < b && !fin) atomicMax(&cmax, C);   // PAD pads to the longest ACTIVE history
     __syncthreads();
     if (i >= b) return;
-    const int32_t* com = S->com + (size_t)i * S->com_cap;
+    ar[a.perm + i] = slot;
+    ar[a.cperm + i] = C;
+    ar[a.gperm + i] = S->ngen[slot];
+    const int32_t* com = S->com + (size_t)slot * S->com_cap;
     for (int f = 0; f < a.nf; ++f) {
         const PlanFwd F = a.f[f];
         const int q = F.q, M = b * q, n = b;
@@ -83,10 +102,14 @@ __global__ void __launch_bounds__(1024) loop_plan_kernel(const DevLoop* __restri
         for (int t = 0; t < q; ++t) {
             const int r = i * q + t;
             mt[r] = F.kind == 0 ? com[C - 2 + t] : F.kind == 1 ? -F.j : (t == 0 ? com[C - 1] : -t);
-            mt[M + r] = i;
+            mt[M + r] = slot;
             mt[2 * M + r] = off + t;
         }
-        mt[3 * M + i] = i;
+        if (i == 0) {
+            ar[F.live] = n_act * q;                        // live rows of the forward
+            ar[F.live + 1] = F.kind == 2 ? n_act * q : n_act;   // live logit rows
+        }
+        mt[3 * M + i] = slot;
         mt[3 * M + n + i] = i * q;
         mt[3 * M + 2 * n + i] = q;
         mt[3 * M + 3 * n + i] = off;
@@ -108,13 +131,13 @@ __global__ void __launch_bounds__(1024) loop_plan_kernel(const DevLoop* __restri
             const int nch = last / a.ch + 1;
             for (int s = 0; s * a.split_ch < nch && k < F.stride; ++s, ++k) {
                 int32_t* it = w + k * 8;
-                it[0] = i; it[1] = i * q; it[2] = q; it[3] = aoff;
+                it[0] = slot; it[1] = i * q; it[2] = q; it[3] = aoff;
                 it[4] = t0; it[5] = s; it[6] = min(a.split_ch, nch - s * a.split_ch); it[7] = min(aoff, safe);
             }
         }
         for (; k < F.stride; ++k) {   // idle padding (skipped by the attention's item loop)
             int32_t* it = w + k * 8;
-            it[0] = i; it[1] = i * q; it[2] = q; it[3] = off; it[4] = q; it[5] = 0; it[6] = 0; it[7] = 0;
+            it[0] = slot; it[1] = i * q; it[2] = q; it[3] = off; it[4] = q; it[5] = 0; it[6] = 0; it[7] = 0;
         }
     }
     for (int j = 0; j <= a.l; ++j) ar[a.pos[j] + i] = C + j;
@@ -125,11 +148,14 @@ __global__ void __launch_bounds__(1024) loop_plan_kernel(const DevLoop* __restri
 // rolled back to the committed prefix, forward-call counters, the step trace,
 // Algorithm 1 over the accepted counts of the slots active at the step start
 // (ref:draft_control.py:49-69), and the graph conditions for the next step.
-__global__ void __launch_bounds__(1024) loop_book_kernel(DevLoop* __restrict__ S) {
+// perm: the slot of each finalize record (the step's sequence order; the
+// prompt step's records are in slot order).
+__global__ void __launch_bounds__(1024) loop_book_kernel(DevLoop* __restrict__ S, const int32_t* __restrict__ perm) {
     __shared__ int mx, any_active, any_err, n_act;
     __shared__ long long dcalls;
     pdl_wait();
-    const int i = threadIdx.x, b = S->b, l = S->l, step = S->step;
+    const int q = threadIdx.x, b = S->b, l = S->l, step = S->step;
+    const int i = q < b ? perm[q] : q;   // this thread's slot
     if (i == 0) {
         mx = 0;
         any_active = 0;
@@ -141,7 +167,7 @@ __global__ void __launch_bounds__(1024) loop_book_kernel(DevLoop* __restrict__ S
     const unsigned long long now = gtimer();
     const bool tr = step < S->steps_cap;
     if (i < b && !S->done[i]) {
-        const char* rec = S->rec + (size_t)i * slot_rec_bytes(S->estride);
+        const char* rec = S->rec + (size_t)q * slot_rec_bytes(S->estride);
         const SlotStep& o = *reinterpret_cast<const SlotStep*>(rec);
         const int32_t* tok = slot_rec_tok(const_cast<char*>(rec));
         const double* lp = slot_rec_lp(const_cast<char*>(rec), S->estride);
@@ -186,7 +212,7 @@ __global__ void __launch_bounds__(1024) loop_book_kernel(DevLoop* __restrict__ S
     }
     __syncthreads();
     if (i < b && tr) S->tr_kv[(size_t)step * b + i] = S->C[i];
-    if (i != 0) return;
+    if (q != 0) return;
     S->main_calls += n_act;
     S->draft_calls += (long long)n_act * l + dcalls;
     if (tr) {

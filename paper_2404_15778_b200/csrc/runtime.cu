@@ -502,6 +502,13 @@ PreMetaOff forward_premeta(const bass_model& m, const Batch& b, int strategy, co
 void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* logits_out,
              const int32_t* proposals, int pstride, const PreMeta* pre) {
     bass_ctx* ctx = m.ctx;
+    // live-row bound of a device-planned forward, seen by every GEMM launch below
+    struct LiveRows {
+        bass_model& m;
+        ~LiveRows() { m.dev_rows = nullptr; }
+    } live_rows{m};
+    const bool devp = pre && pre->dev;
+    m.dev_rows = devp ? pre->m_act : nullptr;
     cudaStream_t st = ctx->stream;
     const bass_geometry& g = m.g;
     const int M = b.rows(), n_seq = (int)b.slot.size(), R = (int)b.logit_rows.size();
@@ -647,6 +654,7 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
         }
         if (R > 0) {
             ln_q(m.lnf_g, m.lnf_b, lrows, R);
+            m.dev_rows = devp ? pre->r_act : nullptr;
             gemm_i8(m, EPI_STORE, xq, xs, m.head, m.shead, R, V, d, so);
         }
         return;
@@ -732,6 +740,7 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
                 hst = cst;
             }
             const TcNorm nh{hst, hf, hf + V, nullptr, stat_tiles};
+            m.dev_rows = devp ? pre->r_act : nullptr;
             gemm(m, EPI_STORE, X, m.head, R, V, d, so, m.packed, &nh);
         } else if (R > 0) {
             launch_layernorm_any(m, x, lrows, m.lnf_g, m.lnf_b, R, hs);

@@ -155,6 +155,7 @@ struct bass_model {
     void* tc_state = nullptr;        // tcgen05 split-K GEMM descriptors (gemm_tc.cu)
     bass::DevBuf attn_work;          // stream-attention work list of the current forward
     bass::DevBuf xq, xs;             // BASS_INT8: per-token int8 GEMM input and its scales
+    const int32_t* dev_rows = nullptr;   // device-planned forward: live row count of the next GEMMs (PreMeta::m_act)
 };
 
 struct bass_kv {
@@ -194,6 +195,10 @@ struct PreMeta {
     // every history is shorter than max_len.
     bool dev = false;
     int work_stride = 0, max_len = 0;
+    // live rows of this forward (the active sequences come first): GEMM token
+    // groups past m_act exit at once, the LM head stops at r_act logit rows
+    const int32_t* m_act = nullptr;
+    const int32_t* r_act = nullptr;
 };
 struct PreMetaOff {
     size_t meta = 0, work = 0;       // offsets into the arena (int32 units, 32-byte aligned)
