@@ -78,6 +78,9 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     while (!mbar_try(bar, parity)) {
     }
@@ -270,7 +273,13 @@ __device__ int g_gp_n, g_gp_k;
 // I8: W8A8 — int8 packed weights and int8 activations (kind::i8, s32
 // accumulators), dequantized in the epilogue: acc * sx[m] * sw[n] in fp64
 // (ref:quant.py:98-123 int_gemm_dequant).  LNF must be 0.
-template <int TT, int MODE, int NB, bool PACKED, int LNF, bool I8 = false>
+// SER: serial split-K for prefill-sized M — one CTA per (token group, tile)
+// runs the S splits one after another, each into its own TMEM accumulator
+// (S x TT <= 512 columns), and the epilogue sums the S partials in split
+// order exactly as the cluster reduction does (same K partition, same
+// accumulation and summation order: bit-identical rows, no cluster
+// barriers, no partial exchange).
+template <int TT, int MODE, int NB, bool PACKED, int LNF, bool I8 = false, bool SER = false>
 __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tw,
                                                              const __grid_constant__ CUtensorMap tx,
                                                              const __nv_bfloat16* __restrict__ wpk, int M, int N,
@@ -292,6 +301,9 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
     // bars[0..S) full, [S..2S) empty, [2S] done; tmem base address after
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 1);
+    static_assert(!SER || NB == 1, "serial split-K: one 128-row sub-tile");
+    // SER: one accumulator per split (the host keeps S x TT <= 512)
+    const uint32_t tcols = SER ? (sp.S * TT <= 256 ? 256u : 512u) : (uint32_t)C::TMEM_COLS;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wq = warp & 3, half = warp >> 2;   // epilogue: TMEM lane quarter, row half
@@ -305,8 +317,8 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
     // (all CTAs of a split-K cluster share the group)
     const int Mv = sp.m_dev ? min(M, __ldg(sp.m_dev)) : M;
     if (m0 >= Mv) return;
-    const int it0 = (int)((int64_t)split * sp.k_iters / sp.S);
-    const int it1 = (int)((int64_t)(split + 1) * sp.k_iters / sp.S);
+    const int it0 = SER ? 0 : (int)((int64_t)split * sp.k_iters / sp.S);
+    const int it1 = SER ? sp.k_iters : (int)((int64_t)(split + 1) * sp.k_iters / sp.S);
     const int nit = it1 - it0;
 
     if (threadIdx.x == 0) {
@@ -322,7 +334,7 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
-                     "r"(C::TMEM_COLS)
+                     "r"(tcols)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -378,27 +390,36 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
     } else if (warp == 1) {
         if (lane == 0) {   // ---- MMA issuer: one accumulator (TT columns) per sub-tile
             constexpr uint32_t ID = I8 ? idesc_i8(TT) : idesc(TT);
+            int ps = 0;                                                  // SER: current split
+            int pb0 = 0, pb1 = SER ? (int)((int64_t)sp.k_iters / sp.S) : nit;   // its k-block range
             for (int i = 0; i < nit; ++i) {
                 const int s = i % C::STAGES;
+                const bool first = i == pb0;
                 mbar_wait(su32(&bars[s]), (i / C::STAGES) & 1);
                 if (i == 0) GPROBE(2);
                 fence_after();
                 const uint32_t st = base + s * C::STAGE;
                 const uint64_t b = sdesc(st + C::W_BYTES);
+                const uint32_t dacc = tmem + (SER ? (uint32_t)(ps * TT) : 0u);
 #pragma unroll
                 for (int sub = 0; sub < NB; ++sub) {
                     const uint64_t a = sdesc(st + sub * BN * BK * 2);
 #pragma unroll
                     for (int kk = 0; kk < BK / UK; ++kk) {   // +32 bytes per UMMA_K step inside the swizzle row
                         if constexpr (I8)
-                            umma_i8(tmem + sub * TT, a + (uint64_t)(kk * 2), b + (uint64_t)(kk * 2), ID,
-                                    (i > 0 || kk > 0) ? 1u : 0u);
+                            umma_i8(dacc + sub * TT, a + (uint64_t)(kk * 2), b + (uint64_t)(kk * 2), ID,
+                                    (!first || kk > 0) ? 1u : 0u);
                         else
-                            umma(tmem + sub * TT, a + (uint64_t)(kk * 2), b + (uint64_t)(kk * 2), ID,
-                                 (i > 0 || kk > 0) ? 1u : 0u);
+                            umma(dacc + sub * TT, a + (uint64_t)(kk * 2), b + (uint64_t)(kk * 2), ID,
+                                 (!first || kk > 0) ? 1u : 0u);
                     }
                 }
                 umma_commit(su32(&bars[C::STAGES + s]));
+                if (SER && i == pb1 - 1) {   // split ps complete: the next one starts a fresh accumulator
+                    ++ps;
+                    pb0 = pb1;
+                    pb1 = (int)((int64_t)(ps + 1) * sp.k_iters / sp.S);
+                }
             }
             umma_commit(su32(&bars[2 * C::STAGES]));
             GPROBE(3);
@@ -463,6 +484,25 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
     fence_after();
     const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
     const int rows = min(TT, Mv - m0);
+    // the finished accumulator chunk of token columns [c0, c0 + 16): TMEM, or
+    // for SER the S per-split accumulators summed in split order (the cluster
+    // reduction's order: 0 + p0 + p1 + ...; s32 partials as integers)
+    auto acc_chunk = [&](int sub, int c0, float* v) {
+        if constexpr (SER) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = 0.f;
+            for (int s2 = 0; s2 < sp.S; ++s2) {
+                float p[16];
+                tmem_ld16(trow + (uint32_t)(s2 * TT) + c0, p);
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    v[j] = I8 ? __int_as_float(__float_as_int(v[j]) + __float_as_int(p[j])) : v[j] + p[j];
+            }
+        } else {
+            tmem_ld16(trow + sub * TT + c0, v);
+        }
+    };
+    const bool direct = SER || sp.S == 1;   // no cross-CTA reduction in the epilogue
     // W8A8: s32 accumulator bits -> acc * s_token * s_channel (fp64, ref:quant.py:119)
     auto deq = [&](int m, int n, float bits) -> float {
         if constexpr (I8) return (float)((double)__float_as_int(bits) * __ldg(sp.sx + m) * __ldg(sp.sw + n));
@@ -531,7 +571,7 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
         }
     };
     if constexpr (LNF == 0) {
-    if (sp.S == 1) {
+    if (direct) {
 #pragma unroll
         for (int sub = 0; sub < NB; ++sub) {
             const int n = n0 + sub * BN + wq * 32 + lane;
@@ -539,7 +579,7 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
             for (int c0 = half * 16; c0 < TT; c0 += 16 * EH) {
                 if (c0 >= rows) break;
                 float v[16];
-                tmem_ld16(trow + sub * TT + c0, v);
+                acc_chunk(sub, c0, v);
                 if (n < N) {
                     if constexpr (QQ) {
                         float w[16];
@@ -787,7 +827,7 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
                 make_float2((a.x + b.x) + (c2.x + d.x), (a.y + b.y) + (c2.y + d.y));
         }
     };
-    if (sp.S == 1) {
+    if (direct) {
         red = reinterpret_cast<float2*>(smem);
 #pragma unroll
         for (int sub = 0; sub < NB; ++sub) {
@@ -796,7 +836,7 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
             for (int c0 = half * 16; c0 < TT; c0 += 16 * EH) {
                 if (c0 >= rows) break;
                 float v[16];
-                tmem_ld16(trow + sub * TT + c0, v);
+                acc_chunk(sub, c0, v);
 #pragma unroll
                 for (int j0 = 0; j0 < 16; j0 += 4) {
                     float nv[4] = {0.f, 0.f, 0.f, 0.f};
@@ -925,7 +965,7 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
     fence_before();
     __syncthreads();
     if (warp == 2)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols)
                      : "memory");
     if (threadIdx.x == 64) GPROBE(11);
     if (tr.buf && threadIdx.x == 0) {   // trace record index: linear block id
@@ -1026,17 +1066,17 @@ struct LaunchArgs {
     XNorm xn;
 };
 
-template <int TT, int MODE, bool PACKED, int LNF, bool I8 = false>
+template <int TT, int MODE, bool PACKED, int LNF, bool I8 = false, bool SER = false>
 static void launch_k(bass_model& m, const LaunchArgs& a, const Epi& e) {
     constexpr int NB = 1;   // (NB = 2 measured slower at every benchmark shape: profiles/r1_gemm_nb_split_sweep.txt)
     using C = Cfg<TT, NB>;
     static unsigned attr = 0;
     once_per_device(attr, [] {
-        BASS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<TT, MODE, NB, PACKED, LNF, I8>,
+        BASS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<TT, MODE, NB, PACKED, LNF, I8, SER>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     });
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((a.M + TT - 1) / TT, a.sp.S, (a.N + NB * BN - 1) / (NB * BN));
+    cfg.gridDim = dim3((a.M + TT - 1) / TT, SER ? 1 : a.sp.S, (a.N + NB * BN - 1) / (NB * BN));
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = m.ctx->stream;
@@ -1048,45 +1088,45 @@ static void launch_k(bass_model& m, const LaunchArgs& a, const Epi& e) {
     at[1].val.clusterDim.y = a.sp.S;
     at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
-    cfg.numAttrs = a.sp.S > 1 ? 2 : 1;
+    cfg.numAttrs = (a.sp.S > 1 && !SER) ? 2 : 1;
     const int nblk = (int)(cfg.gridDim.x * cfg.gridDim.y * cfg.gridDim.z);
-    BASS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TT, MODE, NB, PACKED, LNF, I8>, *a.wm, *a.xm,
+    BASS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TT, MODE, NB, PACKED, LNF, I8, SER>, *a.wm, *a.xm,
                                  (const __nv_bfloat16*)a.W, a.M, a.N, a.sp, e, a.xn,
                                  m.ctx->trace(nblk, BASS_TR_GEMM)));
 }
 
-template <int TT>
+template <int TT, bool SER = false>
 static void launch_mode(bass_model& m, int mode, bool packed, bool xn, const LaunchArgs& a, const Epi& e) {
     if (a.sp.sx) {   // W8A8 (packed int8 weights): plain epilogues after the dequantization
         if (!packed || xn) throw Error(BASS_ERR_STATE, "int8 GEMM: packed weights, no folded LayerNorm");
         if ((mode == EPI_QKV || mode == EPI_GELU) && (a.N % 128 != 0 || (mode == EPI_GELU && !e.amax)))
             throw Error(BASS_ERR_STATE, "int8 QKV / GELU epilogues: N % 128 == 0 (GELU: with its amax buffer)");
-        if (mode == EPI_RESID) launch_k<TT, EPI_RESID, true, 0, true>(m, a, e);
-        else if (mode == EPI_STORE) launch_k<TT, EPI_STORE, true, 0, true>(m, a, e);
-        else if (mode == EPI_QKV) launch_k<TT, EPI_QKV, true, 0, true>(m, a, e);
-        else launch_k<TT, EPI_GELU, true, 0, true>(m, a, e);
+        if (mode == EPI_RESID) launch_k<TT, EPI_RESID, true, 0, true, SER>(m, a, e);
+        else if (mode == EPI_STORE) launch_k<TT, EPI_STORE, true, 0, true, SER>(m, a, e);
+        else if (mode == EPI_QKV) launch_k<TT, EPI_QKV, true, 0, true, SER>(m, a, e);
+        else launch_k<TT, EPI_GELU, true, 0, true, SER>(m, a, e);
         return;
     }
     if (!packed) {   // raw [N, K] pointers (bass_gemm): plain fp32 store
         if (mode != EPI_STORE || xn) throw Error(BASS_ERR_STATE, "tcgen05 GEMM: fused epilogues need packed weights");
-        launch_k<TT, EPI_STORE, false, 0>(m, a, e);
+        launch_k<TT, EPI_STORE, false, 0, false, SER>(m, a, e);
         return;
     }
     if (xn) {   // LayerNorm folded in: the two projections that follow a LayerNorm
-        if (mode == EPI_QKV) launch_k<TT, EPI_QKV, true, 1>(m, a, e);
-        else if (mode == EPI_GELU) launch_k<TT, EPI_GELU, true, 1>(m, a, e);
-        else if (mode == EPI_STORE) launch_k<TT, EPI_STORE, true, 1>(m, a, e);   // head (final LayerNorm)
+        if (mode == EPI_QKV) launch_k<TT, EPI_QKV, true, 1, false, SER>(m, a, e);
+        else if (mode == EPI_GELU) launch_k<TT, EPI_GELU, true, 1, false, SER>(m, a, e);
+        else if (mode == EPI_STORE) launch_k<TT, EPI_STORE, true, 1, false, SER>(m, a, e);   // head (final LayerNorm)
         else throw Error(BASS_ERR_STATE, "tcgen05 GEMM: folded LayerNorm only for QKV / FC / head");
         return;
     }
     switch (mode) {
-        case EPI_QKV: launch_k<TT, EPI_QKV, true, 0>(m, a, e); break;
+        case EPI_QKV: launch_k<TT, EPI_QKV, true, 0, false, SER>(m, a, e); break;
         case EPI_RESID:
-            if (e.stats) launch_k<TT, EPI_RESID, true, 2>(m, a, e);   // emits the next LayerNorm's inputs
-            else launch_k<TT, EPI_RESID, true, 0>(m, a, e);
+            if (e.stats) launch_k<TT, EPI_RESID, true, 2, false, SER>(m, a, e);   // emits the next LayerNorm's inputs
+            else launch_k<TT, EPI_RESID, true, 0, false, SER>(m, a, e);
             break;
-        case EPI_GELU: launch_k<TT, EPI_GELU, true, 0>(m, a, e); break;
-        default: launch_k<TT, EPI_STORE, true, 0>(m, a, e); break;
+        case EPI_GELU: launch_k<TT, EPI_GELU, true, 0, false, SER>(m, a, e); break;
+        default: launch_k<TT, EPI_STORE, true, 0, false, SER>(m, a, e); break;
     }
 }
 
@@ -1142,13 +1182,27 @@ void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N
     Split sp{si->second, i8 ? K / 128 : K / BK, nullptr, (packed && M <= TT) ? 1 : 0, sx, sw, m.dev_rows};
     // reduction loops and cluster size hold <= 8; every split owns >= 1 k block
     sp.S = std::max(1, std::min(std::min(MAX_S, sp.S), sp.k_iters));
-    if (sp.S > 1) {
+    // prefill-sized M (more than two 128-row token groups): serial split-K —
+    // the same K partition and summation order, so the rows' bits do not
+    // change, without the split clusters (whose per-CTA tails dominate there)
+    const bool ser = sp.S > 1 && sp.S <= 4 && M > 256 && packed;
+    if (ser) {
+        TT = sp.S <= 4 ? 128 : 64;   // S accumulators of TT columns in 512 TMEM columns
+        const auto xk2 = std::make_tuple(X, M, i8 ? -K : K, TT);
+        auto x2 = S.xmaps.find(xk2);
+        if (x2 == S.xmaps.end()) x2 = S.xmaps.emplace(xk2, make_map(X, M, K, TT, i8)).first;
+        xm = &x2->second;
+    }
+    if (sp.S > 1 && !ser) {
         const size_t blocks = (size_t)((N + NB * BN - 1) / (NB * BN)) * ((M + TT - 1) / TT);
         sp.ws = (float*)S.ws.need(blocks * sp.S * TT * NB * BN * 4, m.ctx->stream);
     }
     LaunchArgs a{wm, xm, W, M, N, sp, xn};
     const bool xnb = norm != nullptr;
-    switch (TT) {
+    if (ser) {
+        if (TT == 128) launch_mode<128, true>(m, mode, packed, xnb, a, e);
+        else launch_mode<64, true>(m, mode, packed, xnb, a, e);
+    } else switch (TT) {
         case 16: launch_mode<16>(m, mode, packed, xnb, a, e); break;
         case 32: launch_mode<32>(m, mode, packed, xnb, a, e); break;
         case 64: launch_mode<64>(m, mode, packed, xnb, a, e); break;

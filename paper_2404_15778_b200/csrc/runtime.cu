@@ -1357,19 +1357,34 @@ int bass_int_gemm_dequant(bass_ctx* c, int M, int N, int K, const int8_t* a, con
 int bass_gemm(bass_model* m, int mode, int M, int N, int K, const void* x, const void* w, float* y) {
     return guarded(m->ctx, [&] {
         BASS_REQUIRE(M >= 1 && N >= 1 && K >= 1, "geometry: GEMM sizes must be positive");
-        BASS_REQUIRE(mode == BASS_GEMM_SIMT || mode == BASS_GEMM_TC, "gemm mode must be SIMT or TC");
+        BASS_REQUIRE(mode == BASS_GEMM_SIMT || mode == BASS_GEMM_TC || mode == 3,
+                     "gemm mode must be SIMT, TC or 3 (TC on a packed copy)");
+        // mode 3: the weights repacked into the model layout first — the
+        // forward's own path (incl. the serial split-K kernel for M > 256)
+        const bool packed = mode == 3;
+        void* wp = nullptr;
+        if (packed) {
+            BASS_REQUIRE(m->dtype == BASS_BF16 && K % 64 == 0, "packed GEMM: bf16, K % 64 == 0");
+            BASS_CUDA(cudaMalloc(&wp, (size_t)packed_rows(N) * K * 2));
+            BASS_CUDA(cudaMemsetAsync(wp, 0, (size_t)packed_rows(N) * K * 2, m->ctx->stream));
+            pack_weights(m->ctx->stream, w, wp, N, K, 1);
+            w = wp;
+            mode = BASS_GEMM_TC;
+        }
         const int saved = m->gemm_mode;
         m->gemm_mode = mode;
         Epi e{};
         e.out = y;
         try {
-            gemm(*m, EPI_STORE, x, w, M, N, K, e, false);
+            gemm(*m, EPI_STORE, x, w, M, N, K, e, packed);
         } catch (...) {
             m->gemm_mode = saved;
+            if (wp) cudaFree(wp);
             throw;
         }
         m->gemm_mode = saved;
         m->ctx->sync();
+        if (wp) cudaFree(wp);
     });
 }
 
