@@ -141,8 +141,10 @@ int bass_forward_ragged(bass_model* m, bass_kv* kv, int n_seq,
 
 /* Standalone projection GEMM with the forward's kernels (tests / microbench):
  * Y[M, N] (fp32) = X[M, K] . W[N, K]^T with X, W in the model's dtype, all
- * device pointers; gemm_mode BASS_GEMM_SIMT or BASS_GEMM_TC (tcgen05).
- * ref:model.py:160-164 (_linear), output-major weights. */
+ * device pointers; gemm_mode BASS_GEMM_SIMT, BASS_GEMM_TC (tcgen05 on the raw
+ * [N, K] weights) or 3 (tcgen05 on a copy repacked into the model's packed
+ * tile layout — the forward's own path, incl. the serial split-K kernel for
+ * M > 256).  ref:model.py:160-164 (_linear), output-major weights. */
 int bass_gemm(bass_model* m, int gemm_mode, int M, int N, int K,
               const void* x_dev, const void* w_dev, float* y_dev);
 /* Integer-accumulate GEMM with the fused dequantizing epilogue

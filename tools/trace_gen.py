@@ -151,6 +151,15 @@ def analyse(rec):
     for l in launches[mid: mid + 24]:
         print(f"{l['cls']:8s} grid={l['grid']:4d} sms={l['sms']:3d} max/SM={l['maxper']}  start {l['s0'] - base:8.2f}..{l['s1'] - base:8.2f}"
               f"  end {l['e0'] - base:8.2f}..{l['e1'] - base:8.2f}  span {l['e1'] - l['s0']:7.2f}")
+    # a draft-model token in the middle (its attention launches have the smaller grid)
+    dmid = next((i for i in range(len(launches) // 2, len(launches))
+                 if launches[i]["cls"] == "attn" and launches[i]["grid"] != gmax), None)
+    if dmid is not None:
+        print("\ndraft timeline (us, relative):")
+        base = launches[dmid]["s0"]
+        for l in launches[dmid: dmid + 22]:
+            print(f"{l['cls']:8s} grid={l['grid']:4d} sms={l['sms']:3d} max/SM={l['maxper']}  start {l['s0'] - base:8.2f}..{l['s1'] - base:8.2f}"
+                  f"  end {l['e0'] - base:8.2f}..{l['e1'] - base:8.2f}  span {l['e1'] - l['s0']:7.2f}")
 
 
 if __name__ == "__main__":
