@@ -178,3 +178,17 @@ def test_sampled_point_mass_harness_device_equals_host(B, models):
     _same(host, dev)
     acc = [a for s in dev[0].steps for a in s.accepted]
     assert sum(acc) > 0   # the random-init draft alone is never accepted
+
+
+@pytest.mark.parametrize("b,new", [(1, 20), (40, 12), (3, 1), (3, 2)])
+def test_device_loop_edge_batches_and_lengths(B, models, b, new):
+    """b = 1 and b = 40 (several warps in the plan / book kernels), a
+    generation that ends in the prompt step (the graph runs zero iterations)
+    and one that ends right after it."""
+    wm, wd = models
+    prompts = _prompts(b, 2048, 11 + b)
+    req = B.GenerationRequest(prompts, new, temperature=0.0)
+    host = _run(B, wm, wd, req, B.AdaptiveDraftController(), "host")
+    dev = _run(B, wm, wd, req, B.AdaptiveDraftController(), "device")
+    _same(host, dev)
+    assert all(len(t) == new for t in dev[0].tokens)
