@@ -300,7 +300,7 @@ def main():
     ap.add_argument("--trace", type=int, default=1, help="traced generation for the in-chain roofline (0: off)")
     ap.add_argument("--trace-records", type=int, default=6 << 20)
     ap.add_argument("--split", action="append", default=[],
-                    help="split-K override NxK:S for a main-model projection shape (tuning)")
+                    help="split-K override NxK:S for a projection shape of either model (tuning)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.align is None:
@@ -327,10 +327,11 @@ def main():
     gm = {"auto": L.GEMM_AUTO, "simt": L.GEMM_SIMT, "tc": L.GEMM_TC}[args.gemm]
     wm.set_gemm(gm)
     wd.set_gemm(gm)
-    for ov in args.split:
+    for ov in args.split:   # NxK:S — applied to whichever model has that projection shape
         nk, sp = ov.split(":")
         n_, k_ = nk.split("x")
         wm.set_split(int(n_), int(k_), int(sp))
+        wd.set_split(int(n_), int(k_), int(sp))
     from paper_2404_15778_b200.shard import gather_tokens, global_sequence_ids, reduce_run
     # sequence-sharded: a rank owns a contiguous range of global sequences;
     # prompts and RNG keys derive from the global id, so outputs are

@@ -5,3 +5,5 @@ import json,sys; d=json.loads(sys.stdin.read()); print('[$*]', round(d['per_seq_
 run --dtype int8
 for s in 1 2 4; do run --dtype int8 --split 18432x4608:$s; done
 for a in 1.0 0.874 0.0; do for lp in device host; do run --align $a --loop $lp; done; done
+# draft-model split counts in the real chain (profiles/r2/draft_split_sweep.txt: the defaults are the optimum)
+for ov in 2048x2048:4 2048x8192:4 8192x2048:2 6144x2048:2 6144x2048:8; do run --split $ov; done
