@@ -143,3 +143,15 @@ def test_cli_generate_writes_report(B, tmp_path):
     assert cli.main(["generate", "--config", str(cfgp), "--out", str(tmp_path / "o"), "--dtype", "fp32"]) == 0
     rec = json.loads((tmp_path / "o" / "report.jsonl").read_text().splitlines()[0])
     assert rec["greedy_exact_match"] is True
+
+
+def test_quant_enabled_run_is_the_int8_path(B):
+    """ref:bench.py:85, 162-173 (`quant_enabled`): both providers on the INT8
+    W8A8 path; greedy speculative == greedy regular in the report."""
+    from paper_2404_15778_b200 import report as R
+    main = dict(TINY_MAIN, d_model=128, vocab_size=256)
+    conf = tiny_config(temperature=0.0, draft={"alignment": 1.0}, dtype="bf16", quant_enabled=True, main=main)
+    assert conf.device_dtype == "int8"
+    report = R.run_generate(conf, write=False)
+    assert report["greedy_exact_match"] is True
+    assert report["quant_enabled"] is True and report["dtype"] == "int8"
