@@ -63,6 +63,7 @@ struct bass_engine {
     LoopGraph lg;
     int64_t graph_builds = 0;
     int last_mode = BASS_LOOP_HOST, last_syncs = 0;
+    std::string graph_fallback;       // why the last generation fell back to the host loop ("" if it did not)
     char* loop_host = nullptr;        // pinned read-back of the device loop state
     size_t loop_host_cap = 0;
 };
@@ -322,7 +323,7 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
         // the host and enqueued as usual, its outcome booked on the device, and
         // every later step runs from one CUDA graph; one synchronisation per
         // generation
-        const bool use_graph = e->loop_mode == BASS_LOOP_DEVICE && model_uses_stream_attention(M) &&
+        bool use_graph = e->loop_mode == BASS_LOOP_DEVICE && model_uses_stream_attention(M) &&
                                model_uses_stream_attention(D) && !c->profile && !c->trace_buf &&
                                limit <= GL_MAXL && b <= 1024;
         e->last_mode = use_graph ? BASS_LOOP_DEVICE : BASS_LOOP_HOST;
@@ -450,14 +451,23 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
             // prompt step); every launch helper uses ctx->stream
             cudaStream_t cs;
             BASS_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-            struct Restore {
+            struct Restore {   // also on an exception: end a dangling capture, drop the partial graph
                 bass_ctx* c;
                 cudaStream_t st, cs;
+                LoopGraph& g;
+                bool ok = false;
                 ~Restore() {
+                    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+                    if (cudaStreamIsCapturing(cs, &cst) == cudaSuccess && cst != cudaStreamCaptureStatusNone) {
+                        cudaGraph_t dangling = nullptr;
+                        cudaStreamEndCapture(cs, &dangling);
+                    }
                     c->stream = st;
                     cudaStreamDestroy(cs);
+                    if (!ok) g.reset();
+                    cudaGetLastError();
                 }
-            } restore{c, st, cs};
+            } restore{c, st, cs, G};
             c->stream = cs;
             BASS_CUDA(cudaGraphCreate(&G.graph, 0));
             cudaGraphConditionalHandle h_loop, h_len;
@@ -571,6 +581,7 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
             }
             (void)n_cond;
             BASS_CUDA(cudaGraphInstantiate(&G.exec, G.graph, 0));
+            restore.ok = true;
             key[k_epoch] = (double)devbuf_epoch();   // (moves only when a workspace grew while capturing)
             G.key = key;
             ++e->graph_builds;
@@ -682,7 +693,19 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
         // residual) rolls both caches back to the committed prefix first, so
         // the providers stay usable (ref:engine.py:358-360 invariant)
         try {
-            if (use_graph) graph_setup();
+            if (use_graph) {
+                graph_setup();
+                // capture (or reuse) the loop graph before the prompt step, so a
+                // driver without conditional graph nodes falls back to the host
+                // loop before any step is committed to the device path
+                try {
+                    graph_capture();
+                } catch (const Error& ex) {
+                    use_graph = false;
+                    e->last_mode = BASS_LOOP_HOST;
+                    e->graph_fallback = ex.what();
+                }
+            }
             while (true) {
                 std::vector<int> A;
                 for (int s = 0; s < b; ++s)
