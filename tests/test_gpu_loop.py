@@ -150,16 +150,15 @@ def test_graph_reused_across_generations_and_rebuilt_on_change(B, models):
     assert eng.loop_info()["graph_builds"] == builds + 1   # eos is baked into the finalize kernel
 
 
-def test_int8_device_loop_equals_host(B):
-    g = OR.Geometry(2, 2, 256, 128, 1024, 256)
+@pytest.mark.parametrize("temperature,strategy", [(0.0, "ragged"), (0.7, "ragged"), (0.7, "split"), (0.0, "pad")])
+def test_int8_device_loop_equals_host(B, temperature, strategy):
     cfg = B.ModelConfig(2, 2, 256, 128, 1024, 256)
     wm = B.DeviceWeights.init_model(cfg, 6, "int8")
     prompts = _prompts(3, 1024, 6)
-    req = B.GenerationRequest(prompts, 24, temperature=0.0)
-    host = _run(B, wm, wm, req, B.AdaptiveDraftController(), "host")
-    dev = _run(B, wm, wm, req, B.AdaptiveDraftController(), "device")
+    req = B.GenerationRequest(prompts, 24, temperature=temperature, top_p=0.9, seed=5)
+    host = _run(B, wm, wm, req, B.AdaptiveDraftController(), "host", strategy)
+    dev = _run(B, wm, wm, req, B.AdaptiveDraftController(), "device", strategy)
     _same(host, dev)
-    del g
 
 
 def test_sampled_point_mass_harness_device_equals_host(B, models):
