@@ -694,6 +694,8 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
         // the providers stay usable (ref:engine.py:358-360 invariant)
         try {
             if (use_graph) {
+                forward_prepare(M);
+                forward_prepare(D);
                 graph_setup();
                 // capture (or reuse) the loop graph before the prompt step, so a
                 // driver without conditional graph nodes falls back to the host

@@ -294,6 +294,12 @@ __global__ void head_gather_kernel(const __nv_bfloat16* __restrict__ xb, const f
     for (int t = threadIdx.x; t < tiles; t += blockDim.x) so[(int64_t)t * R + r] = st[(int64_t)t * M + src];
 }
 
+// the bf16 forward folds every LayerNorm into the following GEMM (see forward())
+static bool uses_ln_fold(const bass_model& m) {
+    return m.dtype == BASS_BF16 && m.packed && m.gemm_mode != BASS_GEMM_SIMT && tc_gemm_supported(m, m.g.d_model, m.g.d_model) &&
+           m.g.d_model % 8 == 0;
+}
+
 static void ln_fold_prepare(bass_model& m) {
     if (m.lnfold_valid) return;
     const int d = m.g.d_model, L = m.g.n_layer;
@@ -499,6 +505,10 @@ PreMetaOff forward_premeta(const bass_model& m, const Batch& b, int strategy, co
     return o;
 }
 
+void forward_prepare(bass_model& m) {
+    if (uses_ln_fold(m)) ln_fold_prepare(m);
+}
+
 void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* logits_out,
              const int32_t* proposals, int pstride, const PreMeta* pre) {
     bass_ctx* ctx = m.ctx;
@@ -672,12 +682,20 @@ void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* lo
     // exact mean of the stream it normalised (K + mean(x - K)), which is the
     // shift the following residual GEMM centres on (the mean of the stream it
     // adds into).
-    const bool lnfuse = m.dtype == BASS_BF16 && m.packed && m.gemm_mode != BASS_GEMM_SIMT &&
-                        tc_gemm_supported(m, d, d) && d % 8 == 0;
+    const bool lnfuse = uses_ln_fold(m);
     const int stat_tiles = (d + 127) / 128;
     const bool headfold = tc_gemm_supported(m, V, d);
     float *lstats = nullptr, *kmean = nullptr;
     if (lnfuse) {
+        if (!m.lnfold_valid) {
+            // lazily computed per weight upload; never inside a stream capture
+            // (forward_prepare runs it first), or the constants would be computed
+            // only when the captured graph replays
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            BASS_CUDA(cudaStreamIsCapturing(st, &cs));
+            if (cs != cudaStreamCaptureStatusNone)
+                throw Error(BASS_ERR_STATE, "folded-LayerNorm constants missing while capturing (forward_prepare)");
+        }
         ln_fold_prepare(m);
         const size_t slot = (size_t)stat_tiles * (M + R) * 2;   // + gathered head rows
         lstats = (float*)m.lnstats.need((slot + (size_t)M) * 4, st);

@@ -217,6 +217,10 @@ inline PreMeta premeta_at(const int32_t* dev_arena, const PreMetaOff& o) {
 // int8 models, d_head 64 or 128): the precondition of device-planned forwards
 bool model_uses_stream_attention(const bass_model& m);
 
+// the model's lazily computed per-upload state (folded-LayerNorm constants),
+// on the context stream; call before capturing forwards into a CUDA graph
+void forward_prepare(bass_model& m);
+
 // Run `b` through model m over cache kv; logits [logit_rows, V] fp32 -> logits_out (device).
 // `pre`: metadata already on the device (forward_premeta + one upload).
 void forward(bass_model& m, bass_kv& kv, const Batch& b, int strategy, float* logits_out,

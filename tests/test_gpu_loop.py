@@ -191,3 +191,19 @@ def test_device_loop_edge_batches_and_lengths(B, models, b, new):
     dev = _run(B, wm, wd, req, B.AdaptiveDraftController(), "device")
     _same(host, dev)
     assert all(len(t) == new for t in dev[0].tokens)
+
+
+def test_fresh_weights_first_use_in_the_device_loop(B):
+    """Weights whose lazily computed state (the folded-LayerNorm constants)
+    has never been built: the device loop prepares it before capturing its
+    graph (a capture would otherwise record the preparation instead of running
+    it).  Each run gets its own fresh upload."""
+    def fresh(seed):
+        return B.DeviceWeights.from_reference(OR.init_weights(OR.Geometry(2, 4, 512, 128, 1000, 256), seed), "bf16")
+    prompts = _prompts(6, 1000, 21)
+    req = B.GenerationRequest(prompts, 16, temperature=0.0)
+    host = _run(B, fresh(41), fresh(42), req, B.AdaptiveDraftController(), "host")
+    dev = _run(B, fresh(41), fresh(42), req, B.AdaptiveDraftController(), "device")
+    _same(host, dev)
+    reg = B.decode_regular(B.CudaModel(fresh(41), 6), req)
+    assert dev[0].tokens == reg.tokens
