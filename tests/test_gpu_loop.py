@@ -207,3 +207,18 @@ def test_fresh_weights_first_use_in_the_device_loop(B):
     _same(host, dev)
     reg = B.decode_regular(B.CudaModel(fresh(41), 6), req)
     assert dev[0].tokens == reg.tokens
+
+
+def test_sampled_with_eos_device_equals_host(B, models):
+    """Sampled decoding that stops on an EOS token inside accepted blocks,
+    corrections and bonus tokens (ref:engine.py:103-117 finalize rules)."""
+    wm, _ = models
+    prompts = _prompts(5, 2048, 31)
+    base = B.GenerationRequest(prompts, 40, temperature=0.9, top_p=0.95, seed=3)
+    free = _run(B, wm, wm, base, B.AdaptiveDraftController(), "host")[0]
+    eos = free.tokens[0][5]
+    req = B.GenerationRequest(prompts, 40, temperature=0.9, top_p=0.95, seed=3, eos_token=eos)
+    host = _run(B, wm, wm, req, B.AdaptiveDraftController(), "host")
+    dev = _run(B, wm, wm, req, B.AdaptiveDraftController(), "device")
+    _same(host, dev)
+    assert "eos" in dev[0].finish_reason
