@@ -484,7 +484,9 @@ static __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_THRE
     __shared__ ClSmem sm;
     pdl_trigger();
     pdl_wait();
-    const int j = blockIdx.x / CL_CTAS, i = blockIdx.y, z = blockIdx.z, l = a.l;
+    const int l = a.l, i = blockIdx.y;
+    const int j = (a.phase == 2 ? l : 0) + blockIdx.x / CL_CTAS, z = a.phase == 2 ? 1 : blockIdx.z;
+    if (a.phase == 1 && z == 1 && j == l) return;   // the bonus draft row comes later (whole cluster)
     Cl cl(sm, a.V);
     const int64_t r = (int64_t)i * (l + 1) + j;
     const float* row = z == 0 ? a.vlog + r * a.V : a.dlog + (int64_t)(j * a.nA + i) * a.V;
@@ -501,7 +503,7 @@ static __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_THRE
     __shared__ ClSmem sm;
     pdl_trigger();
     pdl_wait();
-    const int j = blockIdx.x / CL_CTAS, i = blockIdx.y, l = a.l;
+    const int j = (a.phase == 2 ? a.l : 0) + blockIdx.x / CL_CTAS, i = blockIdx.y, l = a.l;
     Cl cl(sm, a.V);
     const int slot = a.slot[i], pos = a.committed[i] + j;
     const int64_t sid = a.sid[slot];

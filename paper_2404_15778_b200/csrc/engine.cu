@@ -31,8 +31,8 @@ struct LoopGraph {
     // per branch (l - lmin): launches and algorithmic {launches, bytes, flops} per
     // kernel class of one step, recorded while capturing (attention excluded:
     // its bytes depend on the lengths and are counted from the step trace)
-    std::vector<int64_t> launches;
-    std::vector<std::array<double, 3 * BASS_PROF_N>> algo;
+    std::vector<int64_t> launches, launches_b;   // _b: the conditional bonus part (sampled)
+    std::vector<std::array<double, 3 * BASS_PROF_N>> algo, algo_b;
     void reset() {
         if (exec) cudaGraphExecDestroy(exec);
         if (graph) cudaGraphDestroy(graph);
@@ -341,7 +341,8 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                      o_reason = lay((size_t)b * 4), o_cstep = lay((size_t)b * 4), o_tfin = lay((size_t)b * 8),
                      o_tstep = lay((size_t)steps_cap * 8), o_trl = lay((size_t)steps_cap * 4),
                      o_tracc = lay((size_t)steps_cap * b * 4), o_tremit = lay((size_t)steps_cap * b * 4),
-                     o_trkv = lay((size_t)steps_cap * b * 4), o_ident = lay((size_t)b * 4);
+                     o_trkv = lay((size_t)steps_cap * b * 4), o_ident = lay((size_t)b * 4),
+                     o_trb = lay((size_t)steps_cap * 4);
         const size_t g_total = o_end;
         char* dbase = nullptr;
         DevLoop* dS = nullptr;
@@ -361,6 +362,7 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
             hs.reason = P32(o_reason); hs.cstep = P32(o_cstep);
             hs.tfin = (unsigned long long*)(dbase + o_tfin); hs.tstep = (unsigned long long*)(dbase + o_tstep);
             hs.tr_l = P32(o_trl); hs.tr_acc = P32(o_tracc); hs.tr_emit = P32(o_tremit); hs.tr_kv = P32(o_trkv);
+            hs.tr_bonus = P32(o_trb);
             hs.rec = step_dev;
             std::memcpy(h.data(), &hs, sizeof(hs));
             auto H32 = [&](size_t off) { return (int32_t*)(h.data() + off); };
@@ -447,6 +449,8 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
             G.lmax = g_lmax;
             G.launches.assign(g_nbr, 0);
             G.algo.assign(g_nbr, {});
+            G.launches_b.assign(g_nbr, 0);
+            G.algo_b.assign(g_nbr, {});
             // capture on a private stream (the caller's stream may still run the
             // prompt step); every launch helper uses ctx->stream
             cudaStream_t cs;
@@ -513,19 +517,22 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                     a0[3 * x + 1] = c->algo_bytes[x];
                     a0[3 * x + 2] = c->algo_flops[x];
                 }
-                BASS_CUDA(cudaStreamBeginCaptureToGraph(cs, sw.conditional.phGraph_out[k], nullptr, nullptr, 0,
-                                                        cudaStreamCaptureModeRelaxed));
+                cudaGraph_t bg = sw.conditional.phGraph_out[k];
+                cudaGraphConditionalHandle h_bonus{};
+                if (!greedy) BASS_CUDA(cudaGraphConditionalHandleCreate(&h_bonus, bg, 0, 0));
+                BASS_CUDA(cudaStreamBeginCaptureToGraph(cs, bg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
                 loop_plan_kernel<<<1, ((b + 31) / 32) * 32, 0, cs>>>(dS, ar, B.pa);
                 launched(c);
                 const int32_t* perm = ar + B.pa.perm;
                 const int32_t* cperm = ar + B.pa.cperm;
                 const int32_t* gperm = ar + B.pa.gperm;
-                for (int j = 0; j < nd; ++j) {
+                // the draft forwards j < l; sampled: the bonus row's forward (j = l)
+                // is conditional, after the verify (below)
+                for (int j = 0; j < l; ++j) {
                     const PlanFwd& F = B.pa.f[j];
                     PreMeta pm{ar + F.meta, ar + F.work, true, F.stride, max_len, ar + F.live, ar + F.live + 1};
                     float* out = dlog + (size_t)j * b * V;
                     forward(D, *e->kv_draft, B.bts[j], e->strategy, out, e->props(), e->pstride, &pm);
-                    if (j == l) break;   // sampled bonus row: no pick
                     DraftPick dp{perm, d_sid, ar + B.pa.pos[j], e->props(), e->pstride, j,
                                  r->align, r->align_seed, d_align, d_plen, maxnew};
                     ProfScope prof(c, BASS_PROF_SAMPLE, (double)b * V * 4);
@@ -550,12 +557,66 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                 launched(c);
                 if (!greedy) {
                     VerifyArgs va{b, l, V, r->temperature, r->top_p, r->seed, perm, d_sid, cperm,
-                                  e->props(), e->pstride, vlog, dlog, scratch, accf, corr, btok};
-                    ProfScope prof(c, BASS_PROF_SAMPLE, (double)R * V * 8);
-                    cl_verify_shape_kernel<<<dim3((l + 1) * CL_CTAS, b, 2), CL_THREADS, 0, cs>>>(va, shp);
+                                  e->props(), e->pstride, vlog, dlog, scratch, accf, corr, btok, 1};
+                    {
+                        ProfScope prof(c, BASS_PROF_SAMPLE, (double)R * V * 8);
+                        cl_verify_shape_kernel<<<dim3((l + 1) * CL_CTAS, b, 2), CL_THREADS, 0, cs>>>(va, shp);
+                        launched(c);
+                        cl_verify_accept_kernel<<<dim3(l * CL_CTAS, b), CL_THREADS, 0, cs>>>(va, shp);
+                        launched(c);
+                    }
+                    BASS_CUDA(launch_pdl(loop_bonus_cond_kernel, dim3(1), dim3(((b + 31) / 32) * 32), 0, cs, dS,
+                                         (const int32_t*)accf, perm, l, h_bonus));
                     launched(c);
-                    cl_verify_accept_kernel<<<dim3((l + 1) * CL_CTAS, b), CL_THREADS, 0, cs>>>(va, shp);
-                    launched(c);
+                    // IF(a sequence accepted its whole draft) { bonus draft forward,
+                    // shape its row, draw + accept the bonus token }: end this
+                    // capture, hang the conditional node after its last node,
+                    // capture the body, then resume the chain after the node
+                    cudaStreamCaptureStatus cst;
+                    const cudaGraphNode_t* dp0 = nullptr;
+                    size_t ndp = 0;
+                    BASS_CUDA(cudaStreamGetCaptureInfo(cs, &cst, nullptr, nullptr, &dp0, &ndp));
+                    std::vector<cudaGraphNode_t> deps(dp0, dp0 + ndp);
+                    cudaGraph_t part = nullptr;
+                    BASS_CUDA(cudaStreamEndCapture(cs, &part));
+                    cudaGraphNodeParams ip = {};
+                    ip.type = cudaGraphNodeTypeConditional;
+                    ip.conditional.handle = h_bonus;
+                    ip.conditional.type = cudaGraphCondTypeIf;
+                    ip.conditional.size = 1;
+                    cudaGraphNode_t n_if;
+                    BASS_CUDA(cudaGraphAddNode(&n_if, bg, deps.data(), deps.size(), &ip));
+                    const int64_t lb0 = c->launches;
+                    double b0[3 * BASS_PROF_N];
+                    for (int x = 0; x < BASS_PROF_N; ++x) {
+                        b0[3 * x] = (double)c->algo_n[x];
+                        b0[3 * x + 1] = c->algo_bytes[x];
+                        b0[3 * x + 2] = c->algo_flops[x];
+                    }
+                    BASS_CUDA(cudaStreamBeginCaptureToGraph(cs, ip.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                            cudaStreamCaptureModeRelaxed));
+                    {
+                        const PlanFwd& F = B.pa.f[l];
+                        PreMeta pm{ar + F.meta, ar + F.work, true, F.stride, max_len, ar + F.live, ar + F.live + 1};
+                        forward(D, *e->kv_draft, B.bts[l], e->strategy, dlog + (size_t)l * b * V, e->props(),
+                                e->pstride, &pm);
+                        VerifyArgs vb = va;
+                        vb.phase = 2;
+                        ProfScope prof(c, BASS_PROF_SAMPLE, (double)b * V * 8);
+                        cl_verify_shape_kernel<<<dim3(CL_CTAS, b, 1), CL_THREADS, 0, cs>>>(vb, shp);
+                        launched(c);
+                        cl_verify_accept_kernel<<<dim3(CL_CTAS, b), CL_THREADS, 0, cs>>>(vb, shp);
+                        launched(c);
+                    }
+                    cudaGraph_t body = nullptr;
+                    BASS_CUDA(cudaStreamEndCapture(cs, &body));
+                    G.launches_b[k] = c->launches - lb0;
+                    for (int x = 0; x < BASS_PROF_N; ++x) {
+                        G.algo_b[k][3 * x] = (double)c->algo_n[x] - b0[3 * x];
+                        G.algo_b[k][3 * x + 1] = c->algo_bytes[x] - b0[3 * x + 1];
+                        G.algo_b[k][3 * x + 2] = c->algo_flops[x] - b0[3 * x + 2];
+                    }
+                    BASS_CUDA(cudaStreamBeginCaptureToGraph(cs, bg, &n_if, nullptr, 1, cudaStreamCaptureModeRelaxed));
                 }
                 StepArgs sa{b, l, V, perm, cperm, gperm, e->props(), e->pstride, vlog, vamax, vlse,
                             maxnew, r->eos_token, accf, corr, btok, greedy ? 1 : 0, step_dev, estride};
@@ -565,11 +626,11 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                 launched(c);
                 cudaGraph_t got = nullptr;
                 BASS_CUDA(cudaStreamEndCapture(cs, &got));
-                G.launches[k] = c->launches - l0;
+                G.launches[k] = c->launches - l0 - G.launches_b[k];
                 for (int x = 0; x < BASS_PROF_N; ++x) {
-                    G.algo[k][3 * x] = (double)c->algo_n[x] - a0[3 * x];
-                    G.algo[k][3 * x + 1] = c->algo_bytes[x] - a0[3 * x + 1];
-                    G.algo[k][3 * x + 2] = c->algo_flops[x] - a0[3 * x + 2];
+                    G.algo[k][3 * x] = (double)c->algo_n[x] - a0[3 * x] - G.algo_b[k][3 * x];
+                    G.algo[k][3 * x + 1] = c->algo_bytes[x] - a0[3 * x + 1] - G.algo_b[k][3 * x + 1];
+                    G.algo[k][3 * x + 2] = c->algo_flops[x] - a0[3 * x + 2] - G.algo_b[k][3 * x + 2];
                 }
                 // capture is not execution: its accounting is replayed per executed step
                 c->launches = l0;
@@ -623,12 +684,14 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
             const int H_m = M.g.n_head, dh_m = M.g.d_head, H_d = D.g.n_head, dh_d = D.g.d_head;
             const double es_m = (double)M.esize, es_d = (double)D.esize;
             for (int k = 1; k < n_steps; ++k) {
-                const int l = B32(o_trl)[k], bi = l - G.lmin, nd = l + (greedy ? 0 : 1);
-                c->launches += G.launches[bi] + 3;   // + select / continue / the while bookkeeping
+                const int l = B32(o_trl)[k], bi = l - G.lmin;
+                const bool bon = !greedy && B32(o_trb)[k];   // the conditional bonus draft forward ran
+                const int nd = l + (bon ? 1 : 0);
+                c->launches += G.launches[bi] + 3 + (bon ? G.launches_b[bi] : 0);   // + select / continue / while
                 for (int x = 0; x < BASS_PROF_N; ++x) {
-                    c->algo_n[x] += (int64_t)G.algo[bi][3 * x];
-                    c->algo_bytes[x] += G.algo[bi][3 * x + 1];
-                    c->algo_flops[x] += G.algo[bi][3 * x + 2];
+                    c->algo_n[x] += (int64_t)(G.algo[bi][3 * x] + (bon ? G.algo_b[bi][3 * x] : 0.0));
+                    c->algo_bytes[x] += G.algo[bi][3 * x + 1] + (bon ? G.algo_b[bi][3 * x + 1] : 0.0);
+                    c->algo_flops[x] += G.algo[bi][3 * x + 2] + (bon ? G.algo_b[bi][3 * x + 2] : 0.0);
                 }
                 double ab = 0.0, af = 0.0;
                 auto att = [&](int L, int H, int dh, double es, int off, int qq) {

@@ -43,6 +43,8 @@ struct DevLoop {                      // device-resident generation state
     unsigned long long *tfin;         // [b] globaltimer at completion
     unsigned long long *tstep;        // [steps_cap] globaltimer at the end of each step
     int32_t *tr_l, *tr_acc, *tr_emit, *tr_kv;   // [steps_cap], [steps_cap][b] x 3
+    int32_t *tr_bonus;                // [steps_cap] the sampled bonus draft forward ran
+    int bonus;                        // ... in the current step
     const char* rec;                  // finalize records of the step ([b] x slot_rec_bytes(estride))
 };
 
@@ -218,7 +220,9 @@ __global__ void __launch_bounds__(1024) loop_book_kernel(DevLoop* __restrict__ S
     if (tr) {
         S->tr_l[step] = l;
         S->tstep[step] = now;
+        S->tr_bonus[step] = S->bonus;
     }
+    S->bonus = 0;
     int ln = l, sn = S->s;
     if (!S->fixed && n_act > 0) {   // Algorithm 1
         if (mx == l) {
@@ -239,6 +243,29 @@ __global__ void __launch_bounds__(1024) loop_book_kernel(DevLoop* __restrict__ S
 
 // device time at the start of the generation (before the prompt step)
 __global__ void loop_stamp_kernel(DevLoop* __restrict__ S) { S->t0 = gtimer(); }
+// sampled steps: run the bonus draft forward only when an active sequence
+// accepted its whole draft (ref:engine.py:305-322; the accept flags of rows
+// j < l are final here).  perm: the step's sequence order.
+__global__ void loop_bonus_cond_kernel(DevLoop* __restrict__ S, const int32_t* __restrict__ acc_flag,
+                                       const int32_t* __restrict__ perm, int l,
+                                       cudaGraphConditionalHandle h_bonus) {
+    __shared__ int any;
+    pdl_wait();
+    if (threadIdx.x == 0) any = 0;
+    __syncthreads();
+    const int i = threadIdx.x;
+    if (i < S->b && !S->done[perm[i]]) {
+        bool all = true;
+        for (int j = 0; j < l; ++j) all &= acc_flag[i * (l + 1) + j] != 0;
+        if (all) atomicOr(&any, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        S->bonus = any;
+        cudaGraphSetConditional(h_bonus, any ? 1u : 0u);
+    }
+}
+
 // first node of the graph: the loop condition after the prompt step
 __global__ void loop_init_kernel(DevLoop* __restrict__ S, cudaGraphConditionalHandle h_loop) {
     int act = 0;

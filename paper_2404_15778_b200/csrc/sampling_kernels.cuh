@@ -292,6 +292,11 @@ struct VerifyArgs {
     int32_t* acc_flag;
     int32_t* corr;
     int32_t* bonus_tok;
+    // device loop: 0 = every row of the step at once; 1 = everything except
+    // the bonus draft row (j = l), which 2 handles after its conditional draft
+    // forward (ref:engine.py:305-322 runs that forward only when a sequence
+    // accepted its whole draft)
+    int phase;
 };
 
 // regular decoding: pick one token per active sequence from its current
