@@ -23,6 +23,30 @@
 using namespace bass;
 
 // the captured device-resident decode loop of one request shape (loop_graph.cuh)
+// a context's algorithmic counters {launches, bytes, flops} per kernel class
+using AlgoVec = std::array<double, 3 * BASS_PROF_N>;
+static AlgoVec algo_take(const bass_ctx* c) {
+    AlgoVec v;
+    for (int x = 0; x < BASS_PROF_N; ++x) {
+        v[3 * x] = (double)c->algo_n[x];
+        v[3 * x + 1] = c->algo_bytes[x];
+        v[3 * x + 2] = c->algo_flops[x];
+    }
+    return v;
+}
+static void algo_set(bass_ctx* c, const AlgoVec& v) {
+    for (int x = 0; x < BASS_PROF_N; ++x) {
+        c->algo_n[x] = (int64_t)v[3 * x];
+        c->algo_bytes[x] = v[3 * x + 1];
+        c->algo_flops[x] = v[3 * x + 2];
+    }
+}
+static AlgoVec algo_sub(const AlgoVec& a, const AlgoVec& b) {
+    AlgoVec v;
+    for (int i = 0; i < 3 * BASS_PROF_N; ++i) v[i] = a[i] - b[i];
+    return v;
+}
+
 struct LoopGraph {
     std::vector<double> key;          // every scalar / pointer baked into its kernels
     cudaGraph_t graph = nullptr;
@@ -32,7 +56,7 @@ struct LoopGraph {
     // kernel class of one step, recorded while capturing (attention excluded:
     // its bytes depend on the lengths and are counted from the step trace)
     std::vector<int64_t> launches, launches_b;   // _b: the conditional bonus part (sampled)
-    std::vector<std::array<double, 3 * BASS_PROF_N>> algo, algo_b;
+    std::vector<AlgoVec> algo, algo_b;
     void reset() {
         if (exec) cudaGraphExecDestroy(exec);
         if (graph) cudaGraphDestroy(graph);
@@ -511,12 +535,7 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                 const int l = g_lmin + k, nd = l + (greedy ? 0 : 1), R = b * (l + 1);
                 Branch& B = brs[k];
                 const int64_t l0 = c->launches;
-                double a0[3 * BASS_PROF_N];
-                for (int x = 0; x < BASS_PROF_N; ++x) {
-                    a0[3 * x] = (double)c->algo_n[x];
-                    a0[3 * x + 1] = c->algo_bytes[x];
-                    a0[3 * x + 2] = c->algo_flops[x];
-                }
+                const AlgoVec a0 = algo_take(c);
                 cudaGraph_t bg = sw.conditional.phGraph_out[k];
                 cudaGraphConditionalHandle h_bonus{};
                 if (!greedy) BASS_CUDA(cudaGraphConditionalHandleCreate(&h_bonus, bg, 0, 0));
@@ -587,12 +606,7 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                     cudaGraphNode_t n_if;
                     BASS_CUDA(cudaGraphAddNode(&n_if, bg, deps.data(), deps.size(), &ip));
                     const int64_t lb0 = c->launches;
-                    double b0[3 * BASS_PROF_N];
-                    for (int x = 0; x < BASS_PROF_N; ++x) {
-                        b0[3 * x] = (double)c->algo_n[x];
-                        b0[3 * x + 1] = c->algo_bytes[x];
-                        b0[3 * x + 2] = c->algo_flops[x];
-                    }
+                    const AlgoVec b0 = algo_take(c);
                     BASS_CUDA(cudaStreamBeginCaptureToGraph(cs, ip.conditional.phGraph_out[0], nullptr, nullptr, 0,
                                                             cudaStreamCaptureModeRelaxed));
                     {
@@ -611,11 +625,7 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                     cudaGraph_t body = nullptr;
                     BASS_CUDA(cudaStreamEndCapture(cs, &body));
                     G.launches_b[k] = c->launches - lb0;
-                    for (int x = 0; x < BASS_PROF_N; ++x) {
-                        G.algo_b[k][3 * x] = (double)c->algo_n[x] - b0[3 * x];
-                        G.algo_b[k][3 * x + 1] = c->algo_bytes[x] - b0[3 * x + 1];
-                        G.algo_b[k][3 * x + 2] = c->algo_flops[x] - b0[3 * x + 2];
-                    }
+                    G.algo_b[k] = algo_sub(algo_take(c), b0);
                     BASS_CUDA(cudaStreamBeginCaptureToGraph(cs, bg, &n_if, nullptr, 1, cudaStreamCaptureModeRelaxed));
                 }
                 StepArgs sa{b, l, V, perm, cperm, gperm, e->props(), e->pstride, vlog, vamax, vlse,
@@ -627,18 +637,10 @@ int bass_spec_generate(bass_engine* e, const bass_gen_request* r, bass_gen_resul
                 cudaGraph_t got = nullptr;
                 BASS_CUDA(cudaStreamEndCapture(cs, &got));
                 G.launches[k] = c->launches - l0 - G.launches_b[k];
-                for (int x = 0; x < BASS_PROF_N; ++x) {
-                    G.algo[k][3 * x] = (double)c->algo_n[x] - a0[3 * x] - G.algo_b[k][3 * x];
-                    G.algo[k][3 * x + 1] = c->algo_bytes[x] - a0[3 * x + 1] - G.algo_b[k][3 * x + 1];
-                    G.algo[k][3 * x + 2] = c->algo_flops[x] - a0[3 * x + 2] - G.algo_b[k][3 * x + 2];
-                }
+                G.algo[k] = algo_sub(algo_sub(algo_take(c), a0), G.algo_b[k]);
                 // capture is not execution: its accounting is replayed per executed step
                 c->launches = l0;
-                for (int x = 0; x < BASS_PROF_N; ++x) {
-                    c->algo_n[x] = (int64_t)a0[3 * x];
-                    c->algo_bytes[x] = a0[3 * x + 1];
-                    c->algo_flops[x] = a0[3 * x + 2];
-                }
+                algo_set(c, a0);
             }
             (void)n_cond;
             BASS_CUDA(cudaGraphInstantiate(&G.exec, G.graph, 0));

@@ -109,10 +109,10 @@ def c2(strategies):
 
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
-    if what == "one":   # python tools/attn_bench.py one b q L H [strategy [dh]]  (ncu captures)
+    if what == "one":   # python tools/attn_bench.py one b q L H [strategy [dh [reps]]]  (ncu captures)
         b, q, Lc, H = (int(a) for a in sys.argv[2:6])
-        point([Lc] * b, [q] * b, H, sys.argv[6] if len(sys.argv) > 6 else "ragged", "one", reps=3,
-              dh=int(sys.argv[7]) if len(sys.argv) > 7 else 128)
+        point([Lc] * b, [q] * b, H, sys.argv[6] if len(sys.argv) > 6 else "ragged", "one",
+              reps=int(sys.argv[8]) if len(sys.argv) > 8 else 3, dh=int(sys.argv[7]) if len(sys.argv) > 7 else 128)
         sys.exit(0)
     strategies = (sys.argv[2] if len(sys.argv) > 2 else "ragged").split(",")
     if what in ("c2", "all"):
