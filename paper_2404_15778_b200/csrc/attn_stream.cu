@@ -40,7 +40,7 @@
 namespace bass {
 namespace ast {
 
-constexpr int CH = 128, SPLIT_CH = 8, SPLIT = CH * SPLIT_CH, THREADS = 192;
+constexpr int CH = 128, SPLIT_CH = 8, SPLIT = CH * SPLIT_CH;
 constexpr float TH = 8.f;   // reuse the reference max while scores stay below it + TH (log2 units)
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -276,8 +276,9 @@ struct Cfg {
     static constexpr int P_BUF = CH * NQ * 2;     // P^T [128 keys][NQ] bf16, MN-major (queries contiguous)
     static constexpr int OFF_RED = OFF_P + 2 * P_BUF;    // red[4][NQ], fin, mref, thr, alph [NQ]
     static constexpr int OFF_BAR = OFF_RED + 8 * NQ * 4;
-    // q_full[2] q_empty[2] k_full[S] v_full[S] kv_empty[S] s_full[2] s_free[2] p_full[2] p_free[2] o_full[2] o_free[2]
-    static constexpr int NBAR = 16 + 3 * STAGES;
+    // q_full[2] q_empty[2] k_full[S] v_full[S] k_empty[S] v_empty[S] s_full[2] s_free[2] p_full[2] p_free[2]
+    // o_full[2] o_free[2]
+    static constexpr int NBAR = 16 + 4 * STAGES;
     static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
     static constexpr int TMEM_COLS = 4 * NQ < 32 ? 32 : 4 * NQ;   // S0 S1 O0 O1
 };
@@ -297,6 +298,12 @@ __global__ void __launch_bounds__(attn_threads(NQ), 1) attn_stream_kernel(
     using Cf = Cfg<NQ, DH, STG>;
     constexpr int ST = Cf::STAGES, SUB = Cf::SUB;
     constexpr int SG = softmax_groups(NQ), CQ = NQ / SG;
+    // K ahead of V, except in the long-history NQ = 16 build, whose softmax
+    // never holds up the next S^T (measured: K-ahead costs it 5-8 % at L >= 2K,
+    // while NQ = 64 gains 27-37 % and short histories ~5 %), and for d_head 64,
+    // whose PV MMA also reads the stage's K block (neutral to slightly slower)
+    constexpr bool KA = !(NQ == 16 && ST == 3) && DH != 64;
+    constexpr bool K_EARLY = KA;   // K slot released by the S^T MMA
     if (threadIdx.x == 0) APROBE(0);
     extern __shared__ uint8_t smem_raw[];
     pdl_trigger();
@@ -314,8 +321,9 @@ __global__ void __launch_bounds__(attn_threads(NQ), 1) attn_stream_kernel(
     uint64_t* q_empty = bars + 2;
     uint64_t* k_full = bars + 4;
     uint64_t* v_full = k_full + ST;
-    uint64_t* kv_empty = v_full + ST;
-    uint64_t* s_full = kv_empty + ST;
+    uint64_t* k_empty = v_full + ST;
+    uint64_t* v_empty = k_empty + ST;
+    uint64_t* s_full = v_empty + ST;
     uint64_t* s_free = s_full + 2;
     uint64_t* p_full = s_free + 2;
     uint64_t* p_free = p_full + 2;
@@ -366,19 +374,37 @@ __global__ void __launch_bounds__(attn_threads(NQ), 1) attn_stream_kernel(
             bool have = items.next(wk, h);
             uint64_t kpol;
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(kpol));
+            // K and V of a chunk have their own ring slots.  KA: a K slot frees
+            // when the chunk's S^T MMA completes, a V slot when its PV MMA does,
+            // and K runs one chunk ahead of V (K(c+1) is issued before V(c)), so
+            // the next S^T never waits behind this chunk's softmax
+            int gv = 0, pv_row = -1, pv_c = 0;
+            auto load_v = [&](int kv_row0, int c) {
+                const int st = gv % ST;
+                if (gv >= ST) mbar_wait(su32(&v_empty[st]), ((gv / ST) - 1) & 1);
+                const uint32_t sb = base + st * Cf::STAGE;
+                mbar_expect_tx(su32(&v_full[st]), SUB * Cf::KV_TILE);
+                for (int s = 0; s < SUB; ++s)
+                    tma_2d_ef(&tv, sb + Cf::V_OFF + s * Cf::KV_TILE, su32(&v_full[st]), s * 64, kv_row0 + c * CH,
+                              kpol);
+                ++gv;
+            };
             auto load_kv = [&](int kv_row0, int c) {
                 const int st = g % ST;
-                if (g >= ST) mbar_wait(su32(&kv_empty[st]), ((g / ST) - 1) & 1);
+                if (g >= ST) mbar_wait(su32(&k_empty[st]), ((g / ST) - 1) & 1);
                 const uint32_t sb = base + st * Cf::STAGE;
                 mbar_expect_tx(su32(&k_full[st]), SUB * Cf::KV_TILE);
                 for (int s = 0; s < SUB; ++s)
                     tma_2d_ef(&tk, sb + Cf::K_OFF + s * Cf::KV_TILE, su32(&k_full[st]), s * 64, kv_row0 + c * CH,
                               kpol);
-                mbar_expect_tx(su32(&v_full[st]), SUB * Cf::KV_TILE);
-                for (int s = 0; s < SUB; ++s)
-                    tma_2d_ef(&tv, sb + Cf::V_OFF + s * Cf::KV_TILE, su32(&v_full[st]), s * 64, kv_row0 + c * CH,
-                              kpol);
                 ++g;
+                if (!KA) {
+                    load_v(kv_row0, c);
+                    return;
+                }
+                if (pv_row >= 0) load_v(pv_row, pv_c);
+                pv_row = kv_row0;
+                pv_c = c;
             };
             // first item: its leading history chunks before the dependency wait
             int pre = 0;
@@ -403,6 +429,7 @@ __global__ void __launch_bounds__(attn_threads(NQ), 1) attn_stream_kernel(
                 ++n;
                 have = items.next(wk, h);
             }
+            if (pv_row >= 0) load_v(pv_row, pv_c);
         }
         __syncwarp();
     } else if (warp == 1) {
@@ -429,7 +456,9 @@ __global__ void __launch_bounds__(attn_threads(NQ), 1) attn_stream_kernel(
                     const uint64_t bdesc = (sdesc(ps + kk * 32 * NQ, Cf::P_BUF, 16 * NQ) & ~(7ull << 61)) | (PLT << 61);
                     umma(d, sdesc(vs + kk * 2048, Cf::KV_TILE, 1024), bdesc, ID2, (p.first && kk == 0) ? 0u : 1u);
                 }
-                commit(su32(&kv_empty[p.st]));
+                commit(su32(&v_empty[p.st]));
+                // (d_head 64: the PV A operand's upper block is this stage's K0)
+                if (!K_EARLY) commit(su32(&k_empty[p.st]));
                 commit(su32(&p_free[sb]));
                 if (p.last) commit(su32(&o_full[p.ob]));
             };
@@ -456,6 +485,7 @@ __global__ void __launch_bounds__(attn_threads(NQ), 1) attn_stream_kernel(
                              sdesc(qs + sub * Cf::R_TILE + in, 16, 1024), ID1, kk > 0);
                     }
                     commit(su32(&s_full[sb]));
+                    if (K_EARLY) commit(su32(&k_empty[st]));
                     if (c == wk.nch - 1) commit(su32(&q_empty[qb]));
                     // O^T += V^T P^T of the previous chunk while the softmax works on this one
                     if (pend.g >= 0) pv(pend);
@@ -711,7 +741,10 @@ static void launch(bass_ctx* ctx, const AttnPlan& p, const CUtensorMap& tk, cons
 int stream_split_len() { return ast::SPLIT; }
 int stream_chunk_len() { return ast::CH; }
 int stream_split_chunks() { return ast::SPLIT_CH; }
-int stream_nq_for(int q) { return q <= 16 ? 16 : q <= 32 ? 32 : 64; }
+#ifndef BASS_NQ32_MAXQ
+#define BASS_NQ32_MAXQ 32
+#endif
+int stream_nq_for(int q) { return q <= 16 ? 16 : q <= BASS_NQ32_MAXQ ? 32 : 64; }
 int stream_items_per_seq(int q, int max_len) {
     const int nq = stream_nq_for(q);
     const int chunks = (std::max(max_len, 1) + ast::CH - 1) / ast::CH;
@@ -753,7 +786,7 @@ bool tc_attention_supported(int dtype, int dh) { return dtype == BASS_BF16 && (d
 static int stream_nq(const std::vector<int32_t>& qn) {
     int max_qn = 0;
     for (int v : qn) max_qn = std::max(max_qn, v);
-    return max_qn <= 16 ? 16 : max_qn <= 32 ? 32 : 64;
+    return stream_nq_for(max_qn);
 }
 
 // work items (Work, 8 int32 each) in sequence order; first[i] = sequence i's first item
@@ -774,12 +807,19 @@ static bool stream_items(int strategy, const std::vector<int32_t>& slot, const s
     for (int i = 0; i < n_seq; ++i) {
         if (first) (*first)[i] = (int)(w.size() - w0) / 8;
         const int rows = strategy == BASS_PAD ? max_qn : qn[i];
-        for (int t0 = 0; t0 < rows; t0 += NQ) {
+        // split-major, query tile minor: the tiles of one (split, head) stream
+        // the same K/V rows H items apart, i.e. concurrently, so the later
+        // tiles read them from L2
+        auto n_chunks = [&](int t0) {
             const int last = strategy == BASS_PAD ? max_L - 1 : off[i] + std::min(qn[i], t0 + NQ) - 1;
-            const int n_chunks = last / CH + 1;
-            for (int s = 0; s * SPLIT_CH < n_chunks; ++s) {
-                const int sf = std::min(off[i], safe ? (*safe)[i] : off[i]);
-                w.insert(w.end(), {slot[i], q0, qn[i], off[i], t0, s, std::min(SPLIT_CH, n_chunks - s * SPLIT_CH), sf});
+            return last / CH + 1;
+        };
+        const int sf = std::min(off[i], safe ? (*safe)[i] : off[i]);
+        for (int s = 0; s * SPLIT_CH < n_chunks(rows - 1); ++s) {
+            for (int t0 = 0; t0 < rows; t0 += NQ) {
+                const int nc = n_chunks(t0);
+                if (s * SPLIT_CH >= nc) continue;
+                w.insert(w.end(), {slot[i], q0, qn[i], off[i], t0, s, std::min(SPLIT_CH, nc - s * SPLIT_CH), sf});
                 if (s > 0) multi = true;
             }
         }

@@ -128,13 +128,18 @@ __global__ void __launch_bounds__(1024) loop_plan_kernel(const DevLoop* __restri
         // only sees its first keys (finite values, no history streamed)
         const int aoff = fin ? 0 : off;
         int k = 0;
-        for (int t0 = 0; t0 < q; t0 += F.nq) {
-            const int last = (a.strategy == BASS_PAD && !fin) ? pad_last : aoff + min(q, t0 + F.nq) - 1;
-            const int nch = last / a.ch + 1;
-            for (int s = 0; s * a.split_ch < nch && k < F.stride; ++s, ++k) {
+        // split-major, query tile minor (as stream_items: the tiles of one
+        // split share their K/V rows through L2)
+        const int last_row = (a.strategy == BASS_PAD && !fin) ? pad_last : aoff + q - 1;
+        for (int s = 0; s * a.split_ch < last_row / a.ch + 1; ++s) {
+            for (int t0 = 0; t0 < q && k < F.stride; t0 += F.nq) {
+                const int last = (a.strategy == BASS_PAD && !fin) ? pad_last : aoff + min(q, t0 + F.nq) - 1;
+                const int nch = last / a.ch + 1;
+                if (s * a.split_ch >= nch) continue;
                 int32_t* it = w + k * 8;
                 it[0] = slot; it[1] = i * q; it[2] = q; it[3] = aoff;
                 it[4] = t0; it[5] = s; it[6] = min(a.split_ch, nch - s * a.split_ch); it[7] = min(aoff, safe);
+                ++k;
             }
         }
         for (; k < F.stride; ++k) {   // idle padding (skipped by the attention's item loop)

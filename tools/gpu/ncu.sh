@@ -15,3 +15,4 @@ full ncu_attn_c2 'attn_stream_kernel<\(int\)16, \(int\)128' 300 python bench.py 
 full ncu_gemm_prefill_qkv 'gemm_tc_kernel<\(int\)128, \(int\)0' 0 python tools/prefill_bench.py 8 128 1
 full ncu_gemm_prefill_o 'gemm_tc_kernel<\(int\)256, \(int\)1' 0 python tools/prefill_bench.py 8 128 1
 ls -la gpurun_out/*.ncu-rep
+full ncu_attn_q33 'attn_stream_kernel<\(int\)64, \(int\)128' 0 python tools/attn_bench.py one 64 33 8192 36
