@@ -741,10 +741,9 @@ static void launch(bass_ctx* ctx, const AttnPlan& p, const CUtensorMap& tk, cons
 int stream_split_len() { return ast::SPLIT; }
 int stream_chunk_len() { return ast::CH; }
 int stream_split_chunks() { return ast::SPLIT_CH; }
-#ifndef BASS_NQ32_MAXQ
-#define BASS_NQ32_MAXQ 32
-#endif
-int stream_nq_for(int q) { return q <= 16 ? 16 : q <= BASS_NQ32_MAXQ ? 32 : 64; }
+// query tile: the smallest of 16 / 32 / 64 columns covering the block (q = 33-64
+// as two NQ = 32 tiles measured slower: each tile streams the history again)
+int stream_nq_for(int q) { return q <= 16 ? 16 : q <= 32 ? 32 : 64; }
 int stream_items_per_seq(int q, int max_len) {
     const int nq = stream_nq_for(q);
     const int chunks = (std::max(max_len, 1) + ast::CH - 1) / ast::CH;
@@ -782,7 +781,6 @@ bool tc_attention_supported(int dtype, int dh) { return dtype == BASS_BF16 && (d
 
 // Plan: work items (seq, q tile, split, chunks seen) — RAGGED/SPLIT exact,
 // PAD over the padded [max q] x [max L] grid (padded keys streamed, masked).
-// query tile: smallest of 16 / 32 / 64 columns covering the longest block
 static int stream_nq(const std::vector<int32_t>& qn) {
     int max_qn = 0;
     for (int v : qn) max_qn = std::max(max_qn, v);
