@@ -189,3 +189,31 @@ def test_attention_strategies_bitwise_equal_bf16(ctx, dh):
         w = want[i].transpose(1, 0, 2)
         err = np.abs(got[cu[i]:cu[i + 1]] - w).max() / np.abs(w).max()
         assert err < 1e-2, err
+
+
+@pytest.mark.parametrize("q_max", [16, 32, 65])
+def test_attention_tile_classes_long_histories(ctx, q_max):
+    """Each query-tile build (NQ = 16 with its long-history 3-stage ring,
+    NQ = 32 and NQ = 64 with K streamed ahead of V, two NQ = 64 tiles per
+    block in split-major item order) over histories of up to three 1024-key
+    splits: PAD == SPLIT == RAGGED bitwise and within 1e-2 of the oracle."""
+    import torch
+    from paper_2404_15778_b200 import attend_device
+    rng = np.random.default_rng(q_max)
+    H, dh = 8, 128
+    q_lens = [q_max, 1, max(1, q_max // 2), 3, q_max]
+    kv = [int(rng.integers(max(q, 1100), 3000)) for q in q_lens]
+    qs = [rng.standard_normal((H, q, dh)) for q in q_lens]
+    ks = [rng.standard_normal((H, n, dh)) for n in kv]
+    vs = [rng.standard_normal((H, n, dh)) for n in kv]
+    offs = [n - q for n, q in zip(kv, q_lens)]
+    Q, K, Vv, cu = _workload_to_device(qs, ks, vs, torch.bfloat16)
+    outs = [attend_device(ctx, Q, K, Vv, cu, offs, s) for s in ("pad", "split", "ragged")]
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+    r = lambda a: torch.tensor(a).bfloat16().double().numpy()
+    want = OR.attend_split([r(q) for q in qs], [r(k) for k in ks], [r(v) for v in vs], offs)
+    got = outs[2].double().cpu().numpy()
+    for i in range(len(q_lens)):
+        w = want[i].transpose(1, 0, 2)
+        err = np.abs(got[cu[i]:cu[i + 1]] - w).max() / np.abs(w).max()
+        assert err < 1e-2, err
