@@ -156,6 +156,27 @@ def trace_summary(rec):
         spans = [(x[:, 1].max() - x[:, 0].min()) / 1e3 for x in np.split(r, cut)]
         out["classes"][name] = {"union_ms": _union_ms(r[:, :2]), "launches": len(spans),
                                 "median_span_us": float(np.median(spans)), "ctas": int(len(r))}
+    # critical-path attribution: walking the launches in issue order, the part
+    # of launch i's [first CTA start, last CTA end] that lies past every
+    # earlier launch's end belongs to launch i alone — the per-class sums
+    # partition the traced timeline (their total is the busy time), unlike
+    # the union above, which also counts CTAs launched early (PDL) that
+    # wait on their predecessor
+    if len(rec):
+        o = np.argsort(seq, kind="stable")
+        r, sq, cl = rec[o], seq[o], cls[o]
+        cut = np.flatnonzero(np.diff(sq)) + 1
+        frontier = 0
+        exposed = {}
+        for x, c in zip(np.split(r, cut), np.split(cl, cut)):
+            s0, e1 = int(x[:, 0].min()), int(x[:, 1].max())
+            exp = max(0, e1 - max(frontier, s0))
+            frontier = max(frontier, e1)
+            name = TRACE_CLASSES.get(int(c[0]), "other")
+            exposed[name] = exposed.get(name, 0) + exp
+        for name, ns in exposed.items():
+            if name in out["classes"]:
+                out["classes"][name]["exposed_ms"] = ns / 1e6
     out["untraced_ms"] = None
     if len(rec):
         busy = _union_ms(rec[:, :2])
@@ -493,6 +514,10 @@ def main():
                         "share_of_generation": t["union_ms"] / trace["generation_ms"],
                         "median_launch_span_us": t["median_span_us"],
                         "tflops": g["flops"] / (t["union_ms"] / 1e3) / 1e12})
+            if t.get("exposed_ms"):
+                ex = g["bytes"] / (t["exposed_ms"] / 1e3) / 1e9
+                out.update({"exposed_ms_per_generation": t["exposed_ms"], "achieved_exposed": ex,
+                            "frac_exposed": ex / hbm})
         return out
 
     traffic = None
@@ -509,7 +534,9 @@ def main():
                      "step_frac": all_bytes / (step_ms / 1e3) / 1e9 / hbm,
                      "method": "achieved = algorithmic GEMM bytes per generation / in-chain GEMM time (union of "
                                "the GEMM CTAs' globaltimer intervals in a traced generation); step_frac = all "
-                               "algorithmic bytes per generation / ms_per_step / peak"})
+                               "algorithmic bytes per generation / ms_per_step / peak; frac_exposed = bytes / "
+                               "the class's critical-path share (each launch owns the part of its span past "
+                               "every earlier launch's end; the classes partition the traced timeline)"})
     line = {
         "metric": METRIC,
         "value": tokens / dev_s,

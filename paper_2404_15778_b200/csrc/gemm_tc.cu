@@ -47,7 +47,9 @@ constexpr int UK = 16;           // k per tcgen05.mma for 16-bit inputs
 constexpr int EH = 2;               // epilogue row groups: warps w, w + 4 share TMEM lane quarter w (EH = 3 with 80 registers measured slower)
 constexpr int THREADS = 128 * EH;   // 8 warps: 0 producer, 1 MMA, 2 TMEM alloc / folded-LN stats; all drain
 
-template <int TT, int NB>
+// STG > 0: a fixed ring depth (a GEMM whose every split fits in STG stages
+// takes less shared memory, so its CTAs can start beside the kernel before it)
+template <int TT, int NB, int STG = 0>
 struct Cfg {
     static constexpr int W_BYTES = NB * BN * BK * 2;
     static constexpr int X_BYTES = TT * BK * 2;
@@ -55,7 +57,7 @@ struct Cfg {
     // two CTAs per SM (110 KB) when that still leaves >= 2 stages, else one
     static constexpr int BUDGET = (110 * 1024 - 2048) / STAGE >= 2 ? 110 * 1024 - 2048 : 200 * 1024;
     static constexpr int STAGES_RAW = BUDGET / STAGE;
-    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
+    static constexpr int STAGES = STG > 0 ? STG : STAGES_RAW > 8 ? 8 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
     static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/ + 2 * TT * 4 /*XN row stats*/;
     static constexpr int COLS = NB * TT;
     static constexpr int TMEM_COLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128 : COLS <= 256 ? 256 : 512;
@@ -279,7 +281,7 @@ __device__ int g_gp_n, g_gp_k;
 // order exactly as the cluster reduction does (same K partition, same
 // accumulation and summation order: bit-identical rows, no cluster
 // barriers, no partial exchange).
-template <int TT, int MODE, int NB, bool PACKED, int LNF, bool I8 = false, bool SER = false>
+template <int TT, int MODE, int NB, bool PACKED, int LNF, bool I8 = false, bool SER = false, int STG = 0>
 __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tw,
                                                              const __grid_constant__ CUtensorMap tx,
                                                              const __nv_bfloat16* __restrict__ wpk, int M, int N,
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(THREADS, EH > 2 ? 2 : 1) gemm_tc_kernel(const 
     const bool gp_on = g_gp && N == g_gp_n && sp.k_iters * BK == g_gp_k && gp_cta < 16;
 #endif
     if (threadIdx.x == 0) GPROBE(0);
-    using C = Cfg<TT, NB>;
+    using C = Cfg<TT, NB, STG>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = su32(smem_raw);
     const uint32_t base = (raw + 1023) & ~1023u;
@@ -1064,15 +1066,16 @@ struct LaunchArgs {
     int M, N;
     Split sp;
     XNorm xn;
+    bool lite;
 };
 
-template <int TT, int MODE, bool PACKED, int LNF, bool I8 = false, bool SER = false>
+template <int TT, int MODE, bool PACKED, int LNF, bool I8 = false, bool SER = false, int STG = 0>
 static void launch_k(bass_model& m, const LaunchArgs& a, const Epi& e) {
     constexpr int NB = 1;   // (NB = 2 measured slower at every benchmark shape: profiles/r1_gemm_nb_split_sweep.txt)
-    using C = Cfg<TT, NB>;
+    using C = Cfg<TT, NB, STG>;
     static unsigned attr = 0;
     once_per_device(attr, [] {
-        BASS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<TT, MODE, NB, PACKED, LNF, I8, SER>,
+        BASS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<TT, MODE, NB, PACKED, LNF, I8, SER, STG>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     });
     cudaLaunchConfig_t cfg = {};
@@ -1090,7 +1093,7 @@ static void launch_k(bass_model& m, const LaunchArgs& a, const Epi& e) {
     cfg.attrs = at;
     cfg.numAttrs = (a.sp.S > 1 && !SER) ? 2 : 1;
     const int nblk = (int)(cfg.gridDim.x * cfg.gridDim.y * cfg.gridDim.z);
-    BASS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TT, MODE, NB, PACKED, LNF, I8, SER>, *a.wm, *a.xm,
+    BASS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TT, MODE, NB, PACKED, LNF, I8, SER, STG>, *a.wm, *a.xm,
                                  (const __nv_bfloat16*)a.W, a.M, a.N, a.sp, e, a.xn,
                                  m.ctx->trace(nblk, BASS_TR_GEMM)));
 }
@@ -1122,6 +1125,12 @@ static void launch_mode(bass_model& m, int mode, bool packed, bool xn, const Lau
     switch (mode) {
         case EPI_QKV: launch_k<TT, EPI_QKV, true, 0, false, SER>(m, a, e); break;
         case EPI_RESID:
+            if constexpr (TT == 16 && !SER) {
+                if (e.stats && a.lite) {   // every split in 4 stages (74 KB): starts beside the attention kernel
+                    launch_k<16, EPI_RESID, true, 2, false, false, 4>(m, a, e);
+                    break;
+                }
+            }
             if (e.stats) launch_k<TT, EPI_RESID, true, 2, false, SER>(m, a, e);   // emits the next LayerNorm's inputs
             else launch_k<TT, EPI_RESID, true, 0, false, SER>(m, a, e);
             break;
@@ -1197,7 +1206,13 @@ void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N
         const size_t blocks = (size_t)((N + NB * BN - 1) / (NB * BN)) * ((M + TT - 1) / TT);
         sp.ws = (float*)S.ws.need(blocks * sp.S * TT * NB * BN * 4, m.ctx->stream);
     }
-    LaunchArgs a{wm, xm, W, M, N, sp, xn};
+    // decode-sized residual projection whose splits hold <= 4 k blocks (the
+    // draft's O-projection): a 4-stage ring (74 KB) fits beside the
+    // attention kernel (146 KB), so its CTAs launch during the attention and
+    // have their whole weight slice in shared memory when it ends (C2
+    // 1.263 -> 1.254 ms/token; the same arithmetic, only the ring depth)
+    const bool lite = TT == 16 && !ser && sp.S > 1 && sp.k_iters <= 4 * sp.S && mode == EPI_RESID && packed && !i8;
+    LaunchArgs a{wm, xm, W, M, N, sp, xn, lite};
     const bool xnb = norm != nullptr;
     if (ser) {
         if (TT == 128) launch_mode<128, true>(m, mode, packed, xnb, a, e);
