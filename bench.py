@@ -184,6 +184,42 @@ def trace_summary(rec):
     return out
 
 
+# ------------------------------------------- ragged attention (metric part 3)
+def ragged_attention_point(ctx, hbm, b=64, L=8192, q=17, H=36, dh=128, reps=10, seed=7):
+    """The metric's "ragged-attn HBM GB/s": the RAGGED attention kernel alone
+    at the C4 sweep's largest point (b = 64, L_i ~ U[L/2, L] seeded, q = k + 1
+    = 17 new rows per sequence, H = 36, d_head = 128), device-timed
+    (bass_attention_bench: back-to-back launches, CUDA events); bytes = real
+    K/V rows + Q in + O out, K/V ~ 9.7 GB >> L2."""
+    import ctypes as C
+    import torch
+    from paper_2404_15778_b200 import _lib as L_
+    from paper_2404_15778_b200.attention import strategy_code
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(L // 2, L + 1, b)
+    stride = int(lens.max())
+    K = torch.randn(b * H * stride * dh, device="cuda", dtype=torch.bfloat16)
+    V = torch.randn_like(K)
+    q_lens = np.full(b, q)
+    cu = np.concatenate([[0], np.cumsum(q_lens)]).astype(np.int32)
+    offs = (lens - q_lens).astype(np.int32)
+    Q = torch.randn(int(cu[-1]), H, dh, device="cuda", dtype=torch.bfloat16)
+    out = torch.empty_like(Q)
+    ms = C.c_double()
+    torch.cuda.synchronize()
+    ctx.check(ctx.lib.bass_attention_bench(ctx.handle, strategy_code("ragged"), b, H, dh, L_.ptr(cu, C.c_int32),
+                                           L_.ptr(offs, C.c_int32), C.c_void_p(Q.data_ptr()),
+                                           C.c_void_p(K.data_ptr()), C.c_void_p(V.data_ptr()), stride, 1,
+                                           C.c_void_p(out.data_ptr()), reps, C.byref(ms)))
+    by = sum(2 * H * int(n) * dh * 2 + 2 * H * q * dh * 2 for n in lens)
+    gbs = by / (ms.value / 1e3) / 1e9
+    del K, V, Q, out
+    torch.cuda.empty_cache()
+    return {"kernel": "attn_stream_kernel (RAGGED)", "b": b, "L": f"U[{L // 2}, {L}]", "q": q, "H": H,
+            "d_head": dh, "us_per_launch": ms.value * 1e3, "bytes_per_launch": by, "GB/s": gbs, "peak": hbm,
+            "frac": gbs / hbm, "timing": "device (CUDA events), back-to-back launches, K/V >> L2"}
+
+
 # ------------------------------------------------- acceptance-harness schedule
 _M64 = (1 << 64) - 1
 
@@ -313,6 +349,8 @@ def main():
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "int8"],
                     help="int8: the W8A8 path (SURVEY 8(f1), ref:quant.py) for main and draft")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-attn-point", dest="attn_point", action="store_false",
+                    help="skip the standalone ragged-attention point (the metric's GB/s part)")
     ap.add_argument("--profile-only", action="store_true", help="one profiled generation (ncu)")
     ap.add_argument("--save-traj", default=None, help="save the greedy trajectory (.npy)")
     ap.add_argument("--load-traj", default=None, help="reuse a saved trajectory (ncu runs)")
@@ -578,6 +616,8 @@ def main():
         "kernel_event_ms_per_generation": ({k: v["ms"] for k, v in prof.items()} if prof else None),
         "clocks": clocks.summary(),
     }
+    if rank == 0 and args.attn_point:
+        line["ragged_attention"] = ragged_attention_point(ctx, hbm)
     if world == 1 and not args.no_cpu_baseline:
         # the GPU run's own per-step draft lengths (first timed generation)
         cb = cpu_reference(cfg, [s_.draft_length for s_ in results[0][0].steps],
