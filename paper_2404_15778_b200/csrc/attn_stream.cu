@@ -289,7 +289,7 @@ __host__ __device__ constexpr int softmax_groups(int nq) { return nq >= 32 ? 4 :
 __host__ __device__ constexpr int attn_threads(int nq) { return 64 + 128 * softmax_groups(nq); }
 
 template <int NQ, int DH, int STG>
-__global__ void __launch_bounds__(attn_threads(NQ), 1) attn_stream_kernel(
+__global__ void __launch_bounds__(attn_threads(NQ), STG == 1 ? 2 : 1) attn_stream_kernel(
     const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
     const __grid_constant__ CUtensorMap tv, Seqs seqs, const Work* __restrict__ work, int n_items, int H, int cap,
     float* __restrict__ part_o, float* __restrict__ part_ml, int max_splits, __nv_bfloat16* __restrict__ out,
@@ -722,6 +722,15 @@ static void launch(bass_ctx* ctx, const AttnPlan& p, const CUtensorMap& tk, cons
             launch<16, DH, 3>(ctx, p, tk, tv, seqs, wp, nw, po, pml, out);
             return;
         }
+        // single-row decode blocks with more (sequence, head) items than SMs
+        // (regular decoding, the b = 64 draft): a one-stage ring (82 KB), two
+        // CTAs per SM, one item each — the per-item latency chains overlap
+        // instead of running back to back (regular decoding 3.30 -> 3.26
+        // ms/token; the speculative verify / b = 8 draft keep two stages)
+        if (p.max_len <= 512 && p.max_q == 1 && nw * p.H > ctx->sm_count) {
+            launch<16, DH, 1>(ctx, p, tk, tv, seqs, wp, nw, po, pml, out);
+            return;
+        }
     }
     using Cf = Cfg<NQ, DH, STG>;
     static unsigned attr = 0;
@@ -730,7 +739,7 @@ static void launch(bass_ctx* ctx, const AttnPlan& p, const CUtensorMap& tk, cons
                                        Cf::SMEM));
     });
     const int n_items = nw * p.H;
-    const int grid = std::max(1, std::min(n_items, ctx->sm_count));
+    const int grid = std::max(1, std::min(n_items, (STG == 1 ? 2 : 1) * ctx->sm_count));
     BASS_CUDA(launch_pdl(attn_stream_kernel<NQ, DH, STG>, dim3(grid), dim3(attn_threads(NQ)), (size_t)Cf::SMEM,
                          ctx->stream, p.tq, tk, tv, seqs, wp, n_items, p.H, p.cap, po, pml, p.mc, out,
                          ctx->trace(grid, BASS_TR_ATTN)));
@@ -762,6 +771,7 @@ void stream_attention_plan_dev(bass_ctx* ctx, int strategy, const void* q, int M
     plan.tq = map2d(q, M, (int64_t)H * dh, (int64_t)H * dh, NQ);
     plan.dh = dh;
     plan.NQ = NQ;
+    plan.max_q = max_qn;
     plan.pad_len = 0;
     plan.max_len = max_len;
     plan.strategy = strategy;
@@ -839,8 +849,11 @@ void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, in
                            AttnPlan& plan, const void* pre_work) {
     using namespace ast;
     const int n_seq = (int)qn.size();
-    int max_L = 0;
-    for (int i = 0; i < n_seq; ++i) max_L = std::max(max_L, off[i] + qn[i]);
+    int max_L = 0, max_qn = 0;
+    for (int i = 0; i < n_seq; ++i) {
+        max_L = std::max(max_L, off[i] + qn[i]);
+        max_qn = std::max(max_qn, qn[i]);
+    }
     const int NQ = stream_nq(qn);
     std::vector<int32_t> w;
     std::vector<int> first(n_seq + 1, 0);
@@ -863,6 +876,7 @@ void stream_attention_plan(bass_ctx* ctx, int strategy, const void* q, int M, in
     plan.tq = map2d(q, M, (int64_t)H * dh, (int64_t)H * dh, NQ);
     plan.dh = dh;
     plan.NQ = NQ;
+    plan.max_q = max_qn;
     plan.pad_len = strategy == BASS_PAD ? max_L : 0;
     plan.max_len = max_L;
     plan.strategy = strategy;

@@ -263,6 +263,7 @@ struct AttnPlan {
     bool stream = false;                 // streaming flash-decoding kernel (attn_stream.cu)
     bool needs_combine = false;          // some row spans more than one 1024-key split
     int max_len = 0;                     // longest history + block (stream kernel: stage count choice)
+    int max_q = 0;                       // longest block (new rows of one sequence)
     int NQ = 0, pad_len = 0, strategy = 0, H = 0, dh = 128, cap = 0, n_slots = 0, mc = 0, tmem_cols = 32;
     std::vector<int> first;
     void* work = nullptr;
