@@ -217,3 +217,31 @@ def test_attention_tile_classes_long_histories(ctx, q_max):
         w = want[i].transpose(1, 0, 2)
         err = np.abs(got[cu[i]:cu[i + 1]] - w).max() / np.abs(w).max()
         assert err < 1e-2, err
+
+
+def test_attention_decode_two_ctas_per_sm(ctx):
+    """Single-row decode blocks with more (sequence, head) items than SMs and
+    histories <= 512 run the one-stage ring at two CTAs per SM (RAGGED / PAD:
+    8 x 36 = 288 items); SPLIT launches one sequence (36 items) at a time on
+    the two-stage build — bitwise equal, and within 1e-2 of the oracle."""
+    import torch
+    from paper_2404_15778_b200 import attend_device
+    rng = np.random.default_rng(11)
+    H, dh = 36, 128
+    q_lens = [1] * 8
+    kv = [int(rng.integers(2, 512)) for _ in q_lens]
+    kv[3] = 1   # a history of the new row alone
+    qs = [rng.standard_normal((H, 1, dh)) for _ in q_lens]
+    ks = [rng.standard_normal((H, n, dh)) for n in kv]
+    vs = [rng.standard_normal((H, n, dh)) for n in kv]
+    offs = [n - 1 for n in kv]
+    Q, K, Vv, cu = _workload_to_device(qs, ks, vs, torch.bfloat16)
+    outs = [attend_device(ctx, Q, K, Vv, cu, offs, s) for s in ("pad", "split", "ragged")]
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+    r = lambda a: torch.tensor(a).bfloat16().double().numpy()
+    want = OR.attend_split([r(q) for q in qs], [r(k) for k in ks], [r(v) for v in vs], offs)
+    got = outs[2].double().cpu().numpy()
+    for i in range(len(q_lens)):
+        w = want[i].transpose(1, 0, 2)
+        err = np.abs(got[cu[i]:cu[i + 1]] - w).max() / np.abs(w).max()
+        assert err < 1e-2, err
