@@ -120,8 +120,10 @@ BASS_DEV int aligned_override(const DraftPick& d, int slot, int pos, int V, int 
 // columns [p V/P, (p+1) V/P), parks it, and the row's last-arriving CTA
 // combines the P partials (max value, then first index — order-free, so the
 // result equals a single scan's bit for bit) and writes the proposal.
-// `cnt` [rows] must be zero; the last CTA re-arms it.
-constexpr int GREEDY_PARTS = 16;
+// `cnt` [rows] must be zero; the last CTA re-arms it.  P = 8 (64 CTAs for
+// b = 8; 16 / 32 / 4 / 2 measured equal or slower in the C2 chain,
+// profiles/r2/greedy_parts_ab.txt).
+constexpr int GREEDY_PARTS = 8;
 static __global__ void __launch_bounds__(256) draft_greedy_split_kernel(const float* __restrict__ logits, int V,
                                                                         DraftPick d, float* __restrict__ pv,
                                                                         int* __restrict__ pi, int* __restrict__ cnt) {
