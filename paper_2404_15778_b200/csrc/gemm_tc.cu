@@ -1072,10 +1072,13 @@ struct LaunchArgs {
 template <int TT, int MODE, bool PACKED, int LNF, bool I8 = false, bool SER = false, int STG = 0>
 static void launch_k(bass_model& m, const LaunchArgs& a, const Epi& e) {
     constexpr int NB = 1;   // (NB = 2 measured slower at every benchmark shape: profiles/r1_gemm_nb_split_sweep.txt)
-    using C = Cfg<TT, NB, STG>;
+    // serial split-K at 256-token tiles: 512 TMEM columns hold one CTA per
+    // SM, so its ring takes four 48 KB stages instead of the two-CTA budget
+    constexpr int STG_ = (SER && TT == 256) ? 4 : STG;
+    using C = Cfg<TT, NB, STG_>;
     static unsigned attr = 0;
     once_per_device(attr, [] {
-        BASS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<TT, MODE, NB, PACKED, LNF, I8, SER, STG>,
+        BASS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<TT, MODE, NB, PACKED, LNF, I8, SER, STG_>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     });
     cudaLaunchConfig_t cfg = {};
@@ -1093,7 +1096,7 @@ static void launch_k(bass_model& m, const LaunchArgs& a, const Epi& e) {
     cfg.attrs = at;
     cfg.numAttrs = (a.sp.S > 1 && !SER) ? 2 : 1;
     const int nblk = (int)(cfg.gridDim.x * cfg.gridDim.y * cfg.gridDim.z);
-    BASS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TT, MODE, NB, PACKED, LNF, I8, SER, STG>, *a.wm, *a.xm,
+    BASS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<TT, MODE, NB, PACKED, LNF, I8, SER, STG_>, *a.wm, *a.xm,
                                  (const __nv_bfloat16*)a.W, a.M, a.N, a.sp, e, a.xn,
                                  m.ctx->trace(nblk, BASS_TR_GEMM)));
 }
@@ -1197,6 +1200,11 @@ void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N
     const bool ser = sp.S > 1 && sp.S <= 4 && M > 256 && packed;
     if (ser) {
         TT = sp.S <= 4 ? 128 : 64;   // S accumulators of TT columns in 512 TMEM columns
+        // two splits, at least two 256-row token groups and no more padding
+        // than 128-row groups: 256-token tiles (two 256-column accumulators,
+        // one CTA per SM, a 4-stage 192 KB ring) read each weight tile half
+        // as often from L2 (prefill QKV; prompt prefill 8 x 128 20.7 -> 20.3 ms)
+        if (sp.S <= 2 && !i8 && M >= 512 && (M + 255) / 256 * 256 <= (M + 127) / 128 * 128) TT = 256;
         const auto xk2 = std::make_tuple(X, M, i8 ? -K : K, TT);
         auto x2 = S.xmaps.find(xk2);
         if (x2 == S.xmaps.end()) x2 = S.xmaps.emplace(xk2, make_map(X, M, K, TT, i8)).first;
@@ -1216,6 +1224,7 @@ void tc_gemm(bass_model& m, int mode, const void* X, const void* W, int M, int N
     const bool xnb = norm != nullptr;
     if (ser) {
         if (TT == 128) launch_mode<128, true>(m, mode, packed, xnb, a, e);
+        else if (TT == 256) launch_mode<256, true>(m, mode, packed, xnb, a, e);
         else launch_mode<64, true>(m, mode, packed, xnb, a, e);
     } else switch (TT) {
         case 16: launch_mode<16>(m, mode, packed, xnb, a, e); break;

@@ -48,19 +48,21 @@ def test_tc_gemm_rows_bitwise_independent_of_m(handle):
         assert torch.equal(part, full[:m]), m
 
 
-@pytest.mark.parametrize("N,K", [(4608, 4608), (4608, 18432), (13824, 4608), (2048, 8192)])
-def test_serial_split_k_prefill_rows_bitwise_equal_clustered(handle, N, K):
+@pytest.mark.parametrize("N,K,M", [(4608, 4608, 1100), (4608, 18432, 1100), (13824, 4608, 1100),
+                                   (2048, 8192, 1100), (13824, 4608, 1024)])
+def test_serial_split_k_prefill_rows_bitwise_equal_clustered(handle, N, K, M):
     """Prefill-sized M (> 256 rows) runs the serial split-K kernel: one CTA per
     (token group, tile), the S partials accumulated one after another and
     summed in split order — the same bits as the clustered split-K that
-    decode / verify blocks use (so prompt rows and later rows agree)."""
+    decode / verify blocks use (so prompt rows and later rows agree).  M = 1024
+    with two splits takes the 256-token serial tiles."""
     import torch
     from paper_2404_15778_b200 import _lib as L
     g = torch.Generator(device="cuda").manual_seed(N + K)
-    x = torch.randn(1100, K, device="cuda", generator=g).bfloat16()
+    x = torch.randn(M, K, device="cuda", generator=g).bfloat16()
     w = (torch.randn(N, K, device="cuda", generator=g) * 0.02).bfloat16()
     full = handle.gemm(x, w, 3)              # packed weights, M > 256: serial split-K
-    for lo, hi in ((0, 200), (300, 500), (1000, 1100)):
+    for lo, hi in ((0, 200), (300, 500), (M - 100, M)):
         part = handle.gemm(x[lo:hi].contiguous(), w, 3)   # M <= 256: clustered split-K
         assert torch.equal(part, full[lo:hi]), (lo, hi)
     ref = x.float() @ w.float().T
